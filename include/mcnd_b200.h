@@ -1,0 +1,109 @@
+/*
+ * mcnd_b200 -- C ABI of the B200-native matrix-condensation log-determinant.
+ *
+ * Drop-in boundary for the reference package `mcnd` (pure Python/numpy; it
+ * has no FFI of its own).  Each entry point replaces one reference call; the
+ * Python mirror (paper_1811_08057_b200/condense.py, runtime.py) binds them via
+ * ctypes exactly as INTEGRATION.md shows.  Plain pointers and sizes only.
+ *
+ * Conventions
+ *   - matrices are row-major float64 with a leading dimension (elements);
+ *   - `*_dev` entry points take DEVICE pointers and a cudaStream_t (as void*);
+ *     the others take HOST pointers and perform the host<->device copies
+ *     inside the call (pinned memory makes them asynchronous DMA);
+ *   - return 0 on success, otherwise an MCND_E* code; mcnd_last_error()
+ *     gives a thread-local message.  A singular matrix is a VALUE
+ *     (sign 0, log_abs -inf), never an error, as in condense.py:153-158;
+ *   - the caller's matrix is never modified (condense.py:72, runtime.py:139).
+ */
+#ifndef MCND_B200_H
+#define MCND_B200_H
+
+#include <stdint.h>
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MCND_OK 0
+#define MCND_EINVAL 1        /* bad shape / argument  -> Python ValueError       */
+#define MCND_ECUDA 2         /* CUDA runtime failure  -> RuntimeError            */
+#define MCND_ENCCL 3         /* NCCL failure          -> RuntimeError            */
+#define MCND_EDEVICE 4       /* device-side timeout / protocol error             */
+#define MCND_EPIVOT 5        /* pivot_sequence names an inactive row (ValueError) */
+#define MCND_EPIVOT_SHORT 6  /* pivot_sequence shorter than n-1 (IndexError)      */
+
+/* flags */
+#define MCND_FLAG_FAST 1u     /* fused multiply-add update (default: reference-exact
+                                 multiply-then-subtract, bitwise equal to numpy)   */
+
+/* Result of one log-determinant (mirrors mcnd.LogDet, condense.py:36-43). */
+typedef struct mcnd_logdet {
+    int32_t sign;            /* +1 / -1, 0 = singular                            */
+    int32_t singular;        /* 1 if singular                                    */
+    double log_abs;          /* ln|det|, -inf if singular                        */
+    int64_t singular_step;   /* step whose pivot failed the witness test, or -1 */
+    int64_t invalid_step;    /* first invalid pivot_sequence step, or -1        */
+    int64_t invalid_row;     /* the offending row id (MCND_EPIVOT)              */
+    double device_ms;        /* device time of the condensation (CUDA events)   */
+    int64_t steps;           /* condensation steps executed                      */
+} mcnd_logdet;
+
+/* Communication accounting of the block-row driver (runtime.py:47-66). */
+typedef struct mcnd_comm_stats {
+    int64_t broadcasts;
+    int64_t broadcast_bytes;
+    int64_t pivot_search_msgs;
+    int64_t scalar_updates;
+    int64_t aborted_step;    /* -1 if no abort */
+} mcnd_comm_stats;
+
+/* ---- serial condensation: replaces mcnd.logdet_condensation (condense.py:134) ----
+ * pivot_sequence: optional HOST array of >= n-1 original row ids (condense.py:147-152),
+ *                 NULL = top-to-bottom.  pivots_out / cols_out: optional HOST arrays
+ *                 of n entries receiving each step's pivot value / column (the
+ *                 last entry is the final 1x1). */
+int mcnd_logdet_condensation_dev(const double* d_a, int64_t n, int64_t lda,
+                                 const int64_t* pivot_sequence, int64_t pivot_sequence_len,
+                                 uint32_t flags, void* stream, mcnd_logdet* out,
+                                 double* pivots_out, int32_t* cols_out);
+int mcnd_logdet_condensation(const double* h_a, int64_t n, int64_t lda,
+                             const int64_t* pivot_sequence, int64_t pivot_sequence_len,
+                             uint32_t flags, void* stream, mcnd_logdet* out,
+                             double* pivots_out, int32_t* cols_out);
+
+/* ---- block-row parallel condensation: replaces mcnd.mc_parallel(a, p) (runtime.py:123) ----
+ * One GPU runs the exact p-worker schedule (round-robin owners, topmost live row,
+ * runtime.py:153-204) and the p x p LU tail (runtime.py:206-219).
+ * payload_entries: optional HOST array of n-p entries; row_updates: optional HOST
+ * array of p entries; owners_out: optional HOST array (n-p) of the owner per step. */
+int mcnd_mc_parallel_dev(const double* d_a, int64_t n, int64_t lda, int32_t p, uint32_t flags,
+                         void* stream, mcnd_logdet* out, mcnd_comm_stats* stats,
+                         int64_t* payload_entries, int64_t* row_updates, int32_t* owners_out);
+int mcnd_mc_parallel(const double* h_a, int64_t n, int64_t lda, int32_t p, uint32_t flags,
+                     void* stream, mcnd_logdet* out, mcnd_comm_stats* stats,
+                     int64_t* payload_entries, int64_t* row_updates, int32_t* owners_out);
+
+/* ---- batched: one CTA per small matrix (no reference counterpart; oracle = a loop
+ * of logdet_condensation).  d_sign/d_log_abs: DEVICE outputs (batch entries);
+ * d_pivots: optional DEVICE batch x n pivot values (for bitwise checks). n <= 128. */
+int mcnd_logdet_batched_dev(const double* d_a, int64_t batch, int64_t n, int64_t stride,
+                            uint32_t flags, void* stream, int32_t* d_sign, double* d_log_abs,
+                            double* d_pivots);
+/* host in / host out */
+int mcnd_logdet_batched(const double* h_a, int64_t batch, int64_t n, int64_t stride,
+                        uint32_t flags, void* stream, int32_t* h_sign, double* h_log_abs);
+
+/* ---- introspection ---- */
+const char* mcnd_last_error(void);
+int32_t mcnd_version(void);
+/* Number of CTAs the persistent condensation kernel runs with on the current device. */
+int32_t mcnd_k1_grid(void);
+/* Free the library's cached device workspace and pinned staging buffers. */
+void mcnd_release_workspace(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MCND_B200_H */

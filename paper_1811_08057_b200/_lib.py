@@ -1,0 +1,97 @@
+"""ctypes binding of libmcnd_b200.so (include/mcnd_b200.h).
+
+There is no CPU fallback: if the library is missing or no CUDA device is
+usable, every entry point raises.  The reference (`mcnd`) has no FFI; this is
+the binding its Python callers get.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+from .build import LIB
+
+MCND_OK = 0
+MCND_EINVAL = 1
+MCND_ECUDA = 2
+MCND_ENCCL = 3
+MCND_EDEVICE = 4
+MCND_EPIVOT = 5
+MCND_EPIVOT_SHORT = 6
+FLAG_FAST = 1
+
+
+class McndLogDet(ctypes.Structure):
+    _fields_ = [("sign", ctypes.c_int32), ("singular", ctypes.c_int32), ("log_abs", ctypes.c_double),
+                ("singular_step", ctypes.c_int64), ("invalid_step", ctypes.c_int64),
+                ("invalid_row", ctypes.c_int64), ("device_ms", ctypes.c_double), ("steps", ctypes.c_int64)]
+
+
+class McndCommStats(ctypes.Structure):
+    _fields_ = [("broadcasts", ctypes.c_int64), ("broadcast_bytes", ctypes.c_int64),
+                ("pivot_search_msgs", ctypes.c_int64), ("scalar_updates", ctypes.c_int64),
+                ("aborted_step", ctypes.c_int64)]
+
+
+_lock = threading.Lock()
+_lib = None
+
+EXPORTS = (
+    "mcnd_logdet_condensation_dev", "mcnd_logdet_condensation",
+    "mcnd_mc_parallel_dev", "mcnd_mc_parallel",
+    "mcnd_logdet_batched_dev", "mcnd_logdet_batched",
+    "mcnd_last_error", "mcnd_version", "mcnd_k1_grid", "mcnd_release_workspace",
+)
+
+
+def load(path: str | None = None):
+    """Load (never build) the shared library and declare its signatures."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        path = path or LIB
+        if not os.path.exists(path):
+            raise RuntimeError(
+                f"libmcnd_b200.so not found at {path}: run __graft_entry__.build() "
+                "(there is no CPU fallback)")
+        lib = ctypes.CDLL(path)
+        P, i64, i32, u32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_uint32
+        LD = ctypes.POINTER(McndLogDet)
+        CS = ctypes.POINTER(McndCommStats)
+        for name in ("mcnd_logdet_condensation_dev", "mcnd_logdet_condensation"):
+            f = getattr(lib, name)
+            f.argtypes = [P, i64, i64, P, i64, u32, P, LD, P, P]
+            f.restype = ctypes.c_int
+        for name in ("mcnd_mc_parallel_dev", "mcnd_mc_parallel"):
+            f = getattr(lib, name)
+            f.argtypes = [P, i64, i64, i32, u32, P, LD, CS, P, P, P]
+            f.restype = ctypes.c_int
+        lib.mcnd_logdet_batched_dev.argtypes = [P, i64, i64, i64, u32, P, P, P, P]
+        lib.mcnd_logdet_batched_dev.restype = ctypes.c_int
+        lib.mcnd_logdet_batched.argtypes = [P, i64, i64, i64, u32, P, P, P]
+        lib.mcnd_logdet_batched.restype = ctypes.c_int
+        lib.mcnd_last_error.argtypes = []
+        lib.mcnd_last_error.restype = ctypes.c_char_p
+        lib.mcnd_version.restype = ctypes.c_int32
+        lib.mcnd_k1_grid.restype = ctypes.c_int32
+        lib.mcnd_release_workspace.restype = None
+        _lib = lib
+        return lib
+
+
+def last_error() -> str:
+    return load().mcnd_last_error().decode(errors="replace")
+
+
+def check(rc: int) -> None:
+    if rc == MCND_OK:
+        return
+    msg = last_error()
+    if rc in (MCND_EINVAL, MCND_EPIVOT):
+        raise ValueError(msg)
+    if rc == MCND_EPIVOT_SHORT:
+        raise IndexError(msg)
+    raise RuntimeError(f"mcnd_b200 error {rc}: {msg}")

@@ -1,0 +1,358 @@
+// K1: persistent, barrier-free matrix-condensation kernel for sm_100a.
+//
+// Restates condense_step / logdet_condensation (mcnd/condense.py:82-160) and
+// the worker update of mc_parallel (mcnd/runtime.py:157-203) as ONE
+// cooperative launch with one 1024-thread CTA per SM.
+//
+// Data layout (HBM): the caller's matrix is copied once into a workspace of
+// n rows x ld doubles (ld = n rounded up to 16, so every row starts on a
+// 128-byte line).  Condensation is IN PLACE and never moves rows: step s
+// drops the pivot row, and the column exchange l <-> m-1 of condense.py:104-107
+// is folded into the read pattern (column l of the result reads old column
+// m-1), so the active block is always columns [0, m) of the live rows.
+//
+// Work split: rows are dealt cyclically to CTAs in pivot order, so the live
+// rows (a suffix of the pivot order) stay balanced for any pivot sequence
+// (this is the paper's arbitrary-pivot-row property).  Each
+// CTA updates only its own rows, so the only cross-CTA data is the pivot row.
+//
+// Dataflow instead of grid barriers: the CTA that owns the pivot row of step
+// s+1 updates that row FIRST in step s, reduces its argmax (ties -> lowest
+// column, condense.py:88), runs the witness test (condense.py:90), writes the
+// scaled, column-permuted pivot row (condense.py:110-111) back into the row
+// itself and publishes (value, column) with a release store of a counter.
+// Every CTA waits only for "pivot s published" before step s, so pivot
+// selection runs one step ahead of the bulk update (lookahead) and there is no
+// grid-wide barrier anywhere.
+//
+// Arithmetic: parity mode uses __dmul_rn then __dsub_rn (two roundings, exactly
+// numpy's `sub -= col[:,None]*prow`, condense.py:118) and true division for
+// the pivot row; fast mode uses one FMA.  The running row witness
+// (condense.py:120-122) is fused into the same pass as a per-segment warp max
+// folded into shared memory with a 64-bit atomicMax on the bit pattern.
+#include <cstdint>
+#include <climits>
+#include "mcnd_internal.h"
+
+namespace mcnd {
+namespace {
+
+constexpr int kThreads = kK1Threads;
+constexpr int kWarps = kThreads / 32;
+constexpr int kU = 4;                   // double2 per lane per segment
+constexpr int kSegPairs = 32 * kU;      // 128 pairs = 256 doubles = 2 KB per warp segment
+constexpr unsigned kFull = 0xffffffffu;
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+template <bool kFast>
+__device__ __forceinline__ double upd(double x, double mult, double p) {
+    if (kFast) return fma(-mult, p, x);
+    return __dsub_rn(x, __dmul_rn(mult, p));
+}
+
+// (value, column) argmax order: larger |value| wins, ties -> lower column.
+__device__ __forceinline__ bool beats(double av, int ai, double bv, int bi) {
+    double fa = fabs(av), fb = fabs(bv);
+    return fa > fb || (fa == fb && ai < bi);
+}
+
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(kFull, v, o));
+    return v;
+}
+
+struct Smem {
+    int rows[kK1MaxRowsPerCta];
+    int pstep[kK1MaxRowsPerCta];
+    unsigned long long wit[kK1MaxRowsPerCta];  // non-negative doubles as u64 (order-preserving)
+    double mult[kK1MaxRowsPerCta];             // a[r][l]   (multiplier, old pivot column)
+    double last[kK1MaxRowsPerCta];             // a[r][m-1] (moves into column l)
+    double red_v[kWarps + 1];
+    double red_w[kWarps + 1];
+    int red_i[kWarps + 1];
+    int step_l;
+};
+
+// Whole-CTA reduction of (argmax value, column) and witness max.  Every thread
+// returns the CTA result.
+__device__ __forceinline__ void cta_reduce(Smem& sm, double& v, int& i, double& w) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        double ov = __shfl_xor_sync(kFull, v, o);
+        int oi = __shfl_xor_sync(kFull, i, o);
+        double ow = __shfl_xor_sync(kFull, w, o);
+        if (beats(ov, oi, v, i)) { v = ov; i = oi; }
+        w = fmax(w, ow);
+    }
+    if (lane == 0) { sm.red_v[warp] = v; sm.red_i[warp] = i; sm.red_w[warp] = w; }
+    __syncthreads();
+    if (warp == 0) {
+        v = sm.red_v[lane]; i = sm.red_i[lane]; w = sm.red_w[lane];
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            double ov = __shfl_xor_sync(kFull, v, o);
+            int oi = __shfl_xor_sync(kFull, i, o);
+            double ow = __shfl_xor_sync(kFull, w, o);
+            if (beats(ov, oi, v, i)) { v = ov; i = oi; }
+            w = fmax(w, ow);
+        }
+        if (lane == 0) { sm.red_v[kWarps] = v; sm.red_i[kWarps] = i; sm.red_w[kWarps] = w; }
+    }
+    __syncthreads();
+    v = sm.red_v[kWarps]; i = sm.red_i[kWarps]; w = sm.red_w[kWarps];
+}
+
+// Publish pivot t from row `rowp` whose active width is m_pub (values already
+// final in global memory and visible CTA-wide).  Writes the scaled pivot row
+// prow[c] = row[sigma(c)] / v, c < m_pub-1, into the row itself (the row is
+// dead after pivot t, so nobody else ever touches its storage), then releases
+// the counter.  Whole CTA.
+template <bool kFast>
+__device__ void publish(const K1Params& p, Smem& sm, double* rowp, int t, int m_pub, double v,
+                        int l, double wit) {
+    const bool singular = !(fabs(v) > kSingularRtol * wit);  // condense.py:90
+    const int wp = m_pub - 1;
+    if (!singular && wp > 0) {
+        const double ylast = rowp[wp];
+        for (int c = threadIdx.x; c < wp; c += kThreads) {
+            double x = (c == l) ? ylast : rowp[c];
+            rowp[c] = __ddiv_rn(x, v);  // condense.py:110 (true division)
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        p.piv_val[t] = v;
+        p.piv_col[t] = singular ? -1 : l;
+        p.piv_wit[t] = wit;
+        __threadfence();
+        st_release_u32(&p.ctrl->published, (unsigned)t + 1u);
+    }
+}
+
+template <bool kFast>
+__global__ void __launch_bounds__(kThreads, 1) k1_condense(const K1Params p) {
+    extern __shared__ __align__(16) double s_prow[];
+    __shared__ Smem sm;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int n = p.n;
+    const int rbeg = p.cta_row_ptr[blockIdx.x];
+    const int nr = p.cta_row_ptr[blockIdx.x + 1] - rbeg;
+    for (int i = tid; i < nr; i += kThreads) {
+        const int r = p.cta_rows[rbeg + i];
+        sm.rows[i] = r;
+        sm.pstep[i] = p.row_pstep[r];
+        sm.wit[i] = 0ull;
+    }
+    __syncthreads();
+
+    // ---- prologue: copy my rows into the workspace + initial witness (condense.py:72-78)
+    {
+        constexpr int kSeg = 256;
+        const int nseg = (n + kSeg - 1) / kSeg;
+        const int total = nr * nseg;
+        for (int j = warp; j < total; j += kWarps) {
+            const int i = j / nseg, sg = j - i * nseg;
+            const int r = sm.rows[i];
+            const double* src = p.src + (int64_t)r * p.lds;
+            double* dst = p.ws + (int64_t)r * p.ld;
+            const int c0 = sg * kSeg + lane;
+            double x[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const int c = c0 + 32 * k;
+                x[k] = (c < n) ? __ldg(src + c) : 0.0;
+            }
+            double wm = 0.0;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const int c = c0 + 32 * k;
+                if (c < n) { dst[c] = x[k]; wm = fmax(wm, fabs(x[k])); }
+            }
+            wm = warp_max(wm);
+            if (lane == 0) atomicMax(&sm.wit[i], (unsigned long long)__double_as_longlong(wm));
+        }
+    }
+    __syncthreads();
+
+    // ---- pivot 0 (its row was just copied by this CTA)
+    if (nr > 0 && sm.pstep[0] == 0) {
+        double* rowp = p.ws + (int64_t)sm.rows[0] * p.ld;
+        double bv = 0.0, bw = 0.0;
+        int bi = INT_MAX;
+        for (int c = tid; c < n; c += kThreads) {
+            const double x = rowp[c];
+            if (beats(x, c, bv, bi)) { bv = x; bi = c; }
+        }
+        cta_reduce(sm, bv, bi, bw);
+        publish<kFast>(p, sm, rowp, 0, n, bv, bi, __longlong_as_double((long long)sm.wit[0]));
+    }
+
+    int start = 0;  // first live local row
+    for (int s = 0; s < p.n_steps; ++s) {
+        const int m = n - s, w = m - 1;
+        // ---- wait for pivot s
+        if (tid == 0) {
+            int l = -2;
+            const unsigned long long t0 = globaltimer();
+            for (;;) {
+                if (ld_acquire_u32(&p.ctrl->published) > (unsigned)s) {
+                    l = __ldcg(p.piv_col + s);
+                    break;
+                }
+                if (*(volatile unsigned*)&p.ctrl->error) break;
+                if (globaltimer() - t0 > p.timeout_ns) {
+                    atomicExch(&p.ctrl->error, 1u);
+                    atomicExch(&p.ctrl->err_step, (unsigned)s);
+                    break;
+                }
+                __nanosleep(32);
+            }
+            sm.step_l = l;
+        }
+        __syncthreads();
+        const int l = sm.step_l;
+        if (l < 0) break;  // singular (-1) or error (-2): everybody stops
+        while (start < nr && sm.pstep[start] <= s) ++start;
+
+        // ---- stage multipliers / last column of my live rows, and chunk 0 of the pivot row
+        const double* prow_g = p.ws + (int64_t)__ldg(p.seq + s) * p.ld;
+        for (int i = start + tid; i < nr; i += kThreads) {
+            const double* rp = p.ws + (int64_t)sm.rows[i] * p.ld;
+            sm.mult[i] = rp[l];
+            sm.last[i] = rp[w];
+        }
+        const int cw0 = w < p.chunk ? w : p.chunk;
+        for (int c = tid; c < cw0; c += kThreads) s_prow[c] = __ldcg(prow_g + c);
+        if (tid == 0 && (cw0 & 1)) s_prow[cw0] = 0.0;
+        __syncthreads();
+
+        int bulk_first = start;
+        // ---- lookahead: I own the next pivot row -> update it first with the whole CTA
+        if (start < nr && sm.pstep[start] == s + 1) {
+            bulk_first = start + 1;
+            double* rowp = p.ws + (int64_t)sm.rows[start] * p.ld;
+            const double mult = sm.mult[start], lastv = sm.last[start];
+            const int npairs = (w + 1) >> 1;
+            double bv = 0.0, bw = 0.0;
+            int bi = INT_MAX;
+            for (int pj = tid; pj < npairs; pj += kThreads) {
+                const int c = 2 * pj;
+                double2 x = *reinterpret_cast<const double2*>(rowp + c);
+                if (c == l) x.x = lastv;
+                if (c + 1 == l) x.y = lastv;
+                double p0, p1;
+                if (c < cw0) { p0 = s_prow[c]; p1 = s_prow[c + 1]; }
+                else { p0 = __ldcg(prow_g + c); p1 = (c + 1 < w) ? __ldcg(prow_g + c + 1) : 0.0; }
+                double2 y;
+                y.x = upd<kFast>(x.x, mult, p0);
+                y.y = upd<kFast>(x.y, mult, p1);
+                *reinterpret_cast<double2*>(rowp + c) = y;
+                if (beats(y.x, c, bv, bi)) { bv = y.x; bi = c; }
+                bw = fmax(bw, fabs(y.x));
+                if (c + 1 < w) {
+                    if (beats(y.y, c + 1, bv, bi)) { bv = y.y; bi = c + 1; }
+                    bw = fmax(bw, fabs(y.y));
+                }
+            }
+            cta_reduce(sm, bv, bi, bw);
+            const double wit = fmax(__longlong_as_double((long long)sm.wit[start]), bw);
+            publish<kFast>(p, sm, rowp, s + 1, w, bv, bi, wit);
+            if (tid == 0) sm.wit[start] = (unsigned long long)__double_as_longlong(wit);
+        }
+
+        // ---- bulk update of my other live rows, chunk by chunk
+        for (int c0 = 0; c0 < w; c0 += p.chunk) {
+            const int cend = (c0 + p.chunk < w) ? c0 + p.chunk : w;
+            if (c0 > 0) {
+                __syncthreads();
+                const int clen = cend - c0;
+                for (int c = tid; c < clen; c += kThreads) s_prow[c] = __ldcg(prow_g + c0 + c);
+                if (tid == 0 && (clen & 1)) s_prow[clen] = 0.0;
+                __syncthreads();
+            }
+            const int npairs = (cend - c0 + 1) >> 1;
+            const int nseg = (npairs + kSegPairs - 1) / kSegPairs;
+            const int total = (nr - bulk_first) * nseg;
+            for (int j = warp; j < total; j += kWarps) {
+                const int ii = j / nseg, sg = j - ii * nseg;
+                const int i = bulk_first + ii;
+                double* rowp = p.ws + (int64_t)sm.rows[i] * p.ld + c0;
+                const double mult = sm.mult[i], lastv = sm.last[i];
+                const int pj0 = sg * kSegPairs + lane;
+                double2 x[kU];
+#pragma unroll
+                for (int k = 0; k < kU; ++k) {
+                    const int pj = pj0 + 32 * k;
+                    if (pj < npairs) x[k] = *reinterpret_cast<const double2*>(rowp + 2 * pj);
+                }
+                double wm = 0.0;
+#pragma unroll
+                for (int k = 0; k < kU; ++k) {
+                    const int pj = pj0 + 32 * k;
+                    if (pj < npairs) {
+                        const int c = c0 + 2 * pj;
+                        if (c == l) x[k].x = lastv;
+                        if (c + 1 == l) x[k].y = lastv;
+                        const double2 pv = *reinterpret_cast<const double2*>(s_prow + 2 * pj);
+                        double2 y;
+                        y.x = upd<kFast>(x[k].x, mult, pv.x);
+                        y.y = upd<kFast>(x[k].y, mult, pv.y);
+                        *reinterpret_cast<double2*>(rowp + 2 * pj) = y;
+                        wm = fmax(wm, fabs(y.x));
+                        if (c + 1 < w) wm = fmax(wm, fabs(y.y));
+                    }
+                }
+                wm = warp_max(wm);
+                if (lane == 0) atomicMax(&sm.wit[i], (unsigned long long)__double_as_longlong(wm));
+            }
+        }
+        __syncthreads();  // smem (prow chunk, mult/last) is restaged next step
+    }
+
+    __syncthreads();
+    for (int i = tid; i < nr; i += kThreads)
+        p.row_wit[sm.rows[i]] = __longlong_as_double((long long)sm.wit[i]);
+}
+
+}  // namespace
+
+size_t k1_smem_bytes(int chunk) { return (size_t)(chunk + 2) * sizeof(double); }
+
+int k1_max_grid(int device) {
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    return sms;
+}
+
+cudaError_t k1_launch(const K1Params& p, int grid, bool fast, cudaStream_t s) {
+    const size_t smem = k1_smem_bytes(p.chunk);
+    const void* fn = fast ? (const void*)k1_condense<true> : (const void*)k1_condense<false>;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, smem);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) return cudaErrorInvalidConfiguration;
+    K1Params pc = p;
+    void* args[] = {&pc};
+    // Cooperative launch guarantees co-residency of all CTAs, which the
+    // publish/wait dataflow between CTAs relies on.
+    return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kThreads), args, smem, s);
+}
+
+}  // namespace mcnd
