@@ -37,6 +37,10 @@ extern "C" {
 /* flags */
 #define MCND_FLAG_FAST 1u     /* fused multiply-add update (default: reference-exact
                                  multiply-then-subtract, bitwise equal to numpy)   */
+#define MCND_FLAG_GROUPS 2u   /* mc_parallel only: run the p workers as p CTA groups with
+                                 separate workspaces on one GPU, exchanging pivot rows
+                                 through the same push protocol the multi-GPU driver uses
+                                 over NVLink (p <= 8)                               */
 
 /* Result of one log-determinant (mirrors mcnd.LogDet, condense.py:36-43). */
 typedef struct mcnd_logdet {
@@ -84,6 +88,34 @@ int mcnd_mc_parallel_dev(const double* d_a, int64_t n, int64_t lda, int32_t p, u
 int mcnd_mc_parallel(const double* h_a, int64_t n, int64_t lda, int32_t p, uint32_t flags,
                      void* stream, mcnd_logdet* out, mcnd_comm_stats* stats,
                      int64_t* payload_entries, int64_t* row_updates, int32_t* owners_out);
+
+/* Fold per-step pivots and the p x p remainder of the block-row driver into the
+ * reference's result and accounting (runtime.py:185-229): sign parity, per-worker
+ * log sums reduced in rank order, row-pivoted LU tail (gauss.py:34-68).
+ * piv_vals/piv_cols: n-p (or singular_at+1) entries; rem: p x p row-major (row w =
+ * worker w's last live row); rem_wit: p witnesses; singular_at: -1 or the pivot that
+ * failed the witness test. */
+int mcnd_fold_mc_parallel(int64_t n, int32_t p, const double* piv_vals, const int32_t* piv_cols,
+                          int64_t singular_at, const double* rem, const double* rem_wit, mcnd_logdet* out,
+                          mcnd_comm_stats* stats, int64_t* payload_entries, int64_t* row_updates);
+
+/* ---- multi-GPU block-row driver, one process per GPU (replaces the in-process
+ * _Fabric of runtime.py:69-120 with stores into peer memory over NVLink) ----
+ * 1. mcnd_dist_create on every rank (current device = the rank's GPU) -> handle and an
+ *    opaque IPC handle of mcnd_dist_ipc_handle_bytes() bytes;
+ * 2. all-gather the IPC handles (any host transport), mcnd_dist_connect(all handles);
+ * 3. mcnd_dist_mc_parallel with this rank's block rows (plan_blocks(n, world), DEVICE
+ *    pointer, row stride lda): returns every pivot (all ranks receive all of them),
+ *    this rank's remaining row (first `world` columns) and its witness;
+ * 4. all-gather the remaining rows; mcnd_fold_mc_parallel gives the result.
+ * n must equal n_max.  world <= 8. */
+int32_t mcnd_dist_ipc_handle_bytes(void);
+int mcnd_dist_create(int32_t rank, int32_t world, int64_t n_max, void** handle, void* ipc_out);
+int mcnd_dist_connect(void* handle, const void* ipc_all);
+int mcnd_dist_mc_parallel(void* handle, const double* d_rows, int64_t n, int64_t lda, uint32_t flags,
+                          void* stream, double* piv_vals, int32_t* piv_cols, int64_t* singular_at,
+                          double* rem_row, double* rem_wit, double* device_ms);
+void mcnd_dist_destroy(void* handle);
 
 /* ---- batched: one CTA per small matrix (no reference counterpart; oracle = a loop
  * of logdet_condensation).  d_sign/d_log_abs: DEVICE outputs (batch entries);

@@ -40,7 +40,7 @@ def _load():
     i64, i32 = ctypes.c_int64, ctypes.c_int
     lib.oracle_logdet_condensation.argtypes = [P, i64, P, i32, P, P, P, P, P, P]
     lib.oracle_logdet_lu.argtypes = [P, i64, P, P, P]
-    lib.oracle_mc_parallel.argtypes = [P, i64, i64, i32, P, P, P, P, P, P, P, P]
+    lib.oracle_mc_parallel.argtypes = [P, i64, i64, i32, P, P, P, P, P, P, P, P, P, P]
     lib.oracle_logdet_batched.argtypes = [P, i64, i64, i32, P, P]
     lib.oracle_condense_steps.argtypes = [P, i64, P, i32, P, P, P, P, P, P, i64]
     lib.oracle_condense_steps.restype = ctypes.c_int
@@ -123,6 +123,8 @@ class OracleParallel(NamedTuple):
     owners: np.ndarray
     pivots: np.ndarray
     cols: np.ndarray
+    rem: np.ndarray          # p x p remainder (row w = worker w's last live row)
+    rem_wit: np.ndarray      # its witnesses
 
 
 def mc_parallel(a, p: int, threads: int = 0) -> OracleParallel:
@@ -139,13 +141,16 @@ def mc_parallel(a, p: int, threads: int = 0) -> OracleParallel:
     owners = np.full(max(n - p + 1, 1), -1, dtype=np.int64)
     piv = np.zeros(max(n - p + 1, 1), dtype=np.float64)
     cols = np.zeros(max(n - p + 1, 1), dtype=np.int32)
+    rem = np.zeros((p, p), dtype=np.float64)
+    rem_wit = np.zeros(p, dtype=np.float64)
     lib.oracle_mc_parallel(_ptr(a), n, p, threads, ctypes.byref(sign), ctypes.byref(la), _ptr(stats),
-                           _ptr(payload), _ptr(rows), _ptr(owners), _ptr(piv), _ptr(cols))
+                           _ptr(payload), _ptr(rows), _ptr(owners), _ptr(piv), _ptr(cols), _ptr(rem),
+                           _ptr(rem_wit))
     aborted = int(stats[3])
     n_bcast_payload = (aborted if aborted >= 0 else n - p)
     return OracleParallel(int(sign.value), float(la.value), int(stats[0]), int(stats[1]),
                           int(stats[2]), aborted, [int(x) for x in payload[:n_bcast_payload]],
-                          [int(x) for x in rows], owners, piv, cols)
+                          [int(x) for x in rows], owners, piv, cols, rem, rem_wit)
 
 
 def logdet_batched(a3, threads: int = 0):

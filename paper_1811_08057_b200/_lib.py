@@ -21,6 +21,7 @@ MCND_EDEVICE = 4
 MCND_EPIVOT = 5
 MCND_EPIVOT_SHORT = 6
 FLAG_FAST = 1
+FLAG_GROUPS = 2
 
 
 class McndLogDet(ctypes.Structure):
@@ -41,7 +42,9 @@ _lib = None
 EXPORTS = (
     "mcnd_logdet_condensation_dev", "mcnd_logdet_condensation",
     "mcnd_mc_parallel_dev", "mcnd_mc_parallel",
-    "mcnd_logdet_batched_dev", "mcnd_logdet_batched",
+    "mcnd_logdet_batched_dev", "mcnd_logdet_batched", "mcnd_fold_mc_parallel",
+    "mcnd_dist_ipc_handle_bytes", "mcnd_dist_create", "mcnd_dist_connect", "mcnd_dist_mc_parallel",
+    "mcnd_dist_destroy",
     "mcnd_last_error", "mcnd_version", "mcnd_k1_grid", "mcnd_release_workspace",
 )
 
@@ -73,6 +76,18 @@ def load(path: str | None = None):
         lib.mcnd_logdet_batched_dev.restype = ctypes.c_int
         lib.mcnd_logdet_batched.argtypes = [P, i64, i64, i64, u32, P, P, P]
         lib.mcnd_logdet_batched.restype = ctypes.c_int
+        lib.mcnd_fold_mc_parallel.argtypes = [i64, i32, P, P, i64, P, P, LD, CS, P, P]
+        lib.mcnd_fold_mc_parallel.restype = ctypes.c_int
+        lib.mcnd_dist_ipc_handle_bytes.argtypes = []
+        lib.mcnd_dist_ipc_handle_bytes.restype = ctypes.c_int32
+        lib.mcnd_dist_create.argtypes = [i32, i32, i64, ctypes.POINTER(ctypes.c_void_p), P]
+        lib.mcnd_dist_create.restype = ctypes.c_int
+        lib.mcnd_dist_connect.argtypes = [P, P]
+        lib.mcnd_dist_connect.restype = ctypes.c_int
+        lib.mcnd_dist_mc_parallel.argtypes = [P, P, i64, i64, u32, P, P, P, P, P, P, P]
+        lib.mcnd_dist_mc_parallel.restype = ctypes.c_int
+        lib.mcnd_dist_destroy.argtypes = [P]
+        lib.mcnd_dist_destroy.restype = None
         lib.mcnd_last_error.argtypes = []
         lib.mcnd_last_error.restype = ctypes.c_char_p
         lib.mcnd_version.restype = ctypes.c_int32

@@ -33,7 +33,7 @@ from typing import NamedTuple, Optional, Sequence
 import numpy as np
 
 from . import _lib
-from .matrix import require_square
+from .matrix import square_for_device
 
 SINGULAR_RTOL = 1e-12  # condense.py:29
 
@@ -69,10 +69,11 @@ def _torch_device_args(a):
         a = a.to(torch.float64)
     if a.stride(1) != 1 or a.stride(0) < a.shape[1]:
         a = a.contiguous()
-    if not bool(torch.isfinite(a).all()):
-        raise ValueError("matrix entries must be finite (no NaN/Inf)")
     if a.shape[0] != a.shape[1]:
+        if not bool(torch.isfinite(a).all()):
+            raise ValueError("matrix entries must be finite (no NaN/Inf)")
         raise ValueError(f"matrix must be square, got {tuple(a.shape)}")
+    # finiteness (matrix.py:39-40) is checked on the device, fused into the copy
     torch.cuda.set_device(a.device)
     stream = torch.cuda.current_stream(a.device).cuda_stream
     return a, a.data_ptr(), a.shape[0], a.stride(0), stream
@@ -101,7 +102,7 @@ def logdet_condensation(a, pivot_sequence: Optional[Sequence[int]] = None, *, fa
             ctypes.byref(out), piv.ctypes.data, cols.ctypes.data)
         del keep
     else:
-        a = require_square(a)
+        a = square_for_device(a)
         n = a.shape[0]
         seq, slen = _seq_array(pivot_sequence, n)
         piv = np.zeros(n, dtype=np.float64)

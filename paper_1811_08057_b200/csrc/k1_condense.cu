@@ -1,10 +1,10 @@
 // K1: persistent, barrier-free matrix-condensation kernel for sm_100a.
 //
 // Restates condense_step / logdet_condensation (mcnd/condense.py:82-160) and
-// the worker update of mc_parallel (mcnd/runtime.py:157-203) as ONE
+// the block-row worker update of mc_parallel (mcnd/runtime.py:157-203) as ONE
 // cooperative launch with one 1024-thread CTA per SM.
 //
-// Data layout (HBM): the caller's matrix is copied once into a workspace of
+// Data layout (HBM): the caller's rows are copied once into a workspace of
 // n rows x ld doubles (ld = n rounded up to 16, so every row starts on a
 // 128-byte line).  Condensation is IN PLACE and never moves rows: step s
 // drops the pivot row, and the column exchange l <-> m-1 of condense.py:104-107
@@ -13,23 +13,25 @@
 //
 // Work split: rows are dealt cyclically to CTAs in pivot order, so the live
 // rows (a suffix of the pivot order) stay balanced for any pivot sequence
-// (this is the paper's arbitrary-pivot-row property).  Each
-// CTA updates only its own rows, so the only cross-CTA data is the pivot row.
+// (the paper's arbitrary-pivot-row property).  Each CTA
+// updates only its own rows, so the only cross-CTA data is the pivot row.
 //
 // Dataflow instead of grid barriers: the CTA that owns the pivot row of step
 // s+1 updates that row FIRST in step s, reduces its argmax (ties -> lowest
 // column, condense.py:88), runs the witness test (condense.py:90), writes the
-// scaled, column-permuted pivot row (condense.py:110-111) back into the row
-// itself and publishes (value, column) with a release store of a counter.
-// Every CTA waits only for "pivot s published" before step s, so pivot
-// selection runs one step ahead of the bulk update (lookahead) and there is no
-// grid-wide barrier anywhere.
+// scaled, column-permuted pivot row (condense.py:110-111) into the row's slot
+// of every group's workspace -- the "broadcast" of runtime.py:185, done as
+// stores into peer memory over NVLink when groups are other GPUs -- and then
+// release-stores the pivot record's flag.  Every CTA waits only for "pivot s
+// published" before step s, so pivot selection runs one step ahead of the bulk
+// update (lookahead) and there is no grid- or job-wide barrier anywhere.
 //
 // Arithmetic: parity mode uses __dmul_rn then __dsub_rn (two roundings, exactly
 // numpy's `sub -= col[:,None]*prow`, condense.py:118) and true division for
 // the pivot row; fast mode uses one FMA.  The running row witness
 // (condense.py:120-122) is fused into the same pass as a per-segment warp max
-// folded into shared memory with a 64-bit atomicMax on the bit pattern.
+// folded into shared memory with a 64-bit atomicMax on the bit pattern.  The
+// finiteness check of matrix.py:39-40 is fused into the prologue copy.
 #include <cstdint>
 #include <climits>
 #include "mcnd_internal.h"
@@ -43,13 +45,15 @@ constexpr int kU = 4;                   // double2 per lane per segment
 constexpr int kSegPairs = 32 * kU;      // 128 pairs = 256 doubles = 2 KB per warp segment
 constexpr unsigned kFull = 0xffffffffu;
 
-__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+__device__ __forceinline__ unsigned ld_acquire_flag(const uint32_t* p, bool sys) {
     unsigned v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    if (sys) asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    else asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
-__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
-    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+__device__ __forceinline__ void st_release_flag(uint32_t* p, unsigned v, bool sys) {
+    if (sys) asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+    else asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 __device__ __forceinline__ unsigned long long globaltimer() {
     unsigned long long t;
@@ -117,30 +121,33 @@ __device__ __forceinline__ void cta_reduce(Smem& sm, double& v, int& i, double& 
     v = sm.red_v[kWarps]; i = sm.red_i[kWarps]; w = sm.red_w[kWarps];
 }
 
-// Publish pivot t from row `rowp` whose active width is m_pub (values already
-// final in global memory and visible CTA-wide).  Writes the scaled pivot row
-// prow[c] = row[sigma(c)] / v, c < m_pub-1, into the row itself (the row is
-// dead after pivot t, so nobody else ever touches its storage), then releases
-// the counter.  Whole CTA.
-template <bool kFast>
-__device__ void publish(const K1Params& p, Smem& sm, double* rowp, int t, int m_pub, double v,
-                        int l, double wit) {
+// Publish pivot t of global row `row` (active width m_pub; its values are final
+// in this group's workspace and visible CTA-wide).  Writes the scaled pivot
+// row prow[c] = row[sigma(c)] / v, c < m_pub-1, into that row's slot of every
+// group's workspace (the row is dead after pivot t, so nobody else ever
+// touches those slots), then the record, then the release flag.  Whole CTA.
+__device__ void publish(const K1Params& p, Smem& sm, int g, int row, int t, int m_pub, double v, int l,
+                        double wit) {
     const bool singular = !(fabs(v) > kSingularRtol * wit);  // condense.py:90
     const int wp = m_pub - 1;
+    const bool sys = p.sys_scope != 0;
+    double* own = p.ws[g] + (int64_t)row * p.ld;
     if (!singular && wp > 0) {
-        const double ylast = rowp[wp];
+        const double ylast = own[wp];
         for (int c = threadIdx.x; c < wp; c += kThreads) {
-            double x = (c == l) ? ylast : rowp[c];
-            rowp[c] = __ddiv_rn(x, v);  // condense.py:110 (true division)
+            const double y = __ddiv_rn((c == l) ? ylast : own[c], v);  // condense.py:110 (true division)
+            for (int h = 0; h < p.n_groups; ++h) p.ws[h][(int64_t)row * p.ld + c] = y;
         }
     }
+    if (sys) __threadfence_system();
     __syncthreads();
     if (threadIdx.x == 0) {
-        p.piv_val[t] = v;
-        p.piv_col[t] = singular ? -1 : l;
-        p.piv_wit[t] = wit;
-        __threadfence();
-        st_release_u32(&p.ctrl->published, (unsigned)t + 1u);
+        for (int h = 0; h < p.n_groups; ++h) {
+            p.rec[h][t].v = v;
+            p.rec[h][t].l = singular ? -1 : l;
+        }
+        if (sys) __threadfence_system(); else __threadfence();
+        for (int h = 0; h < p.n_groups; ++h) st_release_flag(&p.rec[h][t].flag, p.epoch, sys);
     }
 }
 
@@ -150,6 +157,11 @@ __global__ void __launch_bounds__(kThreads, 1) k1_condense(const K1Params p) {
     __shared__ Smem sm;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int n = p.n;
+    const int gl = blockIdx.x / p.ctas_per_group;  // local group
+    const int g = p.group0 + gl;                   // global group (worker / rank)
+    double* const ws = p.ws[g];
+    PivRec* const rec = p.rec[g];
+    const bool sys = p.sys_scope != 0;
     const int rbeg = p.cta_row_ptr[blockIdx.x];
     const int nr = p.cta_row_ptr[blockIdx.x + 1] - rbeg;
     for (int i = tid; i < nr; i += kThreads) {
@@ -160,16 +172,18 @@ __global__ void __launch_bounds__(kThreads, 1) k1_condense(const K1Params p) {
     }
     __syncthreads();
 
-    // ---- prologue: copy my rows into the workspace + initial witness (condense.py:72-78)
+    // ---- prologue: copy my rows into the workspace, initial witness (condense.py:72-78)
+    //      and the finiteness check (matrix.py:39-40)
     {
         constexpr int kSeg = 256;
         const int nseg = (n + kSeg - 1) / kSeg;
         const int total = nr * nseg;
+        bool bad = false;
         for (int j = warp; j < total; j += kWarps) {
             const int i = j / nseg, sg = j - i * nseg;
             const int r = sm.rows[i];
-            const double* src = p.src + (int64_t)r * p.lds;
-            double* dst = p.ws + (int64_t)r * p.ld;
+            const double* src = p.src[gl] + (r - p.src_row0[gl]) * p.lds;
+            double* dst = ws + (int64_t)r * p.ld;
             const int c0 = sg * kSeg + lane;
             double x[8];
 #pragma unroll
@@ -181,17 +195,22 @@ __global__ void __launch_bounds__(kThreads, 1) k1_condense(const K1Params p) {
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
                 const int c = c0 + 32 * k;
-                if (c < n) { dst[c] = x[k]; wm = fmax(wm, fabs(x[k])); }
+                if (c < n) {
+                    dst[c] = x[k];
+                    wm = fmax(wm, fabs(x[k]));
+                    bad |= !isfinite(x[k]);
+                }
             }
             wm = warp_max(wm);
             if (lane == 0) atomicMax(&sm.wit[i], (unsigned long long)__double_as_longlong(wm));
         }
+        if (__any_sync(kFull, bad) && lane == 0) atomicOr(&p.err->nonfinite, 1u);
     }
     __syncthreads();
 
     // ---- pivot 0 (its row was just copied by this CTA)
     if (nr > 0 && sm.pstep[0] == 0) {
-        double* rowp = p.ws + (int64_t)sm.rows[0] * p.ld;
+        double* rowp = ws + (int64_t)sm.rows[0] * p.ld;
         double bv = 0.0, bw = 0.0;
         int bi = INT_MAX;
         for (int c = tid; c < n; c += kThreads) {
@@ -199,7 +218,7 @@ __global__ void __launch_bounds__(kThreads, 1) k1_condense(const K1Params p) {
             if (beats(x, c, bv, bi)) { bv = x; bi = c; }
         }
         cta_reduce(sm, bv, bi, bw);
-        publish<kFast>(p, sm, rowp, 0, n, bv, bi, __longlong_as_double((long long)sm.wit[0]));
+        publish(p, sm, g, sm.rows[0], 0, n, bv, bi, __longlong_as_double((long long)sm.wit[0]));
     }
 
     int start = 0;  // first live local row
@@ -210,14 +229,14 @@ __global__ void __launch_bounds__(kThreads, 1) k1_condense(const K1Params p) {
             int l = -2;
             const unsigned long long t0 = globaltimer();
             for (;;) {
-                if (ld_acquire_u32(&p.ctrl->published) > (unsigned)s) {
-                    l = __ldcg(p.piv_col + s);
+                if (ld_acquire_flag(&rec[s].flag, sys) == p.epoch) {
+                    l = *(volatile const int32_t*)&rec[s].l;
                     break;
                 }
-                if (*(volatile unsigned*)&p.ctrl->error) break;
+                if (*(volatile unsigned*)&p.err->error) break;
                 if (globaltimer() - t0 > p.timeout_ns) {
-                    atomicExch(&p.ctrl->error, 1u);
-                    atomicExch(&p.ctrl->err_step, (unsigned)s);
+                    atomicExch(&p.err->error, 1u);
+                    atomicExch(&p.err->err_step, (unsigned)s);
                     break;
                 }
                 __nanosleep(32);
@@ -230,9 +249,9 @@ __global__ void __launch_bounds__(kThreads, 1) k1_condense(const K1Params p) {
         while (start < nr && sm.pstep[start] <= s) ++start;
 
         // ---- stage multipliers / last column of my live rows, and chunk 0 of the pivot row
-        const double* prow_g = p.ws + (int64_t)__ldg(p.seq + s) * p.ld;
+        const double* prow_g = ws + (int64_t)__ldg(p.seq + s) * p.ld;
         for (int i = start + tid; i < nr; i += kThreads) {
-            const double* rp = p.ws + (int64_t)sm.rows[i] * p.ld;
+            const double* rp = ws + (int64_t)sm.rows[i] * p.ld;
             sm.mult[i] = rp[l];
             sm.last[i] = rp[w];
         }
@@ -245,7 +264,7 @@ __global__ void __launch_bounds__(kThreads, 1) k1_condense(const K1Params p) {
         // ---- lookahead: I own the next pivot row -> update it first with the whole CTA
         if (start < nr && sm.pstep[start] == s + 1) {
             bulk_first = start + 1;
-            double* rowp = p.ws + (int64_t)sm.rows[start] * p.ld;
+            double* rowp = ws + (int64_t)sm.rows[start] * p.ld;
             const double mult = sm.mult[start], lastv = sm.last[start];
             const int npairs = (w + 1) >> 1;
             double bv = 0.0, bw = 0.0;
@@ -271,7 +290,7 @@ __global__ void __launch_bounds__(kThreads, 1) k1_condense(const K1Params p) {
             }
             cta_reduce(sm, bv, bi, bw);
             const double wit = fmax(__longlong_as_double((long long)sm.wit[start]), bw);
-            publish<kFast>(p, sm, rowp, s + 1, w, bv, bi, wit);
+            publish(p, sm, g, sm.rows[start], s + 1, w, bv, bi, wit);
             if (tid == 0) sm.wit[start] = (unsigned long long)__double_as_longlong(wit);
         }
 
@@ -291,7 +310,7 @@ __global__ void __launch_bounds__(kThreads, 1) k1_condense(const K1Params p) {
             for (int j = warp; j < total; j += kWarps) {
                 const int ii = j / nseg, sg = j - ii * nseg;
                 const int i = bulk_first + ii;
-                double* rowp = p.ws + (int64_t)sm.rows[i] * p.ld + c0;
+                double* rowp = ws + (int64_t)sm.rows[i] * p.ld + c0;
                 const double mult = sm.mult[i], lastv = sm.last[i];
                 const int pj0 = sg * kSegPairs + lane;
                 double2 x[kU];
@@ -326,20 +345,14 @@ __global__ void __launch_bounds__(kThreads, 1) k1_condense(const K1Params p) {
 
     __syncthreads();
     for (int i = tid; i < nr; i += kThreads)
-        p.row_wit[sm.rows[i]] = __longlong_as_double((long long)sm.wit[i]);
+        p.row_wit[gl][sm.rows[i]] = __longlong_as_double((long long)sm.wit[i]);
 }
 
 }  // namespace
 
 size_t k1_smem_bytes(int chunk) { return (size_t)(chunk + 2) * sizeof(double); }
 
-int k1_max_grid(int device) {
-    int sms = 0;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-    return sms;
-}
-
-cudaError_t k1_launch(const K1Params& p, int grid, bool fast, cudaStream_t s) {
+cudaError_t k1_launch(const K1Params& p, bool fast, cudaStream_t s) {
     const size_t smem = k1_smem_bytes(p.chunk);
     const void* fn = fast ? (const void*)k1_condense<true> : (const void*)k1_condense<false>;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -350,6 +363,7 @@ cudaError_t k1_launch(const K1Params& p, int grid, bool fast, cudaStream_t s) {
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
     K1Params pc = p;
     void* args[] = {&pc};
+    const int grid = p.n_local_groups * p.ctas_per_group;
     // Cooperative launch guarantees co-residency of all CTAs, which the
     // publish/wait dataflow between CTAs relies on.
     return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kThreads), args, smem, s);

@@ -7,8 +7,9 @@
 // sign bookkeeping (condense.py:125-128, runtime.py:179-182), the sequential
 // log sum (condense.py:124; runtime.py:114-120 rank-ordered reduce), the p x p
 // elimination tail of the block-row driver (runtime.py:206-219 ->
-// gauss.py:34-68) and the communication accounting (runtime.py:47-66,
-// 82-90).  The GPU does all O(N^3) work; the host touches O(N) numbers.
+// gauss.py:34-68), the communication accounting (runtime.py:47-66, 82-90) and
+// the multi-GPU plumbing (CUDA IPC mappings of every rank's workspace).
+// The GPU does all O(N^3) work; the host touches O(N) numbers.
 //
 // Compiled with -ffp-contract=off: the tail LU must round exactly like numpy.
 #include <cuda_runtime.h>
@@ -49,17 +50,32 @@ int fail(int code, const char* fmt, ...) {
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
+long env_long(const char* name, long dflt) {
+    const char* v = std::getenv(name);
+    if (!v || !*v) return dflt;
+    return std::strtol(v, nullptr, 10);
+}
+
 // ---- cached device/pinned buffers (one set per device; calls are serialised) ----
 struct Buffers {
     int device = -1;
-    void* dws = nullptr;   size_t dws_bytes = 0;    // condensation workspace
+    void* dws = nullptr;   size_t dws_bytes = 0;    // condensation workspace(s) + records + metadata
     void* din = nullptr;   size_t din_bytes = 0;    // H2D staging for host-input calls
     void* hpin = nullptr;  size_t hpin_bytes = 0;   // pinned metadata / result staging
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     int sms = 0;
+    uint32_t epoch = 0;
 };
 std::mutex g_mu;
 std::deque<Buffers> g_bufs;
+
+int init_buffers(Buffers& b, int dev) {
+    b.device = dev;
+    cudaDeviceGetAttribute(&b.sms, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaEventCreate(&b.ev0) != cudaSuccess || cudaEventCreate(&b.ev1) != cudaSuccess)
+        return fail(MCND_ECUDA, "cudaEventCreate failed");
+    return MCND_OK;
+}
 
 Buffers* buffers_for_current(int* code) {
     int dev = 0;
@@ -67,12 +83,7 @@ Buffers* buffers_for_current(int* code) {
     if (e != cudaSuccess) { *code = fail(MCND_ECUDA, "cudaGetDevice: %s", cudaGetErrorString(e)); return nullptr; }
     for (auto& b : g_bufs) if (b.device == dev) return &b;
     Buffers b;
-    b.device = dev;
-    cudaDeviceGetAttribute(&b.sms, cudaDevAttrMultiProcessorCount, dev);
-    if (cudaEventCreate(&b.ev0) != cudaSuccess || cudaEventCreate(&b.ev1) != cudaSuccess) {
-        *code = fail(MCND_ECUDA, "cudaEventCreate failed");
-        return nullptr;
-    }
+    if ((*code = init_buffers(b, dev)) != MCND_OK) return nullptr;
     g_bufs.push_back(b);
     return &g_bufs.back();
 }
@@ -99,148 +110,269 @@ int ensure_pinned(void** p, size_t* have, size_t need) {
     return MCND_OK;
 }
 
+// ---- schedules ----
+struct Blocks {  // plan_blocks (runtime.py:33-44)
+    std::vector<int64_t> start, len;
+    int32_t group_of(int64_t r) const {
+        for (size_t w = 0; w < start.size(); ++w) if (r < start[w] + len[w]) return (int32_t)w;
+        return (int32_t)start.size() - 1;
+    }
+};
+
+Blocks plan_blocks(int64_t n, int32_t p) {
+    Blocks b;
+    const int64_t base = n / p, extra = n % p;
+    int64_t s0 = 0;
+    for (int32_t w = 0; w < p; ++w) {
+        b.start.push_back(s0);
+        b.len.push_back(base + (w < extra ? 1 : 0));
+        s0 += b.len.back();
+    }
+    return b;
+}
+
+// Round-robin owner schedule of mc_parallel (runtime.py:153-156): each pass
+// visits workers in rank order, skipping those with <= 1 live row; the owner's
+// pivot row is its topmost live row.  n - p steps.
+void round_robin(const Blocks& b, std::vector<int32_t>* seq, std::vector<int32_t>* owner) {
+    const int32_t p = (int32_t)b.start.size();
+    std::vector<int64_t> consumed((size_t)p, 0);
+    for (;;) {
+        bool any = false;
+        for (int32_t w = 0; w < p; ++w) any |= (b.len[(size_t)w] - consumed[(size_t)w] > 1);
+        if (!any) break;
+        for (int32_t w = 0; w < p; ++w) {
+            if (b.len[(size_t)w] - consumed[(size_t)w] <= 1) continue;
+            seq->push_back((int32_t)(b.start[(size_t)w] + consumed[(size_t)w]));
+            owner->push_back(w);
+            consumed[(size_t)w] += 1;
+        }
+    }
+}
+
 // ---- K1 plan and run ----
 struct K1Run {
-    // inputs
     int64_t n = 0;
     int64_t steps = 0;              // S
-    std::vector<int32_t> seq;       // S (+1 if a final 1x1 pivot is published)
-    // outputs
-    std::vector<double> piv_val;    // seq.size()
+    std::vector<int32_t> seq;       // S (+1 when a final 1x1 pivot is published)
+    std::vector<double> piv_val;    // outputs, seq.size()
     std::vector<int32_t> piv_col;
-    std::vector<double> row_wit;    // n (only when want_wit)
     int64_t singular_at = -1;       // pivot index with failed witness test
     double device_ms = 0.0;
 };
 
-// Runs the persistent condensation on device matrix d_a.  If keep_rows is
-// non-null, copies rows keep_rows[i] (first keep_cols columns) of the final
-// workspace to keep_out (row-major).
-int k1_run(Buffers& B, const double* d_a, int64_t n, int64_t lda, bool fast, cudaStream_t st,
-           K1Run& run, bool want_wit, const std::vector<int32_t>* keep_rows, int64_t keep_cols,
-           std::vector<double>* keep_out) {
-    const int64_t S = run.steps;
-    const int64_t npiv = (int64_t)run.seq.size();
-    const int64_t ld = (int64_t)align_up((size_t)n, 16);
-    int64_t G = std::min<int64_t>(B.sms, n);
-    if (const char* eg = std::getenv("MCND_K1_GRID")) {  // test knob: fewer CTAs, more rows per CTA
-        const long v = std::strtol(eg, nullptr, 10);
-        if (v > 0) G = std::min<int64_t>(G, v);
-    }
-    if (G < 1) G = 1;
-    if ((n + G - 1) / G > kK1MaxRowsPerCta)
-        return fail(MCND_EINVAL, "n=%lld exceeds the single-GPU limit (%d rows per SM)", (long long)n,
-                    kK1MaxRowsPerCta);
+// Per-group workspace layout: [matrix n x ld][records npv][row_wit n]
+struct GroupLayout {
+    int64_t ld = 0;
+    size_t o_rec = 0, o_wit = 0, bytes = 0;
+};
 
-    // pivot index of every row, rows dealt cyclically to CTAs in pivot order
-    std::vector<int32_t> pstep((size_t)n, kNever);
-    for (int64_t t = 0; t < npiv; ++t) pstep[(size_t)run.seq[(size_t)t]] = (int32_t)t;
+GroupLayout group_layout(int64_t n, int64_t npv) {
+    GroupLayout L;
+    L.ld = (int64_t)align_up((size_t)n, 16);
+    size_t off = align_up((size_t)n * L.ld * sizeof(double), 256);
+    L.o_rec = off;
+    off = align_up(off + (size_t)npv * sizeof(PivRec), 256);
+    L.o_wit = off;
+    off = align_up(off + (size_t)n * sizeof(double), 256);
+    L.bytes = off;
+    return L;
+}
+
+// Rows of each local group dealt cyclically over its CTAs, ascending pivot index.
+void deal_rows(int64_t n, const std::vector<int32_t>& seq, const std::vector<int32_t>& row_group,
+               int32_t group0, int32_t n_local, int32_t cpg, std::vector<int32_t>* pstep,
+               std::vector<int32_t>* row_ptr, std::vector<int32_t>* rows) {
+    pstep->assign((size_t)n, kNever);
+    for (size_t t = 0; t < seq.size(); ++t) (*pstep)[(size_t)seq[t]] = (int32_t)t;
     std::vector<int32_t> order;
     order.reserve((size_t)n);
-    for (int64_t t = 0; t < npiv; ++t) order.push_back(run.seq[(size_t)t]);
-    for (int64_t r = 0; r < n; ++r) if (pstep[(size_t)r] == kNever) order.push_back((int32_t)r);
-    std::vector<int32_t> row_ptr((size_t)G + 1, 0), rows((size_t)n);
-    for (int64_t g = 0; g < G; ++g) row_ptr[(size_t)g + 1] = row_ptr[(size_t)g] + (int32_t)((n - g + G - 1) / G);
-    {
-        std::vector<int32_t> fill(row_ptr.begin(), row_ptr.end() - 1);
-        for (int64_t i = 0; i < n; ++i) rows[(size_t)fill[(size_t)(i % G)]++] = order[(size_t)i];
+    for (int32_t r : seq) order.push_back(r);
+    for (int64_t r = 0; r < n; ++r) if ((*pstep)[(size_t)r] == kNever) order.push_back((int32_t)r);
+    std::vector<std::vector<int32_t>> per_cta((size_t)n_local * cpg);
+    std::vector<int64_t> dealt((size_t)n_local, 0);
+    for (int32_t r : order) {
+        const int32_t g = row_group[(size_t)r] - group0;
+        if (g < 0 || g >= n_local) continue;
+        per_cta[(size_t)g * cpg + (size_t)(dealt[(size_t)g]++ % cpg)].push_back(r);
     }
+    row_ptr->assign(per_cta.size() + 1, 0);
+    rows->clear();
+    for (size_t c = 0; c < per_cta.size(); ++c) {
+        (*row_ptr)[c + 1] = (*row_ptr)[c] + (int32_t)per_cta[c].size();
+        rows->insert(rows->end(), per_cta[c].begin(), per_cta[c].end());
+    }
+}
 
-    // device workspace layout
-    const size_t npv = (size_t)std::max<int64_t>(npiv, 1);
-    size_t off = 0;
-    auto take = [&](size_t bytes) { size_t o = off; off = align_up(off + bytes, 256); return o; };
-    const size_t o_mat = take((size_t)n * ld * sizeof(double));
-    const size_t o_int = take((npv + (size_t)n + (size_t)G + 1 + (size_t)n) * sizeof(int32_t));
-    const size_t o_pv = take(npv * sizeof(double));
-    const size_t o_pw = take(npv * sizeof(double));
-    const size_t o_pc = take(npv * sizeof(int32_t));
-    const size_t o_rw = take((size_t)n * sizeof(double));
-    const size_t o_ctl = take(sizeof(K1Ctrl));
-    int rc = ensure_dev(&B.dws, &B.dws_bytes, off);
-    if (rc) return rc;
-    char* base = (char*)B.dws;
+// Launch description shared by the single-process and multi-process paths.
+struct K1Launch {
+    int64_t n = 0, lda = 0;
+    int32_t n_groups = 1, group0 = 0, n_local = 1, cpg = 1;
+    bool sys = false;
+    uint32_t epoch = 1;
+    double* ws[kMaxGroups] = {};
+    PivRec* rec[kMaxGroups] = {};
+    double* wit[kMaxGroups] = {};         // local groups
+    const double* src[kMaxGroups] = {};   // local groups
+    int64_t src_row0[kMaxGroups] = {};
+    std::vector<int32_t> row_group;       // group of every row
+    void* d_meta = nullptr;               // device metadata area
+    size_t meta_bytes = 0;
+    unsigned long long timeout_ns = 20ull * 1000000000ull;
+    bool reset_records = true;
+};
 
-    const size_t n_int = npv + (size_t)n + (size_t)G + 1 + (size_t)n;
-    const size_t h_need = std::max(n_int * sizeof(int32_t),
-                                   npv * (sizeof(double) + sizeof(int32_t)) + sizeof(K1Ctrl) + 64);
-    rc = ensure_pinned(&B.hpin, &B.hpin_bytes, std::max(h_need, (size_t)n * sizeof(double)) + 256);
+size_t meta_bytes_for(int64_t n, int64_t npv, int64_t ctas) {
+    return align_up((size_t)(npv + n + ctas + 1 + n) * sizeof(int32_t), 256) + align_up(sizeof(K1Err), 256);
+}
+
+// Uploads the schedule, launches K1, downloads the pivot records of the first
+// local group.  Leaves the stream synchronised.
+int k1_execute(Buffers& B, K1Launch& L, bool fast, cudaStream_t st, K1Run& run) {
+    const int64_t n = L.n;
+    const int64_t npiv = (int64_t)run.seq.size();
+    const int64_t npv = std::max<int64_t>(npiv, 1);
+    const int64_t ctas = (int64_t)L.n_local * L.cpg;
+
+    std::vector<int32_t> pstep, row_ptr, rows;
+    deal_rows(n, run.seq, L.row_group, L.group0, L.n_local, L.cpg, &pstep, &row_ptr, &rows);
+    for (int64_t c = 0; c < ctas; ++c)
+        if (row_ptr[(size_t)c + 1] - row_ptr[(size_t)c] > kK1MaxRowsPerCta)
+            return fail(MCND_EINVAL, "n=%lld needs more than %d rows per CTA on this device", (long long)n,
+                        kK1MaxRowsPerCta);
+
+    const size_t n_int = (size_t)(npv + n + ctas + 1 + n);
+    const size_t rec_bytes = (size_t)npv * sizeof(PivRec);
+    if (meta_bytes_for(n, npv, ctas) > L.meta_bytes) return fail(MCND_EINVAL, "metadata area too small");
+    int rc = ensure_pinned(&B.hpin, &B.hpin_bytes, std::max(n_int * sizeof(int32_t), rec_bytes + 256) + 256);
     if (rc) return rc;
     int32_t* hi = (int32_t*)B.hpin;
-    std::memset(hi, 0, npv * sizeof(int32_t));
+    std::memset(hi, 0, (size_t)npv * sizeof(int32_t));
     std::memcpy(hi, run.seq.data(), (size_t)npiv * sizeof(int32_t));
     std::memcpy(hi + npv, pstep.data(), (size_t)n * sizeof(int32_t));
-    std::memcpy(hi + npv + n, row_ptr.data(), ((size_t)G + 1) * sizeof(int32_t));
-    std::memcpy(hi + npv + n + G + 1, rows.data(), (size_t)n * sizeof(int32_t));
-    CUDA_TRY(cudaMemcpyAsync(base + o_int, hi, n_int * sizeof(int32_t), cudaMemcpyHostToDevice, st));
-    CUDA_TRY(cudaMemsetAsync(base + o_ctl, 0, sizeof(K1Ctrl), st));
+    std::memcpy(hi + npv + n, row_ptr.data(), (size_t)(ctas + 1) * sizeof(int32_t));
+    std::memcpy(hi + npv + n + ctas + 1, rows.data(), (size_t)n * sizeof(int32_t));
+    char* meta = (char*)L.d_meta;
+    const size_t o_err = align_up(n_int * sizeof(int32_t), 256);
+    CUDA_TRY(cudaMemcpyAsync(meta, hi, n_int * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemsetAsync(meta + o_err, 0, sizeof(K1Err), st));
+    if (L.reset_records)
+        for (int32_t g = 0; g < L.n_local; ++g)
+            CUDA_TRY(cudaMemsetAsync(L.rec[L.group0 + g], 0, rec_bytes, st));
 
     K1Params p{};
-    p.src = d_a;
-    p.lds = lda;
-    p.ws = (double*)(base + o_mat);
-    p.ld = ld;
+    for (int g = 0; g < kMaxGroups; ++g) {
+        p.src[g] = L.src[g];
+        p.src_row0[g] = L.src_row0[g];
+        p.ws[g] = L.ws[g];
+        p.rec[g] = L.rec[g];
+        p.row_wit[g] = L.wit[g];
+    }
+    p.lds = L.lda;
+    p.ld = (int64_t)align_up((size_t)n, 16);
     p.n = (int32_t)n;
-    p.n_steps = (int32_t)S;
-    int32_t* di = (int32_t*)(base + o_int);
+    p.n_steps = (int32_t)run.steps;
+    p.n_groups = L.n_groups;
+    p.group0 = L.group0;
+    p.n_local_groups = L.n_local;
+    p.ctas_per_group = L.cpg;
+    p.sys_scope = L.sys ? 1 : 0;
+    p.epoch = L.epoch;
+    int32_t* di = (int32_t*)meta;
     p.seq = di;
     p.row_pstep = di + npv;
     p.cta_row_ptr = di + npv + n;
-    p.cta_rows = di + npv + n + G + 1;
-    p.piv_val = (double*)(base + o_pv);
-    p.piv_wit = (double*)(base + o_pw);
-    p.piv_col = (int32_t*)(base + o_pc);
-    p.row_wit = (double*)(base + o_rw);
-    p.ctrl = (K1Ctrl*)(base + o_ctl);
-    p.chunk = (int32_t)std::min<int64_t>(align_up((size_t)n, 2), kK1MaxChunk);
-    if (const char* ec = std::getenv("MCND_K1_CHUNK")) {  // test knob: force multi-chunk staging
-        const long v = std::strtol(ec, nullptr, 10);
-        if (v >= 2 && v <= kK1MaxChunk) p.chunk = (int32_t)std::min<int64_t>(p.chunk, v & ~1L);
-    }
-    p.timeout_ns = 20ull * 1000000000ull;
+    p.cta_rows = di + npv + n + ctas + 1;
+    p.err = (K1Err*)(meta + o_err);
+    p.chunk = (int32_t)std::min<int64_t>((int64_t)align_up((size_t)n, 2), kK1MaxChunk);
+    const long ck = env_long("MCND_K1_CHUNK", 0);  // test knob: force multi-chunk staging
+    if (ck >= 2 && ck <= kK1MaxChunk) p.chunk = (int32_t)std::min<int64_t>(p.chunk, ck & ~1L);
+    p.timeout_ns = L.timeout_ns;
 
     CUDA_TRY(cudaEventRecord(B.ev0, st));
-    cudaError_t e = k1_launch(p, (int)G, fast, st);
+    cudaError_t e = k1_launch(p, fast, st);
     if (e != cudaSuccess) return fail(MCND_ECUDA, "condensation kernel launch: %s", cudaGetErrorString(e));
     CUDA_TRY(cudaEventRecord(B.ev1, st));
 
-    // results -> pinned host
     char* hp = (char*)B.hpin;
-    double* h_pv = (double*)hp;
-    int32_t* h_pc = (int32_t*)(hp + npv * sizeof(double));
-    K1Ctrl* h_ctl = (K1Ctrl*)(hp + align_up(npv * (sizeof(double) + sizeof(int32_t)), 16));
-    CUDA_TRY(cudaMemcpyAsync(h_pv, base + o_pv, npv * sizeof(double), cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaMemcpyAsync(h_pc, base + o_pc, npv * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaMemcpyAsync(h_ctl, base + o_ctl, sizeof(K1Ctrl), cudaMemcpyDeviceToHost, st));
-    if (want_wit) {
-        run.row_wit.resize((size_t)n);
-        CUDA_TRY(cudaMemcpyAsync(run.row_wit.data(), base + o_rw, (size_t)n * sizeof(double),
-                                 cudaMemcpyDeviceToHost, st));
-    }
-    if (keep_rows && keep_out) {
-        keep_out->assign(keep_rows->size() * (size_t)keep_cols, 0.0);
-        for (size_t i = 0; i < keep_rows->size(); ++i)
-            CUDA_TRY(cudaMemcpyAsync(keep_out->data() + i * keep_cols,
-                                     p.ws + (int64_t)(*keep_rows)[i] * ld, (size_t)keep_cols * sizeof(double),
-                                     cudaMemcpyDeviceToHost, st));
-    }
+    PivRec* h_rec = (PivRec*)hp;
+    K1Err* h_err = (K1Err*)(hp + align_up(rec_bytes, 64));
+    CUDA_TRY(cudaMemcpyAsync(h_rec, L.rec[L.group0], rec_bytes, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(h_err, meta + o_err, sizeof(K1Err), cudaMemcpyDeviceToHost, st));
     e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return fail(MCND_ECUDA, "condensation kernel: %s", cudaGetErrorString(e));
     float ms = 0.f;
     cudaEventElapsedTime(&ms, B.ev0, B.ev1);
     run.device_ms = ms;
-    if (h_ctl->error)
-        return fail(MCND_EDEVICE, "device timeout waiting for pivot %u (published %u)", h_ctl->err_step,
-                    h_ctl->published);
-    run.piv_val.assign(h_pv, h_pv + npiv);
-    run.piv_col.assign(h_pc, h_pc + npiv);
+    if (h_err->nonfinite) return fail(MCND_EINVAL, "matrix entries must be finite (no NaN/Inf)");
+    if (h_err->error) return fail(MCND_EDEVICE, "device timeout waiting for pivot %u", h_err->err_step);
+    run.piv_val.resize((size_t)npiv);
+    run.piv_col.resize((size_t)npiv);
     run.singular_at = -1;
-    const unsigned pub = h_ctl->published;
+    int64_t published = 0;
     for (int64_t t = 0; t < npiv; ++t) {
-        if (run.piv_col[(size_t)t] < 0) { run.singular_at = t; break; }
+        if (h_rec[t].flag != L.epoch) break;
+        run.piv_val[(size_t)t] = h_rec[t].v;
+        run.piv_col[(size_t)t] = h_rec[t].l;
+        ++published;
+        if (h_rec[t].l < 0) { run.singular_at = t; break; }
     }
-    if (run.singular_at < 0 && (int64_t)pub != npiv)
-        return fail(MCND_EDEVICE, "protocol error: %u of %lld pivots published", pub, (long long)npiv);
+    if (run.singular_at < 0 && published != npiv)
+        return fail(MCND_EDEVICE, "protocol error: %lld of %lld pivots published", (long long)published,
+                    (long long)npiv);
+    return MCND_OK;
+}
+
+// Single-process run: P groups (1 = plain single GPU; p > 1 = the p workers as
+// CTA groups with separate workspaces, exercising the multi-GPU push protocol).
+int k1_run_local(Buffers& B, const double* d_a, int64_t n, int64_t lda, bool fast, cudaStream_t st,
+                 K1Run& run, const Blocks* groups, const std::vector<int32_t>* keep_rows, int64_t keep_cols,
+                 std::vector<double>* keep_out, std::vector<double>* keep_wit) {
+    const int32_t P = groups ? (int32_t)groups->start.size() : 1;
+    if (P > kMaxGroups) return fail(MCND_EINVAL, "at most %d CTA groups", kMaxGroups);
+    const int64_t npv = std::max<int64_t>((int64_t)run.seq.size(), 1);
+    const GroupLayout GL = group_layout(n, npv);
+    int64_t cpg = P == 1 ? std::min<int64_t>(B.sms, n) : std::max<int64_t>(B.sms / P, 1);
+    const long eg = env_long("MCND_K1_GRID", 0);  // test knob: fewer CTAs, more rows per CTA
+    if (eg > 0) cpg = std::max<int64_t>(1, std::min<int64_t>(cpg, eg));
+    const size_t mb = meta_bytes_for(n, npv, P * cpg);
+    int rc = ensure_dev(&B.dws, &B.dws_bytes, (size_t)P * GL.bytes + mb);
+    if (rc) return rc;
+    char* base = (char*)B.dws;
+    K1Launch L;
+    L.n = n;
+    L.lda = lda;
+    L.n_groups = P;
+    L.group0 = 0;
+    L.n_local = P;
+    L.cpg = (int32_t)cpg;
+    L.sys = false;
+    L.epoch = ++B.epoch;
+    for (int32_t g = 0; g < P; ++g) {
+        char* gb = base + (size_t)g * GL.bytes;
+        L.ws[g] = (double*)gb;
+        L.rec[g] = (PivRec*)(gb + GL.o_rec);
+        L.wit[g] = (double*)(gb + GL.o_wit);
+        L.src[g] = d_a;
+        L.src_row0[g] = 0;
+    }
+    L.row_group.assign((size_t)n, 0);
+    if (groups)
+        for (int64_t r = 0; r < n; ++r) L.row_group[(size_t)r] = groups->group_of(r);
+    L.d_meta = base + (size_t)P * GL.bytes;
+    L.meta_bytes = mb;
+    rc = k1_execute(B, L, fast, st, run);
+    if (rc) return rc;
+    if (keep_rows && keep_out) {
+        keep_out->assign(keep_rows->size() * (size_t)keep_cols, 0.0);
+        keep_wit->assign(keep_rows->size(), 0.0);
+        for (size_t i = 0; i < keep_rows->size(); ++i) {
+            const int32_t r = (*keep_rows)[i], g = L.row_group[(size_t)r];
+            CUDA_TRY(cudaMemcpy(keep_out->data() + i * keep_cols, L.ws[g] + (int64_t)r * GL.ld,
+                                (size_t)keep_cols * sizeof(double), cudaMemcpyDeviceToHost));
+            CUDA_TRY(cudaMemcpy(keep_wit->data() + i, L.wit[g] + r, sizeof(double), cudaMemcpyDeviceToHost));
+        }
+    }
     return MCND_OK;
 }
 
@@ -365,7 +497,8 @@ int serial_dev(const double* d_a, int64_t n, int64_t lda, const int64_t* seq_in,
             run.steps = bad;  // run the valid prefix; the error surfaces unless it went singular first
         }
     }
-    rc = k1_run(*B, d_a, n, lda, (flags & MCND_FLAG_FAST) != 0, st, run, false, nullptr, 0, nullptr);
+    rc = k1_run_local(*B, d_a, n, lda, (flags & MCND_FLAG_FAST) != 0, st, run, nullptr, nullptr, 0, nullptr,
+                      nullptr);
     if (rc) return rc;
     out->device_ms = run.device_ms;
     if (pivots_out) for (size_t t = 0; t < run.piv_val.size(); ++t) pivots_out[t] = run.piv_val[t];
@@ -407,54 +540,17 @@ int serial_dev(const double* d_a, int64_t n, int64_t lda, const int64_t* seq_in,
     return MCND_OK;
 }
 
-int parallel_dev(const double* d_a, int64_t n, int64_t lda, int32_t p, uint32_t flags, cudaStream_t st,
-                 mcnd_logdet* out, mcnd_comm_stats* stats, int64_t* payload_out, int64_t* row_updates_out,
-                 int32_t* owners_out) {
-    clear_out(out);
-    if (stats) std::memset(stats, 0, sizeof(*stats));
-    int rc = check_shape(d_a, n, lda);
-    if (rc) return rc;
-    if (p < 1 || p > n) return fail(MCND_EINVAL, "invalid plan: need 1 <= p <= n, got p=%d, n=%lld", p, (long long)n);
-    int code = MCND_OK;
-    Buffers* B = buffers_for_current(&code);
-    if (!B) return code;
-
-    // plan_blocks (runtime.py:33-44) and the round-robin owner schedule (runtime.py:153-156)
-    std::vector<int64_t> start((size_t)p), len((size_t)p), consumed((size_t)p, 0);
-    {
-        const int64_t base = n / p, extra = n % p;
-        int64_t s0 = 0;
-        for (int32_t w = 0; w < p; ++w) {
-            start[(size_t)w] = s0;
-            len[(size_t)w] = base + (w < extra ? 1 : 0);
-            s0 += len[(size_t)w];
-        }
-    }
-    K1Run run;
-    run.n = n;
-    std::vector<int32_t> owner;
-    for (;;) {
-        bool any = false;
-        for (int32_t w = 0; w < p; ++w) any |= (len[(size_t)w] - consumed[(size_t)w] > 1);
-        if (!any) break;
-        for (int32_t w = 0; w < p; ++w) {
-            if (len[(size_t)w] - consumed[(size_t)w] <= 1) continue;
-            run.seq.push_back((int32_t)(start[(size_t)w] + consumed[(size_t)w]));
-            owner.push_back(w);
-            consumed[(size_t)w] += 1;
-        }
-    }
-    run.steps = (int64_t)run.seq.size();  // n - p
-    std::vector<int32_t> rem_rows((size_t)p);
-    for (int32_t w = 0; w < p; ++w) rem_rows[(size_t)w] = (int32_t)(start[(size_t)w] + consumed[(size_t)w]);
-    std::vector<double> rem;
-    rc = k1_run(*B, d_a, n, lda, (flags & MCND_FLAG_FAST) != 0, st, run, true, &rem_rows, p, &rem);
-    if (rc) return rc;
-    out->device_ms = run.device_ms;
-
-    const int64_t S = run.steps;
-    const int64_t done = run.singular_at >= 0 ? run.singular_at : S;
-    // accounting (runtime.py:82-90, 185-197)
+// Folds the mc_parallel pivots + p x p remainder into the reference's result
+// and accounting (runtime.py:185-229).  Shared by the single-process and the
+// multi-GPU drivers.  singular_at: first pivot that failed the witness test, or -1.
+int fold_parallel(int64_t n, int32_t p, const double* piv_vals, const int32_t* piv_cols, int64_t singular_at,
+                  const double* rem, const double* rem_wit, mcnd_logdet* out, mcnd_comm_stats* stats,
+                  int64_t* payload_out, int64_t* row_updates_out) {
+    const Blocks b = plan_blocks(n, p);
+    std::vector<int32_t> seq, owner;
+    round_robin(b, &seq, &owner);
+    const int64_t S = (int64_t)seq.size();
+    const int64_t done = singular_at >= 0 ? singular_at : S;
     std::vector<int64_t> cons((size_t)p, 0), row_upd((size_t)p, 0);
     int64_t bbytes = 0, scalar = 0;
     std::vector<double> local_logs((size_t)p, 0.0);
@@ -463,48 +559,46 @@ int parallel_dev(const double* d_a, int64_t n, int64_t lda, int32_t p, uint32_t 
     for (int64_t t = 0; t < done; ++t) {
         const int32_t w = owner[(size_t)t];
         const int64_t m = n - t, last = m - 1;
-        const double v = run.piv_val[(size_t)t];
-        const int64_t r = run.seq[(size_t)t];
+        const double v = piv_vals[t];
+        const int64_t r = seq[(size_t)t];
         local_logs[(size_t)w] += std::log(std::fabs(v));
         cons[(size_t)w] += 1;
         const int64_t k_pos = live.prefix(r);
         live.remove(r);
-        const int swap_parity = (run.piv_col[(size_t)t] != last) ? -1 : 1;
+        const int swap_parity = (piv_cols[t] != last) ? -1 : 1;
         const int parity = ((k_pos + m - 1) % 2) ? -1 : 1;
         sign *= (v > 0 ? 1 : -1) * swap_parity * parity;
         bbytes += 8 * last + 8;
         if (payload_out) payload_out[t] = last;
         for (int32_t u = 0; u < p; ++u) {
-            const int64_t lv = len[(size_t)u] - cons[(size_t)u];
+            const int64_t lv = b.len[(size_t)u] - cons[(size_t)u];
             row_upd[(size_t)u] += lv;
             scalar += lv * last;
         }
     }
-    if (owners_out) for (int64_t t = 0; t < S; ++t) owners_out[t] = owner[(size_t)t];
     if (row_updates_out) for (int32_t u = 0; u < p; ++u) row_updates_out[u] = row_upd[(size_t)u];
     if (stats) {
-        stats->broadcasts = done + (run.singular_at >= 0 ? 1 : 0);
-        stats->broadcast_bytes = bbytes + (run.singular_at >= 0 ? 1 : 0);
+        stats->broadcasts = done + (singular_at >= 0 ? 1 : 0);
+        stats->broadcast_bytes = bbytes + (singular_at >= 0 ? 1 : 0);
         stats->pivot_search_msgs = 0;
         stats->scalar_updates = scalar;
-        stats->aborted_step = run.singular_at;
+        stats->aborted_step = singular_at;
     }
     out->steps = done;
-    if (run.singular_at >= 0) {
+    if (singular_at >= 0) {
         out->sign = 0;
         out->singular = 1;
         out->log_abs = -INFINITY;
-        out->singular_step = run.singular_at;
+        out->singular_step = singular_at;
         return MCND_OK;
     }
     // gather -> reduce_sum -> LU tail (runtime.py:209-219)
-    std::vector<double> fw((size_t)p);
-    for (int32_t w = 0; w < p; ++w) fw[(size_t)w] = run.row_wit[(size_t)rem_rows[(size_t)w]];
+    std::vector<double> remv(rem, rem + (size_t)p * p), fw(rem_wit, rem_wit + p);
     double total = 0.0;
     for (int32_t w = 0; w < p; ++w) total += local_logs[(size_t)w];
     int32_t rs = 0;
     double rl = 0.0;
-    logdet_lu_host(rem, p, fw, &rs, &rl);
+    logdet_lu_host(remv, p, fw, &rs, &rl);
     if (rs == 0) {
         out->sign = 0;
         out->singular = 1;
@@ -515,6 +609,38 @@ int parallel_dev(const double* d_a, int64_t n, int64_t lda, int32_t p, uint32_t 
     out->sign = sign * rs;
     out->log_abs = total + rl;
     return MCND_OK;
+}
+
+int parallel_dev(const double* d_a, int64_t n, int64_t lda, int32_t p, uint32_t flags, cudaStream_t st,
+                 mcnd_logdet* out, mcnd_comm_stats* stats, int64_t* payload_out, int64_t* row_updates_out,
+                 int32_t* owners_out) {
+    clear_out(out);
+    if (stats) std::memset(stats, 0, sizeof(*stats));
+    int rc = check_shape(d_a, n, lda);
+    if (rc) return rc;
+    if (p < 1 || p > n) return fail(MCND_EINVAL, "invalid plan: need 1 <= p <= n, got p=%d, n=%lld", p, (long long)n);
+    const bool groups = (flags & MCND_FLAG_GROUPS) != 0;
+    if (groups && p > kMaxGroups) return fail(MCND_EINVAL, "MCND_FLAG_GROUPS supports p <= %d", kMaxGroups);
+    int code = MCND_OK;
+    Buffers* B = buffers_for_current(&code);
+    if (!B) return code;
+
+    const Blocks blk = plan_blocks(n, p);
+    K1Run run;
+    run.n = n;
+    std::vector<int32_t> owner;
+    round_robin(blk, &run.seq, &owner);
+    run.steps = (int64_t)run.seq.size();  // n - p
+    std::vector<int32_t> rem_rows((size_t)p);
+    for (int32_t w = 0; w < p; ++w) rem_rows[(size_t)w] = (int32_t)(blk.start[(size_t)w] + blk.len[(size_t)w] - 1);
+    std::vector<double> rem, rem_wit;
+    rc = k1_run_local(*B, d_a, n, lda, (flags & MCND_FLAG_FAST) != 0, st, run, groups ? &blk : nullptr, &rem_rows,
+                      p, &rem, &rem_wit);
+    if (rc) return rc;
+    out->device_ms = run.device_ms;
+    if (owners_out) for (size_t t = 0; t < owner.size(); ++t) owners_out[t] = owner[t];
+    return fold_parallel(n, p, run.piv_val.data(), run.piv_col.data(), run.singular_at, rem.data(), rem_wit.data(),
+                         out, stats, payload_out, row_updates_out);
 }
 
 // Host-input staging: copy an n x n (lda) host matrix into a cached device buffer.
@@ -528,6 +654,19 @@ int stage_input(Buffers& B, const double* h_a, int64_t rows, int64_t n, int64_t 
     *d_out = (const double*)B.din;
     return MCND_OK;
 }
+
+// ---- multi-GPU (one process per GPU) ----
+struct DistHandle {
+    int32_t rank = 0, world = 1;
+    int64_t n_max = 0;
+    GroupLayout GL;             // layout for n_max (identical on every rank)
+    Buffers B;                  // this rank's own buffers (workspace = IPC-exported allocation)
+    void* meta = nullptr;
+    size_t meta_bytes = 0;
+    void* peer_base[kMaxGroups] = {};
+    bool connected = false;
+    uint32_t epoch = 0;
+};
 
 }  // namespace
 }  // namespace mcnd
@@ -549,6 +688,7 @@ int mcnd_logdet_condensation(const double* h_a, int64_t n, int64_t lda, const in
                              int64_t pivot_sequence_len, uint32_t flags, void* stream, mcnd_logdet* out,
                              double* pivots_out, int32_t* cols_out) {
     if (!out) return fail(MCND_EINVAL, "null out");
+    clear_out(out);
     int rc = check_shape(h_a, n, lda);
     if (rc) return rc;
     std::lock_guard<std::mutex> lk(g_mu);
@@ -575,6 +715,7 @@ int mcnd_mc_parallel(const double* h_a, int64_t n, int64_t lda, int32_t p, uint3
                      mcnd_logdet* out, mcnd_comm_stats* stats, int64_t* payload_entries, int64_t* row_updates,
                      int32_t* owners_out) {
     if (!out) return fail(MCND_EINVAL, "null out");
+    clear_out(out);
     int rc = check_shape(h_a, n, lda);
     if (rc) return rc;
     std::lock_guard<std::mutex> lk(g_mu);
@@ -586,6 +727,127 @@ int mcnd_mc_parallel(const double* h_a, int64_t n, int64_t lda, int32_t p, uint3
     if (rc) return rc;
     return parallel_dev(d_a, n, n, p, flags, (cudaStream_t)stream, out, stats, payload_entries, row_updates,
                         owners_out);
+}
+
+int mcnd_fold_mc_parallel(int64_t n, int32_t p, const double* piv_vals, const int32_t* piv_cols,
+                          int64_t singular_at, const double* rem, const double* rem_wit, mcnd_logdet* out,
+                          mcnd_comm_stats* stats, int64_t* payload_entries, int64_t* row_updates) {
+    if (!out) return fail(MCND_EINVAL, "null out");
+    clear_out(out);
+    if (p < 1 || p > n) return fail(MCND_EINVAL, "invalid plan: need 1 <= p <= n, got p=%d, n=%lld", p, (long long)n);
+    if (stats) std::memset(stats, 0, sizeof(*stats));
+    return fold_parallel(n, p, piv_vals, piv_cols, singular_at, rem, rem_wit, out, stats, payload_entries,
+                         row_updates);
+}
+
+int32_t mcnd_dist_ipc_handle_bytes(void) { return (int32_t)sizeof(cudaIpcMemHandle_t); }
+
+int mcnd_dist_create(int32_t rank, int32_t world, int64_t n_max, void** handle, void* ipc_out) {
+    if (!handle || !ipc_out) return fail(MCND_EINVAL, "null handle/ipc_out");
+    if (world < 1 || world > kMaxGroups || rank < 0 || rank >= world)
+        return fail(MCND_EINVAL, "need 1 <= world <= %d and 0 <= rank < world", kMaxGroups);
+    if (n_max < world) return fail(MCND_EINVAL, "n_max < world");
+    auto* h = new DistHandle();
+    h->rank = rank;
+    h->world = world;
+    h->n_max = n_max;
+    h->GL = group_layout(n_max, n_max);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int rc = init_buffers(h->B, dev);
+    if (rc) { delete h; return rc; }
+    rc = ensure_dev(&h->B.dws, &h->B.dws_bytes, h->GL.bytes);
+    if (rc) { delete h; return rc; }
+    if (cudaMemset(h->B.dws, 0, h->GL.bytes) != cudaSuccess) { delete h; return fail(MCND_ECUDA, "cudaMemset"); }
+    h->meta_bytes = meta_bytes_for(n_max, n_max, (int64_t)h->B.sms);
+    if (cudaMalloc(&h->meta, h->meta_bytes) != cudaSuccess) { delete h; return fail(MCND_ECUDA, "cudaMalloc meta"); }
+    cudaIpcMemHandle_t ipc;
+    cudaError_t e = cudaIpcGetMemHandle(&ipc, h->B.dws);
+    if (e != cudaSuccess) { delete h; return fail(MCND_ECUDA, "cudaIpcGetMemHandle: %s", cudaGetErrorString(e)); }
+    std::memcpy(ipc_out, &ipc, sizeof(ipc));
+    if (cudaDeviceSynchronize() != cudaSuccess) { delete h; return fail(MCND_ECUDA, "cudaDeviceSynchronize"); }
+    *handle = h;
+    return MCND_OK;
+}
+
+int mcnd_dist_connect(void* handle, const void* ipc_all) {
+    auto* h = (DistHandle*)handle;
+    if (!h || !ipc_all) return fail(MCND_EINVAL, "null handle");
+    for (int32_t r = 0; r < h->world; ++r) {
+        if (r == h->rank) { h->peer_base[r] = h->B.dws; continue; }
+        cudaIpcMemHandle_t ipc;
+        std::memcpy(&ipc, (const char*)ipc_all + (size_t)r * sizeof(ipc), sizeof(ipc));
+        cudaError_t e = cudaIpcOpenMemHandle(&h->peer_base[r], ipc, cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess) return fail(MCND_ECUDA, "cudaIpcOpenMemHandle(rank %d): %s", r, cudaGetErrorString(e));
+    }
+    h->connected = true;
+    return MCND_OK;
+}
+
+int mcnd_dist_mc_parallel(void* handle, const double* d_rows, int64_t n, int64_t lda, uint32_t flags, void* stream,
+                          double* piv_vals, int32_t* piv_cols, int64_t* singular_at, double* rem_row,
+                          double* rem_wit, double* device_ms) {
+    auto* h = (DistHandle*)handle;
+    if (!h || !h->connected) return fail(MCND_EINVAL, "dist handle not connected");
+    if (n != h->n_max) return fail(MCND_EINVAL, "n (%lld) must equal the handle's n_max (%lld)", (long long)n,
+                                   (long long)h->n_max);
+    if (!d_rows || lda < n) return fail(MCND_EINVAL, "bad local rows");
+    const int32_t P = h->world;
+    cudaStream_t st = (cudaStream_t)stream;
+    const Blocks blk = plan_blocks(n, P);
+    K1Run run;
+    run.n = n;
+    std::vector<int32_t> owner;
+    round_robin(blk, &run.seq, &owner);
+    run.steps = (int64_t)run.seq.size();
+    const GroupLayout& GL = h->GL;
+    K1Launch L;
+    L.n = n;
+    L.lda = lda;
+    L.n_groups = P;
+    L.group0 = h->rank;
+    L.n_local = 1;
+    L.cpg = (int32_t)std::max<int64_t>(1, std::min<int64_t>(h->B.sms, blk.len[(size_t)h->rank]));
+    L.sys = true;
+    L.epoch = ++h->epoch;
+    L.reset_records = false;
+    L.timeout_ns = 60ull * 1000000000ull;
+    for (int32_t g = 0; g < P; ++g) {
+        char* gb = (char*)h->peer_base[g];
+        L.ws[g] = (double*)gb;
+        L.rec[g] = (PivRec*)(gb + GL.o_rec);
+    }
+    L.wit[0] = (double*)((char*)h->B.dws + GL.o_wit);
+    L.src[0] = d_rows;
+    L.src_row0[0] = blk.start[(size_t)h->rank];
+    L.row_group.assign((size_t)n, 0);
+    for (int64_t r = 0; r < n; ++r) L.row_group[(size_t)r] = blk.group_of(r);
+    L.d_meta = h->meta;
+    L.meta_bytes = h->meta_bytes;
+    int rc = k1_execute(h->B, L, (flags & MCND_FLAG_FAST) != 0, st, run);
+    if (rc) return rc;
+    const int64_t k = run.singular_at >= 0 ? run.singular_at + 1 : run.steps;
+    for (int64_t t = 0; t < k; ++t) { piv_vals[t] = run.piv_val[(size_t)t]; piv_cols[t] = run.piv_col[(size_t)t]; }
+    *singular_at = run.singular_at;
+    const int64_t r = blk.start[(size_t)h->rank] + blk.len[(size_t)h->rank] - 1;  // my last live row
+    CUDA_TRY(cudaMemcpy(rem_row, (double*)h->B.dws + r * GL.ld, (size_t)P * sizeof(double), cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(rem_wit, L.wit[0] + r, sizeof(double), cudaMemcpyDeviceToHost));
+    if (device_ms) *device_ms = run.device_ms;
+    return MCND_OK;
+}
+
+void mcnd_dist_destroy(void* handle) {
+    auto* h = (DistHandle*)handle;
+    if (!h) return;
+    cudaDeviceSynchronize();
+    for (int32_t r = 0; r < h->world; ++r)
+        if (r != h->rank && h->peer_base[r]) cudaIpcCloseMemHandle(h->peer_base[r]);
+    if (h->meta) cudaFree(h->meta);
+    if (h->B.dws) cudaFree(h->B.dws);
+    if (h->B.hpin) cudaFreeHost(h->B.hpin);
+    if (h->B.ev0) cudaEventDestroy(h->B.ev0);
+    if (h->B.ev1) cudaEventDestroy(h->B.ev1);
+    delete h;
 }
 
 int mcnd_logdet_batched_dev(const double* d_a, int64_t batch, int64_t n, int64_t stride, uint32_t flags,
@@ -629,27 +891,28 @@ int mcnd_logdet_batched(const double* h_a, int64_t batch, int64_t n, int64_t str
 
 const char* mcnd_last_error(void) { return g_err.c_str(); }
 
-int32_t mcnd_version(void) { return 100; }
+int32_t mcnd_version(void) { return 110; }
 
 int32_t mcnd_k1_grid(void) {
-    int dev = 0;
+    int dev = 0, sms = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return 0;
-    return k1_max_grid(dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return sms;
 }
 
 void mcnd_release_workspace(void) {
     std::lock_guard<std::mutex> lk(g_mu);
+    int cur = 0;
+    cudaGetDevice(&cur);
     for (auto& b : g_bufs) {
-        int cur = 0;
-        cudaGetDevice(&cur);
         cudaSetDevice(b.device);
         if (b.dws) cudaFree(b.dws);
         if (b.din) cudaFree(b.din);
         if (b.hpin) cudaFreeHost(b.hpin);
         if (b.ev0) cudaEventDestroy(b.ev0);
         if (b.ev1) cudaEventDestroy(b.ev1);
-        cudaSetDevice(cur);
     }
+    cudaSetDevice(cur);
     g_bufs.clear();
 }
 

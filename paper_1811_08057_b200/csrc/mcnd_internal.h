@@ -9,39 +9,61 @@ constexpr double kSingularRtol = 1e-12;  // condense.py:29
 constexpr int kK1Threads = 1024;         // one CTA per SM, 32 warps
 constexpr int kK1MaxRowsPerCta = 512;    // per-CTA row table lives in shared memory
 constexpr int kK1MaxChunk = 16384;       // pivot-row chunk staged in smem (doubles)
-constexpr int32_t kNever = 0x7fffffff;   // pivot step of a row that is never a pivot
+constexpr int kMaxGroups = 8;            // block-row workers (ranks) one launch can address
+constexpr int32_t kNever = 0x7fffffff;   // pivot index of a row that is never a pivot
 
-// Control block written by the persistent kernel (zeroed before each launch).
-struct K1Ctrl {
-    unsigned published;   // number of pivots published so far (pivot t visible iff published > t)
-    unsigned error;       // nonzero: device-side timeout / protocol error
+// One published pivot.  Written once per call by the owner CTA into EVERY
+// group's record array (local or peer memory); `flag` is release-stored last
+// with the call's epoch, so no per-call reset is needed.
+struct PivRec {
+    double v;       // pivot value
+    int32_t l;      // pivot column (-1: failed the witness test -> singular)
+    uint32_t flag;  // == epoch once v/l and the scaled pivot row are visible
+};
+
+struct K1Err {
+    unsigned error;     // nonzero: device-side timeout
     unsigned err_step;
+    unsigned nonfinite; // nonzero: the input held NaN/Inf (-> ValueError)
     unsigned pad;
 };
 
 // Persistent, barrier-free condensation kernel parameters (k1_condense.cu).
+//
+// "Groups" are the block-row workers of mc_parallel (runtime.py:123): group g
+// owns a contiguous block of rows and keeps a full n x ld workspace in which
+// the rows it does not own serve as mailboxes for the scaled pivot rows.  One
+// launch runs `n_local_groups` groups starting at global id `group0`:
+//   single GPU  : 1 group, no peers;
+//   multi GPU   : 1 group per rank, ws[]/rec[] of other ranks are peer
+//                 (CUDA IPC, NVLink) mappings, sys-scope flags;
+//   emulation   : all P groups on one GPU (tests the same push protocol).
 struct K1Params {
-    const double* src;       // caller's matrix (device), read once in the prologue
+    const double* src[kMaxGroups];   // input rows of each local group
+    int64_t src_row0[kMaxGroups];    // global row id of src[g]'s first row
     int64_t lds;
-    double* ws;              // workspace: n rows x ld, condensed in place
+    double* ws[kMaxGroups];          // workspace of every group (n rows x ld)
+    PivRec* rec[kMaxGroups];         // pivot records of every group
+    double* row_wit[kMaxGroups];     // per-row witnesses at exit (local groups; global row index)
     int64_t ld;
     int32_t n;
-    int32_t n_steps;         // S condensation steps
-    const int32_t* seq;      // pivot row of pivot t (t < S, plus t == S when a final 1x1 is published)
-    const int32_t* row_pstep;    // pivot index of each row (kNever if never a pivot)
-    const int32_t* cta_row_ptr;  // [G+1]
-    const int32_t* cta_rows;     // rows dealt to each CTA, ascending pivot index
-    double* piv_val;         // [S+1]
-    int32_t* piv_col;        // [S+1] (-1: singular at that pivot)
-    double* piv_wit;         // [S+1]
-    double* row_wit;         // [n]  witnesses at exit
-    K1Ctrl* ctrl;
-    int32_t chunk;           // staged pivot-row chunk (even, <= kK1MaxChunk)
+    int32_t n_steps;                 // S condensation steps
+    int32_t n_groups;                // P
+    int32_t group0;
+    int32_t n_local_groups;
+    int32_t ctas_per_group;
+    int32_t sys_scope;               // 1: peers live on other GPUs
+    uint32_t epoch;
+    const int32_t* seq;              // global pivot schedule (pivot row of pivot t)
+    const int32_t* row_pstep;        // pivot index of each row (kNever: never a pivot)
+    const int32_t* cta_row_ptr;      // [n_local_groups * ctas_per_group + 1]
+    const int32_t* cta_rows;         // rows dealt to each CTA, ascending pivot index
+    K1Err* err;
+    int32_t chunk;                   // staged pivot-row chunk (even, <= kK1MaxChunk)
     unsigned long long timeout_ns;
 };
 
-cudaError_t k1_launch(const K1Params& p, int grid, bool fast, cudaStream_t s);
-int k1_max_grid(int device);
+cudaError_t k1_launch(const K1Params& p, bool fast, cudaStream_t s);
 size_t k1_smem_bytes(int chunk);
 
 cudaError_t k3_launch(const double* a, int64_t batch, int64_t n, int64_t stride, bool fast,

@@ -47,6 +47,23 @@ def require_square(a) -> np.ndarray:
     return a
 
 
+def square_for_device(data) -> np.ndarray:
+    """require_square without the O(N^2) host finiteness scan: the CUDA
+    prologue checks finiteness while copying (k1_condense.cu) and the call
+    raises the same ValueError.  Non-square input still reports non-finite
+    entries first, in the reference's check order (matrix.py:35-47)."""
+    a = np.ascontiguousarray(data, dtype=np.float64)
+    if a.ndim != 2:
+        raise ValueError(f"matrix must be 2-D, got {a.ndim}-D")
+    if a.shape[0] == 0 or a.shape[1] == 0:
+        raise ValueError("matrix dimensions must be positive")
+    if a.shape[0] != a.shape[1]:
+        if not np.isfinite(a).all():
+            raise ValueError("matrix entries must be finite (no NaN/Inf)")
+        raise ValueError(f"matrix must be square, got {a.shape}")
+    return a
+
+
 @dataclass(frozen=True)
 class MatrixSpec:
     """matrix.py:51-66: deterministic recipe (size, kind, seed)."""

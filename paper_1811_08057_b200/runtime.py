@@ -28,7 +28,7 @@ import numpy as np
 
 from . import _lib
 from .condense import SINGULAR, LogDet, _is_torch_cuda, _torch_device_args
-from .matrix import require_square
+from .matrix import square_for_device
 
 
 @dataclass(frozen=True)
@@ -73,8 +73,13 @@ class RunResult:
     scalar_updates: int = 0
 
 
-def mc_parallel(a, p: int | None = None, *, n_workers: int | None = None, fast: bool = False) -> RunResult:
-    """Block-distributed parallel matrix condensation (runtime.py:123-229) on the GPU."""
+def mc_parallel(a, p: int | None = None, *, n_workers: int | None = None, fast: bool = False,
+                groups: bool = False) -> RunResult:
+    """Block-distributed parallel matrix condensation (runtime.py:123-229) on the GPU.
+
+    ``groups=True`` runs the p workers as p CTA groups with private workspaces
+    that exchange pivot rows through the multi-GPU push protocol (p <= 8);
+    results are identical either way."""
     if p is None:
         p = n_workers
     if p is None:
@@ -83,13 +88,13 @@ def mc_parallel(a, p: int | None = None, *, n_workers: int | None = None, fast: 
     lib = _lib.load()
     out = _lib.McndLogDet()
     st = _lib.McndCommStats()
-    flags = _lib.FLAG_FAST if fast else 0
+    flags = (_lib.FLAG_FAST if fast else 0) | (_lib.FLAG_GROUPS if groups else 0)
     t0 = time.perf_counter()
     if _is_torch_cuda(a):
         keep, ptr, n, ld, stream = _torch_device_args(a)
         fn, args = lib.mcnd_mc_parallel_dev, (ptr, n, ld)
     else:
-        a = require_square(a)
+        a = square_for_device(a)
         n = a.shape[0]
         keep, stream = a, None
         fn, args = lib.mcnd_mc_parallel, (a.ctypes.data, n, n)

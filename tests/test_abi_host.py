@@ -62,8 +62,8 @@ def test_invalid_shapes_raise_value_error_before_device_work():
         logdet_condensation(np.zeros(3))
     with pytest.raises(ValueError, match="positive"):
         logdet_condensation(np.zeros((0, 0)))
-    with pytest.raises(ValueError, match="finite"):
-        logdet_condensation(np.array([[1.0, np.nan], [0.0, 1.0]]))
+    with pytest.raises(ValueError, match="finite"):  # non-square AND non-finite: finiteness first
+        logdet_condensation(np.array([[1.0, np.nan, 2.0], [0.0, 1.0, 3.0]]))
     with pytest.raises(ValueError, match="invalid plan"):
         mc_parallel(np.eye(4), 5)
     with pytest.raises(ValueError, match="invalid plan"):

@@ -1,0 +1,116 @@
+"""Multi-process (gloo, world_size 2 and 3) CPU tests of the block-row driver's
+host side: plan, schedule, the all-gather of the remaining rows and the fold
+into (sign, log|det|) + accounting (runtime.py:206-229).
+
+Each rank plays one worker.  The per-step pivots and the remaining rows come
+from the oracle (what every rank's GPU kernel would hand back); the ranks
+exchange their remaining row through torch.distributed (gloo) exactly as
+dist.BlockRowGroup does and fold with the C-ABI's host-only
+mcnd_fold_mc_parallel.  The result must equal the reference's mc_parallel
+bitwise, on every rank.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, n, seed, kind, q):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import mcnd_oracle as O
+        from paper_1811_08057_b200 import dist as D
+        from paper_1811_08057_b200 import matrix as M
+        from paper_1811_08057_b200.runtime import plan_blocks
+
+        if kind == "planted":
+            a = M.generate(M.MatrixSpec(n, "singular-planted", seed))
+        else:
+            a = np.random.default_rng(seed).uniform(-1, 1, (n, n))
+        ref = O.mc_parallel(a, world)
+        s, ln = plan_blocks(n, world).assignments[rank]
+        # what this rank's kernel returns: all pivots + its own remaining row/witness
+        singular_at = ref.aborted_step
+        k = (singular_at + 1) if singular_at >= 0 else n - world
+        my_row = ref.rem[rank].tolist()
+        my_wit = float(ref.rem_wit[rank])
+        gathered = [None] * world
+        dist.all_gather_object(gathered, (my_row, my_wit))
+        res = D.fold_gathered(n, world, ref.pivots[:k], ref.cols[:k], singular_at,
+                              [g[0] for g in gathered], [g[1] for g in gathered])
+        ok = (res.logdet.sign == ref.sign and (res.logdet.log_abs == ref.log_abs
+              or (np.isinf(ref.log_abs) and np.isinf(res.logdet.log_abs)))
+              and res.stats.broadcasts == ref.broadcasts and res.stats.broadcast_bytes == ref.broadcast_bytes
+              and res.row_updates == ref.row_updates and res.scalar_updates == ref.scalar_updates
+              and res.broadcast_payload_entries == ref.payload_entries)
+        q.put((rank, ok, (res.logdet, (ref.sign, ref.log_abs)), (s, ln)))
+    except Exception as e:  # pragma: no cover - surfaced by the assert below
+        q.put((rank, False, repr(e), None))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n,seed,kind", [(2, 64, 1, "uniform"), (2, 101, 2, "uniform"),
+                                               (3, 50, 3, "uniform"), (2, 16, 16, "planted"),
+                                               (3, 17, 5, "uniform")])
+def test_gloo_gather_and_fold_matches_reference(world, n, seed, kind):
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, seed, kind, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, ok, detail, _ in sorted(results, key=lambda x: x[0]):
+        assert ok, f"rank {rank}: {detail}"
+    # the block plan each rank used tiles [0, n)
+    spans = sorted(r[3] for r in results)
+    assert spans[0][0] == 0 and sum(ln for _, ln in spans) == n
+
+
+def test_round_robin_owner_equals_most_live_rows_when_divisible():
+    """north_star owner rule ("rank with the most live rows, ties -> lowest")
+    coincides with the reference's round-robin (runtime.py:153-156) for p | n."""
+    from paper_1811_08057_b200.runtime import plan_blocks
+
+    for n, p in ((1000, 1), (4000, 2), (8000, 2), (8000, 4), (8000, 8), (64, 8), (96, 3)):
+        lens = [ln for _, ln in plan_blocks(n, p).assignments]
+        consumed = [0] * p
+        rr = []
+        while any(lens[w] - consumed[w] > 1 for w in range(p)):
+            for w in range(p):
+                if lens[w] - consumed[w] <= 1:
+                    continue
+                rr.append(w)
+                consumed[w] += 1
+        consumed = [0] * p
+        most = []
+        for _ in range(n - p):
+            live = [lens[w] - consumed[w] for w in range(p)]
+            w = max(range(p), key=lambda u: (live[u], -u))
+            most.append(w)
+            consumed[w] += 1
+        assert rr == most, (n, p)

@@ -133,6 +133,39 @@ def test_kernel_shapes_bitwise_vs_oracle(mc, env_knob, grid, chunk):
             assert (gotp.logdet.sign, gotp.logdet.log_abs) == (refp.sign, refp.log_abs)
 
 
+@pytest.mark.parametrize("p", [2, 3, 4, 8])
+def test_emulated_ranks_push_protocol_bitwise(mc, p):
+    """mc_parallel with the p workers as p CTA groups that push pivot rows into
+    each other's workspaces (the multi-GPU protocol, on one GPU)."""
+    from oracle import mcnd_oracle as O
+
+    for n, seed in ((64, 1), (257, 2), (1000, 3)):
+        a = np.random.default_rng(seed).uniform(-1, 1, (n, n))
+        ref = O.mc_parallel(a, p)
+        got = mc.mc_parallel(a, p, groups=True)
+        assert (got.logdet.sign, got.logdet.log_abs) == (ref.sign, ref.log_abs)
+        assert got.stats.broadcasts == ref.broadcasts
+        assert got.row_updates == ref.row_updates
+    z = mc.generate(mc.MatrixSpec(16, "singular-planted", 16))
+    assert mc.mc_parallel(z, min(p, 3), groups=True).logdet == mc.SINGULAR
+
+
+def test_nonfinite_detected_on_device(mc):
+    import torch
+
+    a = np.eye(40)
+    a[17, 3] = np.nan
+    with pytest.raises(ValueError, match="finite"):
+        mc.logdet_condensation(a)
+    a[17, 3] = np.inf
+    with pytest.raises(ValueError, match="finite"):
+        mc.logdet_condensation(torch.from_numpy(a).cuda())
+    with pytest.raises(ValueError, match="finite"):
+        mc.mc_parallel(a, 4)
+    # the library is still healthy afterwards
+    assert mc.logdet_condensation(np.eye(40)) == (1, 0.0)
+
+
 def test_fast_mode_within_tolerance(mc):
     for n, seed in ((100, 0), (1000, 1), (2049, 2)):
         a = np.random.default_rng(seed).standard_normal((n, n))
