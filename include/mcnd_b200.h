@@ -89,6 +89,17 @@ int mcnd_mc_parallel(const double* h_a, int64_t n, int64_t lda, int32_t p, uint3
                      void* stream, mcnd_logdet* out, mcnd_comm_stats* stats,
                      int64_t* payload_entries, int64_t* row_updates, int32_t* owners_out);
 
+/* ---- blocked rank-b condensation (b = mcnd_blocked_panel() = 64): panels of b pivot
+ * rows factorised with the unblocked rule, then one rank-b trailing update on FP64
+ * tensor cores (DMMA).  Same pivot rule and result type as logdet_condensation
+ * (top-to-bottom order); rounding differs from the reference (tolerance parity).
+ * No reference counterpart (PAPER.md:89 leaves it to future work). */
+int mcnd_logdet_blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, void* stream,
+                            mcnd_logdet* out, double* pivots_out, int32_t* cols_out);
+int mcnd_logdet_blocked(const double* h_a, int64_t n, int64_t lda, uint32_t flags, void* stream,
+                        mcnd_logdet* out, double* pivots_out, int32_t* cols_out);
+int32_t mcnd_blocked_panel(void);
+
 /* Fold per-step pivots and the p x p remainder of the block-row driver into the
  * reference's result and accounting (runtime.py:185-229): sign parity, per-worker
  * log sums reduced in rank order, row-pivoted LU tail (gauss.py:34-68).

@@ -10,7 +10,7 @@ Everything below the Python surface is sm_100a CUDA behind a C ABI
 """
 
 from .batched import logdet_batched
-from .condense import SINGULAR, SINGULAR_RTOL, LogDet, SingularRowError, logdet_condensation
+from .condense import SINGULAR, SINGULAR_RTOL, LogDet, SingularRowError, logdet_blocked, logdet_condensation
 from .matrix import GENERATOR_KINDS, MatrixSpec, as_matrix, generate, require_square
 from .registry import ALGORITHMS, run_algorithm
 from .runtime import CommStats, RunResult, WorkerPlan, mc_parallel, plan_blocks
@@ -21,6 +21,7 @@ __all__ = [
     "SINGULAR_RTOL",
     "SingularRowError",
     "logdet_condensation",
+    "logdet_blocked",
     "logdet_batched",
     "mc_parallel",
     "plan_blocks",

@@ -46,6 +46,7 @@ EXPORTS = (
     "mcnd_dist_ipc_handle_bytes", "mcnd_dist_create", "mcnd_dist_connect", "mcnd_dist_mc_parallel",
     "mcnd_dist_destroy",
     "mcnd_last_error", "mcnd_version", "mcnd_k1_grid", "mcnd_release_workspace",
+    "mcnd_logdet_blocked_dev", "mcnd_logdet_blocked", "mcnd_blocked_panel",
 )
 
 
@@ -88,6 +89,11 @@ def load(path: str | None = None):
         lib.mcnd_dist_mc_parallel.restype = ctypes.c_int
         lib.mcnd_dist_destroy.argtypes = [P]
         lib.mcnd_dist_destroy.restype = None
+        for name in ("mcnd_logdet_blocked_dev", "mcnd_logdet_blocked"):
+            f = getattr(lib, name)
+            f.argtypes = [P, i64, i64, u32, P, LD, P, P]
+            f.restype = ctypes.c_int
+        lib.mcnd_blocked_panel.restype = ctypes.c_int32
         lib.mcnd_last_error.argtypes = []
         lib.mcnd_last_error.restype = ctypes.c_char_p
         lib.mcnd_version.restype = ctypes.c_int32

@@ -118,3 +118,34 @@ def logdet_condensation(a, pivot_sequence: Optional[Sequence[int]] = None, *, fa
         return res, piv[: k + (1 if out.singular else 0)], cols[: k + (1 if out.singular else 0)], float(out.device_ms)
     return res
 
+
+
+def logdet_blocked(a, *, fast: bool = False, return_pivots: bool = False):
+    """Blocked rank-64 condensation (K2, csrc/k2_blocked.cu): panels of 64 pivot
+    rows chosen by the reference's rule, trailing update on FP64 tensor cores.
+    Same result type and pivot rule as logdet_condensation (top-to-bottom);
+    rounding differs from the reference, so parity is by tolerance.  Input
+    handling as logdet_condensation."""
+    lib = _lib.load()
+    out = _lib.McndLogDet()
+    flags = _lib.FLAG_FAST if fast else 0
+    if _is_torch_cuda(a):
+        keep, ptr, n, ld, stream = _torch_device_args(a)
+        piv = np.zeros(n, dtype=np.float64)
+        cols = np.zeros(n, dtype=np.int32)
+        rc = lib.mcnd_logdet_blocked_dev(ptr, n, ld, flags, stream, ctypes.byref(out), piv.ctypes.data,
+                                         cols.ctypes.data)
+        del keep
+    else:
+        a = square_for_device(a)
+        n = a.shape[0]
+        piv = np.zeros(n, dtype=np.float64)
+        cols = np.zeros(n, dtype=np.int32)
+        rc = lib.mcnd_logdet_blocked(a.ctypes.data, n, n, flags, None, ctypes.byref(out), piv.ctypes.data,
+                                     cols.ctypes.data)
+    _lib.check(rc)
+    res = SINGULAR if out.singular else LogDet(int(out.sign), float(out.log_abs))
+    if return_pivots:
+        k = int(out.steps) + (0 if out.singular else 1)
+        return res, piv[:k], cols[:k], float(out.device_ms)
+    return res

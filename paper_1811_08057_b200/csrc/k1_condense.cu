@@ -156,7 +156,6 @@ __global__ void __launch_bounds__(kThreads, 1) k1_condense(const K1Params p) {
     extern __shared__ __align__(16) double s_prow[];
     __shared__ Smem sm;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int n = p.n;
     const int gl = blockIdx.x / p.ctas_per_group;  // local group
     const int g = p.group0 + gl;                   // global group (worker / rank)
     double* const ws = p.ws[g];
@@ -167,16 +166,29 @@ __global__ void __launch_bounds__(kThreads, 1) k1_condense(const K1Params p) {
     for (int i = tid; i < nr; i += kThreads) {
         const int r = p.cta_rows[rbeg + i];
         sm.rows[i] = r;
-        sm.pstep[i] = p.row_pstep[r];
+        sm.pstep[i] = p.row_pstep[r] - p.pstep_offset;
         sm.wit[i] = 0ull;
     }
     __syncthreads();
 
+    if (p.abort_flag && *(volatile const unsigned*)p.abort_flag) return;  // uniform per CTA
+    const int ncol0 = p.ncol0;
+
     // ---- prologue: copy my rows into the workspace, initial witness (condense.py:72-78)
-    //      and the finiteness check (matrix.py:39-40)
-    {
+    //      and the finiteness check (matrix.py:39-40).  In panel mode (blocked K2) the
+    //      rows are already in place: only the witness is refreshed.
+    if (p.in_place) {
+        for (int i = warp; i < nr; i += kWarps) {
+            const int r = sm.rows[i];
+            const double* row = ws + (int64_t)r * p.ld;
+            double wm = 0.0;
+            for (int c = lane; c < ncol0; c += 32) wm = fmax(wm, fabs(row[c]));
+            wm = fmax(warp_max(wm), p.wit_in[r]);
+            if (lane == 0) sm.wit[i] = (unsigned long long)__double_as_longlong(wm);
+        }
+    } else {
         constexpr int kSeg = 256;
-        const int nseg = (n + kSeg - 1) / kSeg;
+        const int nseg = (ncol0 + kSeg - 1) / kSeg;
         const int total = nr * nseg;
         bool bad = false;
         for (int j = warp; j < total; j += kWarps) {
@@ -189,13 +201,13 @@ __global__ void __launch_bounds__(kThreads, 1) k1_condense(const K1Params p) {
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
                 const int c = c0 + 32 * k;
-                x[k] = (c < n) ? __ldg(src + c) : 0.0;
+                x[k] = (c < ncol0) ? __ldg(src + c) : 0.0;
             }
             double wm = 0.0;
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
                 const int c = c0 + 32 * k;
-                if (c < n) {
+                if (c < ncol0) {
                     dst[c] = x[k];
                     wm = fmax(wm, fabs(x[k]));
                     bad |= !isfinite(x[k]);
@@ -213,17 +225,17 @@ __global__ void __launch_bounds__(kThreads, 1) k1_condense(const K1Params p) {
         double* rowp = ws + (int64_t)sm.rows[0] * p.ld;
         double bv = 0.0, bw = 0.0;
         int bi = INT_MAX;
-        for (int c = tid; c < n; c += kThreads) {
+        for (int c = tid; c < ncol0; c += kThreads) {
             const double x = rowp[c];
             if (beats(x, c, bv, bi)) { bv = x; bi = c; }
         }
         cta_reduce(sm, bv, bi, bw);
-        publish(p, sm, g, sm.rows[0], 0, n, bv, bi, __longlong_as_double((long long)sm.wit[0]));
+        publish(p, sm, g, sm.rows[0], 0, ncol0, bv, bi, __longlong_as_double((long long)sm.wit[0]));
     }
 
     int start = 0;  // first live local row
     for (int s = 0; s < p.n_steps; ++s) {
-        const int m = n - s, w = m - 1;
+        const int m = ncol0 - s, w = m - 1;
         // ---- wait for pivot s
         if (tid == 0) {
             int l = -2;

@@ -288,6 +288,11 @@ int k1_execute(Buffers& B, K1Launch& L, bool fast, cudaStream_t st, K1Run& run) 
     const long ck = env_long("MCND_K1_CHUNK", 0);  // test knob: force multi-chunk staging
     if (ck >= 2 && ck <= kK1MaxChunk) p.chunk = (int32_t)std::min<int64_t>(p.chunk, ck & ~1L);
     p.timeout_ns = L.timeout_ns;
+    p.ncol0 = (int32_t)n;
+    p.in_place = 0;
+    p.wit_in = nullptr;
+    p.abort_flag = nullptr;
+    p.pstep_offset = 0;
 
     CUDA_TRY(cudaEventRecord(B.ev0, st));
     cudaError_t e = k1_launch(p, fast, st);
@@ -655,6 +660,173 @@ int stage_input(Buffers& B, const double* h_a, int64_t rows, int64_t n, int64_t 
     return MCND_OK;
 }
 
+// ---- blocked rank-b condensation (K2) ----
+// Panels of b = 64 pivot rows while at least `m_tail` columns remain after the
+// panel, then the unblocked K1 finishes the last m_tail..m_tail+b-1 rows.  All
+// launches are asynchronous; a failed witness test raises a device abort flag
+// that turns every later launch into a no-op; one D2H at the end.
+int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaStream_t st, mcnd_logdet* out,
+                double* pivots_out, int32_t* cols_out) {
+    clear_out(out);
+    int rc = check_shape(d_a, n, lda);
+    if (rc) return rc;
+    int code = MCND_OK;
+    Buffers* B = buffers_for_current(&code);
+    if (!B) return code;
+    const bool fast = (flags & MCND_FLAG_FAST) != 0;
+    const int64_t b = kK2B;
+    int64_t m_tail = env_long("MCND_K2_TAIL", 1024);
+    if (m_tail < 2) m_tail = 2;
+    const int64_t n_panels = (n - m_tail >= b) ? (n - m_tail) / b : 0;
+    const int64_t kb_end = n_panels * b;
+    const int64_t mt = n - kb_end;
+    const int64_t ld = (int64_t)align_up((size_t)n, 16);
+    const int64_t G0 = std::min<int64_t>(B->sms, n);
+    const int64_t Gt = std::min<int64_t>(B->sms, mt);
+    if ((n + G0 - 1) / G0 > kK1MaxRowsPerCta) return fail(MCND_EINVAL, "n=%lld too large for one GPU", (long long)n);
+
+    // device layout
+    size_t off = 0;
+    auto take = [&](size_t bytes) { size_t o = off; off = align_up(off + bytes, 256); return o; };
+    const size_t o_ws = take((size_t)n * ld * sizeof(double));
+    const size_t o_wit = take((size_t)n * sizeof(double));
+    const size_t o_rec = take((size_t)n * sizeof(PivRec));
+    const size_t o_L = take((size_t)std::max<int64_t>(n, 1) * b * sizeof(double));
+    const size_t o_W = take((size_t)b * ld * sizeof(double));
+    const size_t o_pan = take(sizeof(K2Panel));
+    const size_t o_ctl = take(sizeof(K1Err) + 16);
+    // int metadata: iota[n] | never[n] | panel_ptr[b+1] | init_ptr[G0+1] init_rows[n] | tail_ptr[Gt+1] tail_rows[mt]
+    const size_t n_int = (size_t)(n + n + (b + 1) + (G0 + 1) + n + (Gt + 1) + mt);
+    const size_t o_int = take(n_int * sizeof(int32_t));
+    rc = ensure_dev(&B->dws, &B->dws_bytes, off);
+    if (rc) return rc;
+    rc = ensure_pinned(&B->hpin, &B->hpin_bytes, std::max(n_int * sizeof(int32_t), (size_t)n * sizeof(PivRec) + 256) + 256);
+    if (rc) return rc;
+    char* base = (char*)B->dws;
+    int32_t* hi = (int32_t*)B->hpin;
+    int32_t* h_iota = hi;
+    int32_t* h_never = h_iota + n;
+    int32_t* h_pptr = h_never + n;
+    int32_t* h_iptr = h_pptr + (b + 1);
+    int32_t* h_irows = h_iptr + (G0 + 1);
+    int32_t* h_tptr = h_irows + n;
+    int32_t* h_trows = h_tptr + (Gt + 1);
+    for (int64_t i = 0; i < n; ++i) { h_iota[i] = (int32_t)i; h_never[i] = kNever; }
+    for (int64_t i = 0; i <= b; ++i) h_pptr[i] = (int32_t)i;
+    auto deal = [](int64_t first, int64_t count, int64_t G, int32_t* ptr, int32_t* rows) {
+        ptr[0] = 0;
+        for (int64_t c = 0; c < G; ++c) ptr[c + 1] = ptr[c] + (int32_t)((count - c + G - 1) / G);
+        std::vector<int32_t> fill(ptr, ptr + G);
+        for (int64_t i = 0; i < count; ++i) rows[fill[(size_t)(i % G)]++] = (int32_t)(first + i);
+    };
+    deal(0, n, G0, h_iptr, h_irows);
+    deal(kb_end, mt, Gt, h_tptr, h_trows);
+    CUDA_TRY(cudaMemcpyAsync(base + o_int, hi, n_int * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemsetAsync(base + o_rec, 0, (size_t)n * sizeof(PivRec), st));
+    CUDA_TRY(cudaMemsetAsync(base + o_ctl, 0, sizeof(K1Err) + 16, st));
+    const int32_t* d_int = (const int32_t*)(base + o_int);
+    const int32_t* d_iota = d_int;
+    const int32_t* d_never = d_iota + n;
+    const int32_t* d_pptr = d_never + n;
+    const int32_t* d_iptr = d_pptr + (b + 1);
+    const int32_t* d_irows = d_iptr + (G0 + 1);
+    const int32_t* d_tptr = d_irows + n;
+    const int32_t* d_trows = d_tptr + (Gt + 1);
+    double* ws = (double*)(base + o_ws);
+    double* wit = (double*)(base + o_wit);
+    PivRec* recs = (PivRec*)(base + o_rec);
+    double* Lb = (double*)(base + o_L);
+    double* Wb = (double*)(base + o_W);
+    K2Panel* pan = (K2Panel*)(base + o_pan);
+    K1Err* err = (K1Err*)(base + o_ctl);
+    unsigned* abort = (unsigned*)(base + o_ctl + sizeof(K1Err));
+    const uint32_t epoch = ++B->epoch;
+
+    K1Params p{};
+    p.src[0] = d_a;
+    p.src_row0[0] = 0;
+    p.lds = lda;
+    p.ws[0] = ws;
+    p.row_wit[0] = wit;
+    p.ld = ld;
+    p.n = (int32_t)n;
+    p.n_groups = 1;
+    p.group0 = 0;
+    p.n_local_groups = 1;
+    p.sys_scope = 0;
+    p.epoch = epoch;
+    p.err = err;
+    p.chunk = (int32_t)std::min<int64_t>((int64_t)align_up((size_t)n, 2), kK1MaxChunk);
+    p.timeout_ns = 20ull * 1000000000ull;
+    p.abort_flag = abort;
+
+    CUDA_TRY(cudaEventRecord(B->ev0, st));
+    // 1. copy + initial witness + finiteness (no pivots)
+    p.ncol0 = (int32_t)n; p.n_steps = 0; p.in_place = 0; p.wit_in = nullptr;
+    p.seq = d_iota; p.row_pstep = d_never; p.pstep_offset = 0;
+    p.cta_row_ptr = d_iptr; p.cta_rows = d_irows; p.ctas_per_group = (int32_t)G0; p.rec[0] = recs;
+    cudaError_t e = k1_launch(p, fast, st);
+    if (e != cudaSuccess) return fail(MCND_ECUDA, "K2 init launch: %s", cudaGetErrorString(e));
+    // 2. panels
+    p.in_place = 1; p.wit_in = wit; p.row_pstep = d_iota; p.cta_row_ptr = d_pptr; p.ctas_per_group = (int32_t)b;
+    for (int64_t k = 0; k < n_panels; ++k) {
+        const int64_t kb = k * b, m = n - kb;
+        p.ncol0 = (int32_t)m; p.n_steps = (int32_t)(b - 1); p.seq = d_iota + kb; p.pstep_offset = (int32_t)kb;
+        p.cta_rows = d_iota + kb; p.rec[0] = recs + kb;
+        e = k1_launch(p, fast, st);
+        if (e != cudaSuccess) return fail(MCND_ECUDA, "K2 panel launch: %s", cudaGetErrorString(e));
+        e = k2_bookkeep(recs + kb, epoch, ws, ld, (int32_t)kb, (int32_t)m, pan, abort, st);
+        if (e == cudaSuccess) e = k2_make_w(ws, ld, (int32_t)kb, (int32_t)m, pan, Wb, ld, abort, st);
+        if (e == cudaSuccess) e = k2_gather_fix(ws, ld, (int32_t)(kb + b), (int32_t)(n - kb - b), pan, Lb, abort, st);
+        if (e == cudaSuccess)
+            e = k2_gemm(ws, ld, (int32_t)(kb + b), (int32_t)(n - kb - b), (int32_t)(m - b), Lb, Wb, ld, wit, abort, st);
+        if (e != cudaSuccess) return fail(MCND_ECUDA, "K2 panel kernels: %s", cudaGetErrorString(e));
+    }
+    // 3. unblocked tail (publishes the final 1x1)
+    p.ncol0 = (int32_t)mt; p.n_steps = (int32_t)(mt - 1); p.seq = d_iota + kb_end; p.pstep_offset = (int32_t)kb_end;
+    p.cta_row_ptr = d_tptr; p.cta_rows = d_trows; p.ctas_per_group = (int32_t)Gt; p.rec[0] = recs + kb_end;
+    e = k1_launch(p, fast, st);
+    if (e != cudaSuccess) return fail(MCND_ECUDA, "K2 tail launch: %s", cudaGetErrorString(e));
+    CUDA_TRY(cudaEventRecord(B->ev1, st));
+
+    PivRec* h_rec = (PivRec*)B->hpin;
+    K1Err* h_err = (K1Err*)((char*)B->hpin + align_up((size_t)n * sizeof(PivRec), 64));
+    CUDA_TRY(cudaMemcpyAsync(h_rec, recs, (size_t)n * sizeof(PivRec), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(h_err, err, sizeof(K1Err), cudaMemcpyDeviceToHost, st));
+    e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return fail(MCND_ECUDA, "blocked condensation: %s", cudaGetErrorString(e));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, B->ev0, B->ev1);
+    out->device_ms = ms;
+    if (h_err->nonfinite) return fail(MCND_EINVAL, "matrix entries must be finite (no NaN/Inf)");
+    if (h_err->error) return fail(MCND_EDEVICE, "device timeout waiting for pivot %u", h_err->err_step);
+    int64_t sing = -1;
+    for (int64_t t = 0; t < n; ++t) {
+        if (h_rec[t].flag != epoch || h_rec[t].l < 0) { sing = t; break; }
+        if (pivots_out) pivots_out[t] = h_rec[t].v;
+        if (cols_out) cols_out[t] = h_rec[t].l;
+    }
+    if (sing >= 0) {
+        out->sign = 0; out->singular = 1; out->log_abs = -INFINITY; out->singular_step = sing; out->steps = sing;
+        return MCND_OK;
+    }
+    double log_acc = 0.0;
+    int sign_acc = 1;
+    for (int64_t t = 0; t < n - 1; ++t) {
+        const int64_t m = n - t;
+        const double v = h_rec[t].v;
+        log_acc += std::log(std::fabs(v));
+        const int swap_parity = (h_rec[t].l != m - 1) ? -1 : 1;
+        const int parity = ((m - 1) % 2) ? -1 : 1;  // k_pos = 0 (top-to-bottom)
+        sign_acc *= (v > 0 ? 1 : -1) * swap_parity * parity;
+    }
+    const double vf = h_rec[n - 1].v;
+    out->sign = sign_acc * (vf > 0 ? 1 : -1);
+    out->log_abs = log_acc + std::log(std::fabs(vf));
+    out->steps = n - 1;
+    return MCND_OK;
+}
+
 // ---- multi-GPU (one process per GPU) ----
 struct DistHandle {
     int32_t rank = 0, world = 1;
@@ -728,6 +900,31 @@ int mcnd_mc_parallel(const double* h_a, int64_t n, int64_t lda, int32_t p, uint3
     return parallel_dev(d_a, n, n, p, flags, (cudaStream_t)stream, out, stats, payload_entries, row_updates,
                         owners_out);
 }
+
+int mcnd_logdet_blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, void* stream,
+                            mcnd_logdet* out, double* pivots_out, int32_t* cols_out) {
+    if (!out) return fail(MCND_EINVAL, "null out");
+    std::lock_guard<std::mutex> lk(g_mu);
+    return blocked_dev(d_a, n, lda, flags, (cudaStream_t)stream, out, pivots_out, cols_out);
+}
+
+int mcnd_logdet_blocked(const double* h_a, int64_t n, int64_t lda, uint32_t flags, void* stream, mcnd_logdet* out,
+                        double* pivots_out, int32_t* cols_out) {
+    if (!out) return fail(MCND_EINVAL, "null out");
+    clear_out(out);
+    int rc = check_shape(h_a, n, lda);
+    if (rc) return rc;
+    std::lock_guard<std::mutex> lk(g_mu);
+    int code = MCND_OK;
+    Buffers* B = buffers_for_current(&code);
+    if (!B) return code;
+    const double* d_a = nullptr;
+    rc = stage_input(*B, h_a, n, n, lda, (cudaStream_t)stream, &d_a);
+    if (rc) return rc;
+    return blocked_dev(d_a, n, n, flags, (cudaStream_t)stream, out, pivots_out, cols_out);
+}
+
+int32_t mcnd_blocked_panel(void) { return kK2B; }
 
 int mcnd_fold_mc_parallel(int64_t n, int32_t p, const double* piv_vals, const int32_t* piv_cols,
                           int64_t singular_at, const double* rem, const double* rem_wit, mcnd_logdet* out,

@@ -46,8 +46,13 @@ struct K1Params {
     PivRec* rec[kMaxGroups];         // pivot records of every group
     double* row_wit[kMaxGroups];     // per-row witnesses at exit (local groups; global row index)
     int64_t ld;
-    int32_t n;
+    int32_t n;                       // rows of the workspace (global row ids < n)
+    int32_t ncol0;                   // active width at step 0 (n for a whole logdet)
     int32_t n_steps;                 // S condensation steps
+    int32_t in_place;                // 1: rows already in ws (panel mode): no copy, witness
+                                     //    starts from wit_in[r] (blocked K2)
+    const double* wit_in;            // carried-in witnesses (in_place mode)
+    const unsigned* abort_flag;      // nullable: nonzero -> exit immediately
     int32_t n_groups;                // P
     int32_t group0;
     int32_t n_local_groups;
@@ -56,6 +61,7 @@ struct K1Params {
     uint32_t epoch;
     const int32_t* seq;              // global pivot schedule (pivot row of pivot t)
     const int32_t* row_pstep;        // pivot index of each row (kNever: never a pivot)
+    int32_t pstep_offset;            // subtracted from row_pstep (panel launches of K2)
     const int32_t* cta_row_ptr;      // [n_local_groups * ctas_per_group + 1]
     const int32_t* cta_rows;         // rows dealt to each CTA, ascending pivot index
     K1Err* err;
@@ -65,6 +71,27 @@ struct K1Params {
 
 cudaError_t k1_launch(const K1Params& p, bool fast, cudaStream_t s);
 size_t k1_smem_bytes(int chunk);
+
+// ---- K2: blocked rank-b condensation (k2_blocked.cu) ----
+constexpr int kK2B = 64;  // panel height b (rank of the trailing update)
+struct K2Panel {
+    int32_t l[kK2B];           // pivot position at its own step (layout s)
+    int32_t p[kK2B];           // pivot column in panel-start positions
+    double T[kK2B][kK2B];      // T[t][s] = u_t(p_s) for t < s (unit upper triangular)
+    int32_t n_moved;           // final positions whose source column moved
+    int32_t moved_c[kK2B];
+    int32_t moved_src[kK2B];
+};
+// All launches are asynchronous on `s`; `abort` (device) short-circuits every
+// kernel once a panel pivot failed the witness test.
+cudaError_t k2_bookkeep(const PivRec* rec, uint32_t epoch, const double* ws, int64_t ld, int32_t row0,
+                        int32_t m, K2Panel* pan, unsigned* abort, cudaStream_t s);
+cudaError_t k2_make_w(const double* ws, int64_t ld, int32_t row0, int32_t m, K2Panel* pan, double* W,
+                      int64_t ldw, const unsigned* abort, cudaStream_t s);
+cudaError_t k2_gather_fix(double* ws, int64_t ld, int32_t rbase, int32_t nrows, const K2Panel* pan, double* L,
+                          const unsigned* abort, cudaStream_t s);
+cudaError_t k2_gemm(double* ws, int64_t ld, int32_t rbase, int32_t M, int32_t N2, const double* L, const double* W,
+                    int64_t ldw, double* row_wit, const unsigned* abort, cudaStream_t s);
 
 cudaError_t k3_launch(const double* a, int64_t batch, int64_t n, int64_t stride, bool fast,
                       int32_t* sign, double* log_abs, double* pivots, cudaStream_t s);

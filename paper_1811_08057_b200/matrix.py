@@ -139,3 +139,20 @@ def config_batched_spd(batch: int = 4096, n: int = 64, seed: int = 4, ridge: flo
     a = np.matmul(x, x.transpose(0, 2, 1)) / (2 * n)
     a[:, np.arange(n), np.arange(n)] += ridge
     return a
+
+
+def config_spd_device(n: int = 32768, seed: int = 5, ridge: float = 1e-2, device: str = "cuda"):
+    """C5: A = X X^T / N + ridge*I with X in R^{N x N} iid N(0,1), generated on the
+    GPU by a seeded torch CUDA generator (row blocks of X are consumed in order,
+    i.e. "blockwise from a seed"); the Gram product is one DGEMM.  Returns a
+    float64 CUDA tensor (8.6 GB at N=32768)."""
+    import torch
+
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    x = torch.randn((n, n), dtype=torch.float64, device=device, generator=g)
+    a = x @ x.T
+    del x
+    a /= n
+    a.diagonal().add_(ridge)
+    return a

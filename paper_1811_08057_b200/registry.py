@@ -12,10 +12,10 @@ from __future__ import annotations
 
 import time
 
-from .condense import logdet_condensation
+from .condense import logdet_blocked, logdet_condensation
 from .runtime import CommStats, RunResult, mc_parallel
 
-ALGORITHMS = ("mc-serial", "mc-parallel")
+ALGORITHMS = ("mc-serial", "mc-parallel", "mc-blocked")
 REFERENCE_ONLY = ("ge-serial", "ge-parallel")
 
 
@@ -26,6 +26,10 @@ def run_algorithm(algorithm: str, a, p: int, *, fast: bool = False) -> RunResult
     if algorithm == "mc-serial":
         t0 = time.perf_counter()
         ld = logdet_condensation(a, fast=fast)
+        return RunResult(logdet=ld, stats=CommStats(), n_workers=1, total_seconds=time.perf_counter() - t0)
+    if algorithm == "mc-blocked":
+        t0 = time.perf_counter()
+        ld = logdet_blocked(a, fast=fast)
         return RunResult(logdet=ld, stats=CommStats(), n_workers=1, total_seconds=time.perf_counter() - t0)
     if algorithm in REFERENCE_ONLY:
         raise ValueError(f"algorithm {algorithm!r} is not on the GPU condensation path; use mcnd for it")
