@@ -694,6 +694,10 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
     const size_t o_L = take((size_t)std::max<int64_t>(n, 1) * b * sizeof(double));
     const size_t o_W = take((size_t)b * ld * sizeof(double));
     const size_t o_pan = take(sizeof(K2Panel));
+    const size_t o_cand = take((size_t)64 * kKPMaxG * sizeof(double2));
+    const size_t o_wrec = take((size_t)64 * kKPMaxG * sizeof(double2));
+    const size_t o_colb = take((size_t)64 * kKPMaxG * 64 * sizeof(double2));
+    const size_t o_lastb = take((size_t)64 * 64 * sizeof(double2));
     const size_t o_ctl = take(sizeof(K1Err) + 16);
     // int metadata: iota[n] | never[n] | panel_ptr[b+1] | init_ptr[G0+1] init_rows[n] | tail_ptr[Gt+1] tail_rows[mt]
     const size_t n_int = (size_t)(n + n + (b + 1) + (G0 + 1) + n + (Gt + 1) + mt);
@@ -767,22 +771,46 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
     p.cta_row_ptr = d_iptr; p.cta_rows = d_irows; p.ctas_per_group = (int32_t)G0; p.rec[0] = recs;
     cudaError_t e = k1_launch(p, fast, st);
     if (e != cudaSuccess) return fail(MCND_ECUDA, "K2 init launch: %s", cudaGetErrorString(e));
-    // 2. panels
-    p.in_place = 1; p.wit_in = wit; p.row_pstep = d_iota; p.cta_row_ptr = d_pptr; p.ctas_per_group = (int32_t)b;
+    // 2. panels: column-distributed panel factorisation, gather, DMMA trailing update
+    KPParams kp{};
+    kp.ws = ws;
+    kp.ld = ld;
+    kp.wit = wit;
+    kp.epoch = epoch;
+    kp.W = Wb;
+    kp.ldw = ld;
+    kp.pan = pan;
+    kp.abort = abort;
+    kp.cand = (double2*)(base + o_cand);
+    kp.wrec = (double2*)(base + o_wrec);
+    kp.colbuf = (double2*)(base + o_colb);
+    kp.lastbuf = (double2*)(base + o_lastb);
+    kp.err = err;
+    kp.timeout_ns = 20ull * 1000000000ull;
     for (int64_t k = 0; k < n_panels; ++k) {
         const int64_t kb = k * b, m = n - kb;
-        p.ncol0 = (int32_t)m; p.n_steps = (int32_t)(b - 1); p.seq = d_iota + kb; p.pstep_offset = (int32_t)kb;
-        p.cta_rows = d_iota + kb; p.rec[0] = recs + kb;
-        e = k1_launch(p, fast, st);
+        int64_t G = std::min<int64_t>({(int64_t)B->sms, (int64_t)kKPMaxG, std::max<int64_t>(1, m / 128)});
+        int64_t cw = 0;
+        for (;; --G) {
+            cw = (int64_t)align_up((size_t)((m + G - 1) / G), 2);
+            if (G == 1 || m - (G - 1) * cw >= b) break;
+        }
+        if (kp_smem_bytes((int)cw) > 190 * 1024) return fail(MCND_EINVAL, "blocked panel chunk too wide (n=%lld)", (long long)n);
+        kp.row0 = (int32_t)kb;
+        kp.m = (int32_t)m;
+        kp.G = (int32_t)G;
+        kp.cw = (int32_t)cw;
+        kp.rec = recs + kb;
+        kp.tag0 = (epoch << 16) ^ (uint32_t)(kb + 1);  // kb + s + 1 < 2^16 for n <= 65472
+        e = kp_launch(kp, st);
         if (e != cudaSuccess) return fail(MCND_ECUDA, "K2 panel launch: %s", cudaGetErrorString(e));
-        e = k2_bookkeep(recs + kb, epoch, ws, ld, (int32_t)kb, (int32_t)m, pan, abort, st);
-        if (e == cudaSuccess) e = k2_make_w(ws, ld, (int32_t)kb, (int32_t)m, pan, Wb, ld, abort, st);
-        if (e == cudaSuccess) e = k2_gather_fix(ws, ld, (int32_t)(kb + b), (int32_t)(n - kb - b), pan, Lb, abort, st);
+        e = k2_gather_fix(ws, ld, (int32_t)(kb + b), (int32_t)(n - kb - b), pan, Lb, abort, st);
         if (e == cudaSuccess)
             e = k2_gemm(ws, ld, (int32_t)(kb + b), (int32_t)(n - kb - b), (int32_t)(m - b), Lb, Wb, ld, wit, abort, st);
         if (e != cudaSuccess) return fail(MCND_ECUDA, "K2 panel kernels: %s", cudaGetErrorString(e));
     }
     // 3. unblocked tail (publishes the final 1x1)
+    p.in_place = 1; p.wit_in = wit; p.row_pstep = d_iota;
     p.ncol0 = (int32_t)mt; p.n_steps = (int32_t)(mt - 1); p.seq = d_iota + kb_end; p.pstep_offset = (int32_t)kb_end;
     p.cta_row_ptr = d_tptr; p.cta_rows = d_trows; p.ctas_per_group = (int32_t)Gt; p.rec[0] = recs + kb_end;
     e = k1_launch(p, fast, st);

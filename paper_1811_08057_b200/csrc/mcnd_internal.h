@@ -82,12 +82,37 @@ struct K2Panel {
     int32_t moved_c[kK2B];
     int32_t moved_src[kK2B];
 };
+// Column-distributed panel factorisation (k2_panel.cu).  Every exchanged
+// value travels in a 16-byte record {value, tag|aux} written with ONE 16-byte
+// store, so readers poll the records themselves (no fences, no counters).
+struct KPParams {
+    double* ws;
+    int64_t ld;
+    int32_t row0;             // first panel row
+    int32_t m;                // active width at panel start
+    int32_t G;                // CTAs (column chunks)
+    int32_t cw;               // chunk width (columns per CTA)
+    const double* wit;        // running witnesses, global row index
+    PivRec* rec;              // this panel's 64 pivot records
+    uint32_t epoch;
+    uint32_t tag0;            // record tag of step s is tag0 + s (unique per call and panel)
+    double* W;                // out: T^{-1} U, 64 x (m - 64), row stride ldw
+    int64_t ldw;
+    K2Panel* pan;             // out: panel-start pivot columns, moved columns
+    unsigned* abort;
+    double2* cand;            // [64][G]   {candidate value, pos | tag}
+    double2* wrec;            // [64][G]   {running max of the pivot row, tag}
+    double2* colbuf;          // [64][G][64] {candidate column values, tag}
+    double2* lastbuf;         // [64][64]  {last active column values, tag}
+    K1Err* err;
+    unsigned long long timeout_ns;
+};
+constexpr int kKPMaxG = 160;
+cudaError_t kp_launch(const KPParams& p, cudaStream_t s);
+size_t kp_smem_bytes(int cw);
+
 // All launches are asynchronous on `s`; `abort` (device) short-circuits every
 // kernel once a panel pivot failed the witness test.
-cudaError_t k2_bookkeep(const PivRec* rec, uint32_t epoch, const double* ws, int64_t ld, int32_t row0,
-                        int32_t m, K2Panel* pan, unsigned* abort, cudaStream_t s);
-cudaError_t k2_make_w(const double* ws, int64_t ld, int32_t row0, int32_t m, K2Panel* pan, double* W,
-                      int64_t ldw, const unsigned* abort, cudaStream_t s);
 cudaError_t k2_gather_fix(double* ws, int64_t ld, int32_t rbase, int32_t nrows, const K2Panel* pan, double* L,
                           const unsigned* abort, cudaStream_t s);
 cudaError_t k2_gemm(double* ws, int64_t ld, int32_t rbase, int32_t M, int32_t N2, const double* L, const double* W,
