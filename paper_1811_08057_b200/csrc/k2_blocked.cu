@@ -30,38 +30,96 @@ namespace {
 
 constexpr int kB = kK2B;
 
-// One warp per trailing row.
+// One warp per trailing row: L[r, 0:K] = A[r, P], then the moved columns.
+template <int K>
 __global__ void k2_gather_fix_kernel(double* __restrict__ ws, int64_t ld, int32_t rbase, int32_t nrows,
-                                     const K2Panel* __restrict__ pan, double* __restrict__ L,
+                                     const K2Gather* __restrict__ gp, double* __restrict__ L,
                                      const unsigned* __restrict__ abort) {
     if (*(volatile const unsigned*)abort) return;
     const int lane = threadIdx.x & 31;
     const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (i >= nrows) return;
     double* row = ws + (int64_t)(rbase + i) * ld;
-    const double x0 = row[pan->p[lane]];
-    const double x1 = row[pan->p[lane + 32]];
+    constexpr int KL = K / 32;
+    double x[KL];
+#pragma unroll
+    for (int k = 0; k < KL; ++k) x[k] = row[gp->P[lane + 32 * k]];
+    const int nm = gp->n_moved;
+    double v[KL];
+#pragma unroll
+    for (int k = 0; k < KL; ++k) v[k] = (lane + 32 * k < nm) ? row[gp->moved_src[lane + 32 * k]] : 0.0;
     __syncwarp();
-    L[(int64_t)i * kB + lane] = x0;
-    L[(int64_t)i * kB + lane + 32] = x1;
-    const int nm = pan->n_moved;
-    double v = 0.0;
-    if (lane < nm) v = row[pan->moved_src[lane]];
-    double v2 = 0.0;
-    if (lane + 32 < nm) v2 = row[pan->moved_src[lane + 32]];
-    __syncwarp();
-    if (lane < nm) row[pan->moved_c[lane]] = v;
-    if (lane + 32 < nm) row[pan->moved_c[lane + 32]] = v2;
+#pragma unroll
+    for (int k = 0; k < KL; ++k) L[(int64_t)i * K + lane + 32 * k] = x[k];
+#pragma unroll
+    for (int k = 0; k < KL; ++k)
+        if (lane + 32 * k < nm) row[gp->moved_c[lane + 32 * k]] = v[k];
 }
 
-// ---- DMMA GEMM: C[M x N2] (rows rbase.., in ws) -= L[M x 64] * W[64 x N2] ----
-constexpr int BM = 64, BN = 128, BK = kB;
-constexpr int LDLS = BK + 4;   // padded smem strides (conflict-free fragment loads)
+__device__ __forceinline__ int pi_of(const K2Gather* g, int x) {
+    for (int k = 0; k < g->n_moved; ++k)
+        if (g->moved_c[k] == x) return g->moved_src[k];
+    return x;
+}
+
+// Single CTA (256 threads).  g0: panel k (layout width m), g1: panel k+1 (layout
+// width m-64).  Wc rows 0..63 = W_k (width m-64 layout), rows 64..127 = W_{k+1}.
+__global__ void k2_pair_prep_kernel(const K2Gather* __restrict__ g0, const K2Gather* __restrict__ g1, int32_t m,
+                                    double* __restrict__ Wc, int64_t ldw, double* __restrict__ Wp,
+                                    K2Gather* __restrict__ gpair, const unsigned* __restrict__ abort) {
+    if (*(volatile const unsigned*)abort) return;
+    const int tid = threadIdx.x;
+    __shared__ int s_cand[4 * kK2B];
+    __shared__ int s_nc, s_nm;
+    // (a) Wp[s][s'] = W_k[s][P1[s']] (before W_k's columns are permuted)
+    for (int e = tid; e < kK2B * kK2B; e += blockDim.x) {
+        const int sr = e / kK2B, sp = e % kK2B;
+        Wp[sr * kK2B + sp] = Wc[(int64_t)sr * ldw + g1->P[sp]];
+    }
+    // (b) composite gather columns: panel k's pivots, then panel k+1's pivots mapped to width m
+    if (tid < kK2B) {
+        gpair->P[tid] = g0->P[tid];
+        gpair->P[kK2B + tid] = pi_of(g0, g1->P[tid]);
+        gpair->l[tid] = g1->l[tid];
+    }
+    if (tid == 0) { s_nc = 0; s_nm = 0; }
+    __syncthreads();
+    // candidate moved columns of the pair: targets of either panel inside the final width
+    const int wf = m - 2 * kK2B;
+    if (tid < g1->n_moved && g1->moved_c[tid] < wf) s_cand[atomicAdd(&s_nc, 1)] = g1->moved_c[tid];
+    if (tid < g0->n_moved && g0->moved_c[tid] < wf) s_cand[atomicAdd(&s_nc, 1)] = g0->moved_c[tid];
+    __syncthreads();
+    if (tid < s_nc) {
+        const int c = s_cand[tid];
+        bool first = true;
+        for (int k = 0; k < tid && first; ++k) first = s_cand[k] != c;
+        if (first) {
+            const int src = pi_of(g0, pi_of(g1, c));
+            if (src != c) {
+                const int k = atomicAdd(&s_nm, 1);
+                gpair->moved_c[k] = c;
+                gpair->moved_src[k] = src;
+            }
+        }
+    }
+    __syncthreads();
+    if (tid == 0) gpair->n_moved = s_nm;
+    // (c) W_k's columns into the pair's final layout: column c <- column pi_{k+1}(c)
+    //     (sources lie in the tail [m-128, m-64), never written)
+    const int nm1 = g1->n_moved;
+    for (int e = tid; e < kK2B * nm1; e += blockDim.x) {
+        const int sr = e / nm1, k = e % nm1;
+        const int c = g1->moved_c[k];
+        if (c < wf) Wc[(int64_t)sr * ldw + c] = Wc[(int64_t)sr * ldw + g1->moved_src[k]];
+    }
+}
+
+// ---- DMMA GEMM: C[M x N2] (rows rbase.., in ws) -= L[M x K] * W[K x N2], K = 64 or 128 ----
+constexpr int BM = 64, BN = 128, BKS = 64;   // tile rows / cols, K per pipeline stage
+constexpr int LDLS = BKS + 4;                // padded smem strides (conflict-free fragment loads)
 constexpr int LDWS = BN + 8;
-#ifndef MCND_GEMM_VARIANT
-#define MCND_GEMM_VARIANT 0  // microbenchmark knob: 1 = no C traffic, 2 = operands loaded once
-#endif
-constexpr int kGThreads = 512;  // 16 warps: 2 (M) x 8 (N), warp tile 32 x 16
+constexpr int kStage = BM * LDLS + BKS * LDWS;  // doubles per stage buffer
+constexpr int kGThreads = 512;               // 16 warps: 2 (M) x 8 (N), warp tile 32 x 16
 constexpr int WN = 8, WTN = 16, NJ = WTN / 8;
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
@@ -76,16 +134,20 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 }
 
 // Persistent: one CTA per SM walks a contiguous range of 64 x 128 output tiles
-// (row-block major, so L is reused and W streams from L2).  Software pipeline
-// per tile: operands of tile t+1 go to the other shared-memory buffer with
-// cp.async and the C fragments of tile t+1 are loaded into registers while the
-// DMMAs of tile t run; stores are fire-and-forget.  Row maxima (witness) are
-// kept in registers and flushed with one atomicMax per row-block change.
+// (row-block major, so L is reused from L2 and W streams from L2).  K is
+// consumed in stages of 64: the operands of stage j+1 (next K half or next
+// tile) are copied into the other shared-memory buffer with cp.async while the
+// DMMAs of stage j run, and the C fragments of tile t+1 are loaded into
+// registers during tile t; stores are streaming and fire-and-forget.  Row
+// maxima (the running witness) stay in registers and are flushed with one
+// atomicMax per row-block change (skipped when wit == nullptr).
+template <int K>
 __global__ void __launch_bounds__(kGThreads, 1) k2_gemm_kernel(double* __restrict__ ws, int64_t ld, int32_t rbase,
                                                                int32_t M, int32_t N2, const double* __restrict__ L,
-                                                               const double* __restrict__ W, int64_t ldw,
+                                                               int64_t ldl, const double* __restrict__ W, int64_t ldw,
                                                                unsigned long long* __restrict__ wit,
                                                                const unsigned* __restrict__ abort) {
+    constexpr int NS = K / BKS;  // stages per tile
     extern __shared__ __align__(16) double sh[];
     if (*(volatile const unsigned*)abort) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -96,23 +158,24 @@ __global__ void __launch_bounds__(kGThreads, 1) k2_gemm_kernel(double* __restric
     const int64_t t_begin = T * blockIdx.x / gridDim.x, t_end = T * (blockIdx.x + 1) / gridDim.x;
     if (t_begin >= t_end) return;
 
-    auto Ls = [&](int buf) { return sh + buf * (BM * LDLS + BK * LDWS); };
-    auto Ws = [&](int buf) { return sh + buf * (BM * LDLS + BK * LDWS) + BM * LDLS; };
-    auto load_operands = [&](int64_t t, int buf) {
+    // stage j of this CTA = (tile t_begin + j / NS, K half j % NS), buffer j & 1
+    auto load_stage = [&](int64_t j) {
+        const int64_t t = t_begin + j / NS;
+        const int kh = (int)(j % NS);
         const int row0 = (int)(t / ntn) * BM, col0 = (int)(t % ntn) * BN;
-        double* ls = Ls(buf);
-        double* wsm = Ws(buf);
-        for (int i = tid; i < BM * (BK / 2); i += kGThreads) {
-            const int r = i / (BK / 2), c2 = i % (BK / 2);
+        double* ls = sh + (j & 1) * kStage;
+        double* wsm = ls + BM * LDLS;
+        for (int i = tid; i < BM * (BKS / 2); i += kGThreads) {
+            const int r = i / (BKS / 2), c2 = i % (BKS / 2);
             double* dst = ls + r * LDLS + 2 * c2;
-            if (row0 + r < M) cp_async16(dst, L + (int64_t)(row0 + r) * BK + 2 * c2);
+            if (row0 + r < M) cp_async16(dst, L + (int64_t)(row0 + r) * ldl + kh * BKS + 2 * c2);
             else { dst[0] = 0.0; dst[1] = 0.0; }
         }
-        for (int i = tid; i < BK * (BN / 2); i += kGThreads) {
+        for (int i = tid; i < BKS * (BN / 2); i += kGThreads) {
             const int k = i / (BN / 2), c2 = i % (BN / 2);
             const int col = col0 + 2 * c2;
             double* dst = wsm + k * LDWS + 2 * c2;
-            if (col < N2) cp_async16(dst, W + (int64_t)k * ldw + col);
+            if (col < N2) cp_async16(dst, W + (int64_t)(kh * BKS + k) * ldw + col);
             else { dst[0] = 0.0; dst[1] = 0.0; }
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
@@ -127,7 +190,7 @@ __global__ void __launch_bounds__(kGThreads, 1) k2_gemm_kernel(double* __restric
 #pragma unroll
             for (int j = 0; j < NJ; ++j) {
                 const int c = col0 + wn * WTN + j * 8 + 2 * q;
-                if (MCND_GEMM_VARIANT != 1 && MCND_GEMM_VARIANT != 4 && r < M && c < N2) {
+                if (r < M && c < N2) {
                     const double2 v = __ldcs(reinterpret_cast<const double2*>(crow + c));
                     cn[i][j][0] = v.x;
                     cn[i][j][1] = v.y;
@@ -139,61 +202,62 @@ __global__ void __launch_bounds__(kGThreads, 1) k2_gemm_kernel(double* __restric
         }
     };
 
-    load_operands(t_begin, 0);
+    const int64_t nstages = (t_end - t_begin) * NS;
+    load_stage(0);
     load_c(t_begin);
     double rmx[4] = {0.0, 0.0, 0.0, 0.0};
-    for (int64_t t = t_begin; t < t_end; ++t) {
-        const int buf = (int)((t - t_begin) & 1);
-        const int bm = (int)(t / ntn);
-        const int row0 = bm * BM, col0 = (int)(t % ntn) * BN;
+    double acc[4][NJ][2];
+    for (int64_t j = 0; j < nstages; ++j) {
+        const int64_t t = t_begin + j / NS;
+        const int kh = (int)(j % NS);
         asm volatile("cp.async.wait_all;" ::: "memory");
-        __syncthreads();
-        double acc[4][NJ][2];
+        __syncthreads();  // stage j landed; everybody is done with buffer (j+1)&1
+        if (kh == 0) {
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+            for (int i = 0; i < 4; ++i)
 #pragma unroll
-            for (int j = 0; j < NJ; ++j) { acc[i][j][0] = cn[i][j][0]; acc[i][j][1] = cn[i][j][1]; }
-        if (t + 1 < t_end) {
-            if (MCND_GEMM_VARIANT != 2 || t == t_begin) load_operands(t + 1, buf ^ 1);
-            load_c(t + 1);
+                for (int jj = 0; jj < NJ; ++jj) { acc[i][jj][0] = cn[i][jj][0]; acc[i][jj][1] = cn[i][jj][1]; }
         }
-        const double* ls = Ls(buf);
-        const double* wsm = Ws(buf);
+        if (j + 1 < nstages) load_stage(j + 1);
+        if (kh == 0 && t + 1 < t_end) load_c(t + 1);
+        const double* ls = sh + (j & 1) * kStage;
+        const double* wsm = ls + BM * LDLS;
 #pragma unroll 4
-        for (int k0 = 0; k0 < BK; k0 += 4) {
+        for (int k0 = 0; k0 < BKS; k0 += 4) {
             double a[4], b[NJ];
 #pragma unroll
             for (int i = 0; i < 4; ++i) a[i] = -ls[(wm * 32 + i * 8 + g) * LDLS + k0 + q];
 #pragma unroll
-            for (int j = 0; j < NJ; ++j) b[j] = wsm[(k0 + q) * LDWS + wn * WTN + j * 8 + g];
+            for (int jj = 0; jj < NJ; ++jj) b[jj] = wsm[(k0 + q) * LDWS + wn * WTN + jj * 8 + g];
 #pragma unroll
             for (int i = 0; i < 4; ++i)
 #pragma unroll
-                for (int j = 0; j < NJ; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+                for (int jj = 0; jj < NJ; ++jj) dmma(acc[i][jj][0], acc[i][jj][1], a[i], b[jj]);
         }
-        // epilogue: store, fold |.| into the per-row maxima
+        if (kh != NS - 1) continue;
+        // epilogue of tile t: store, fold |.| into the per-row maxima
+        const int bm = (int)(t / ntn);
+        const int row0 = bm * BM, col0 = (int)(t % ntn) * BN;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             const int r = row0 + wm * 32 + i * 8 + g;
             double* crow = ws + (int64_t)(rbase + r) * ld;
 #pragma unroll
-            for (int j = 0; j < NJ; ++j) {
-                const int c = col0 + wn * WTN + j * 8 + 2 * q;
-                if (MCND_GEMM_VARIANT == 1 || MCND_GEMM_VARIANT == 3)
-                    rmx[i] = fmax(rmx[i], fabs(acc[i][j][0] + acc[i][j][1]));
-                if (MCND_GEMM_VARIANT != 1 && MCND_GEMM_VARIANT != 3 && r < M && c < N2) {
+            for (int jj = 0; jj < NJ; ++jj) {
+                const int c = col0 + wn * WTN + jj * 8 + 2 * q;
+                if (r < M && c < N2) {
                     if (c + 1 < N2) {
-                        __stcs(reinterpret_cast<double2*>(crow + c), make_double2(acc[i][j][0], acc[i][j][1]));
-                        rmx[i] = fmax(rmx[i], fmax(fabs(acc[i][j][0]), fabs(acc[i][j][1])));
+                        __stcs(reinterpret_cast<double2*>(crow + c), make_double2(acc[i][jj][0], acc[i][jj][1]));
+                        rmx[i] = fmax(rmx[i], fmax(fabs(acc[i][jj][0]), fabs(acc[i][jj][1])));
                     } else {
-                        crow[c] = acc[i][j][0];
-                        rmx[i] = fmax(rmx[i], fabs(acc[i][j][0]));
+                        crow[c] = acc[i][jj][0];
+                        rmx[i] = fmax(rmx[i], fabs(acc[i][jj][0]));
                     }
                 }
             }
         }
         const bool flush = (t + 1 == t_end) || ((int)((t + 1) / ntn) != bm);
-        if (flush) {
+        if (flush && wit) {
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 double mx = rmx[i];
@@ -209,21 +273,33 @@ __global__ void __launch_bounds__(kGThreads, 1) k2_gemm_kernel(double* __restric
 
 }  // namespace
 
-cudaError_t k2_gather_fix(double* ws, int64_t ld, int32_t rbase, int32_t nrows, const K2Panel* pan, double* L,
-                          const unsigned* abort, cudaStream_t s) {
+cudaError_t k2_gather_fix(double* ws, int64_t ld, int32_t rbase, int32_t nrows, int32_t K, const K2Gather* gp,
+                          double* L, const unsigned* abort, cudaStream_t s) {
     if (nrows <= 0) return cudaSuccess;
     const int warps = 8;
-    k2_gather_fix_kernel<<<(nrows + warps - 1) / warps, warps * 32, 0, s>>>(ws, ld, rbase, nrows, pan, L, abort);
+    const dim3 grid((nrows + warps - 1) / warps);
+    if (K == 64) k2_gather_fix_kernel<64><<<grid, warps * 32, 0, s>>>(ws, ld, rbase, nrows, gp, L, abort);
+    else if (K == 128) k2_gather_fix_kernel<128><<<grid, warps * 32, 0, s>>>(ws, ld, rbase, nrows, gp, L, abort);
+    else return cudaErrorInvalidValue;
     return cudaGetLastError();
 }
 
-cudaError_t k2_gemm(double* ws, int64_t ld, int32_t rbase, int32_t M, int32_t N2, const double* L, const double* W,
-                    int64_t ldw, double* row_wit, const unsigned* abort, cudaStream_t s) {
+cudaError_t k2_pair_prep(const K2Gather* g0, const K2Gather* g1, int32_t m, double* Wc, int64_t ldw, double* Wp,
+                         K2Gather* gpair, const unsigned* abort, cudaStream_t s) {
+    k2_pair_prep_kernel<<<1, 256, 0, s>>>(g0, g1, m, Wc, ldw, Wp, gpair, abort);
+    return cudaGetLastError();
+}
+
+cudaError_t k2_gemm(double* ws, int64_t ld, int32_t rbase, int32_t M, int32_t N2, int32_t K, const double* L,
+                    int64_t ldl, const double* W, int64_t ldw, double* row_wit, const unsigned* abort, cudaStream_t s) {
     if (M <= 0 || N2 <= 0) return cudaSuccess;
-    const size_t smem = (size_t)2 * (BM * LDLS + BK * LDWS) * sizeof(double);
+    if (K != 64 && K != 128) return cudaErrorInvalidValue;
+    const size_t smem = (size_t)2 * kStage * sizeof(double);
     static int sms = 0;
     if (!sms) {
-        cudaError_t e = cudaFuncSetAttribute(k2_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaError_t e = cudaFuncSetAttribute(k2_gemm_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(k2_gemm_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         int dev = 0;
         cudaGetDevice(&dev);
@@ -231,8 +307,9 @@ cudaError_t k2_gemm(double* ws, int64_t ld, int32_t rbase, int32_t M, int32_t N2
     }
     const int64_t tiles = (int64_t)((N2 + BN - 1) / BN) * ((M + BM - 1) / BM);
     const int grid = (int)std::min<int64_t>(tiles, sms);
-    k2_gemm_kernel<<<grid, kGThreads, smem, s>>>(ws, ld, rbase, M, N2, L, W, ldw,
-                                                 reinterpret_cast<unsigned long long*>(row_wit), abort);
+    auto* w = reinterpret_cast<unsigned long long*>(row_wit);
+    if (K == 64) k2_gemm_kernel<64><<<grid, kGThreads, smem, s>>>(ws, ld, rbase, M, N2, L, ldl, W, ldw, w, abort);
+    else k2_gemm_kernel<128><<<grid, kGThreads, smem, s>>>(ws, ld, rbase, M, N2, L, ldl, W, ldw, w, abort);
     return cudaGetLastError();
 }
 

@@ -341,7 +341,7 @@ __global__ void __launch_bounds__(kThreads, 1) kp_panel_kernel(const KPParams p)
         const int s = tid;
         int pos = s_l[s];
         for (int j = s - 1; j >= 0; --j) pos = (pos == s_l[j]) ? (m - j - 1) : pos;
-        p.pan->p[s] = pos;
+        p.pan->P[s] = pos;
         p.pan->l[s] = s_l[s];
         const int c = s_l[s];
         bool first = c < m - kB;

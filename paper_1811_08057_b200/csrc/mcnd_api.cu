@@ -691,9 +691,10 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
     const size_t o_ws = take((size_t)n * ld * sizeof(double));
     const size_t o_wit = take((size_t)n * sizeof(double));
     const size_t o_rec = take((size_t)n * sizeof(PivRec));
-    const size_t o_L = take((size_t)std::max<int64_t>(n, 1) * b * sizeof(double));
-    const size_t o_W = take((size_t)b * ld * sizeof(double));
-    const size_t o_pan = take(sizeof(K2Panel));
+    const size_t o_L = take((size_t)std::max<int64_t>(n, 1) * 2 * b * sizeof(double));
+    const size_t o_W = take((size_t)2 * b * ld * sizeof(double));
+    const size_t o_pan = take(3 * sizeof(K2Gather));
+    const size_t o_Wp = take((size_t)b * b * sizeof(double));
     const size_t o_cand = take((size_t)64 * kKPMaxG * sizeof(double2));
     const size_t o_wrec = take((size_t)64 * kKPMaxG * sizeof(double2));
     const size_t o_colb = take((size_t)64 * kKPMaxG * 64 * sizeof(double2));
@@ -741,7 +742,10 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
     PivRec* recs = (PivRec*)(base + o_rec);
     double* Lb = (double*)(base + o_L);
     double* Wb = (double*)(base + o_W);
-    K2Panel* pan = (K2Panel*)(base + o_pan);
+    K2Gather* gp0 = (K2Gather*)(base + o_pan);
+    K2Gather* gp1 = gp0 + 1;
+    K2Gather* gpair = gp0 + 2;
+    double* Wp = (double*)(base + o_Wp);
     K1Err* err = (K1Err*)(base + o_ctl);
     unsigned* abort = (unsigned*)(base + o_ctl + sizeof(K1Err));
     const uint32_t epoch = ++B->epoch;
@@ -777,9 +781,7 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
     kp.ld = ld;
     kp.wit = wit;
     kp.epoch = epoch;
-    kp.W = Wb;
     kp.ldw = ld;
-    kp.pan = pan;
     kp.abort = abort;
     kp.cand = (double2*)(base + o_cand);
     kp.wrec = (double2*)(base + o_wrec);
@@ -787,26 +789,54 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
     kp.lastbuf = (double2*)(base + o_lastb);
     kp.err = err;
     kp.timeout_ns = 20ull * 1000000000ull;
-    for (int64_t k = 0; k < n_panels; ++k) {
-        const int64_t kb = k * b, m = n - kb;
+    auto run_kp = [&](int64_t kb, K2Gather* gp, double* Wout) -> cudaError_t {
+        const int64_t m = n - kb;
         int64_t G = std::min<int64_t>({(int64_t)B->sms, (int64_t)kKPMaxG, std::max<int64_t>(1, m / 128)});
         int64_t cw = 0;
         for (;; --G) {
             cw = (int64_t)align_up((size_t)((m + G - 1) / G), 2);
             if (G == 1 || m - (G - 1) * cw >= b) break;
         }
-        if (kp_smem_bytes((int)cw) > 190 * 1024) return fail(MCND_EINVAL, "blocked panel chunk too wide (n=%lld)", (long long)n);
+        if (kp_smem_bytes((int)cw) > 190 * 1024) return cudaErrorInvalidValue;
         kp.row0 = (int32_t)kb;
         kp.m = (int32_t)m;
         kp.G = (int32_t)G;
         kp.cw = (int32_t)cw;
         kp.rec = recs + kb;
+        kp.pan = gp;
+        kp.W = Wout;
         kp.tag0 = (epoch << 16) ^ (uint32_t)(kb + 1);  // kb + s + 1 < 2^16 for n <= 65472
-        e = kp_launch(kp, st);
-        if (e != cudaSuccess) return fail(MCND_ECUDA, "K2 panel launch: %s", cudaGetErrorString(e));
-        e = k2_gather_fix(ws, ld, (int32_t)(kb + b), (int32_t)(n - kb - b), pan, Lb, abort, st);
-        if (e == cudaSuccess)
-            e = k2_gemm(ws, ld, (int32_t)(kb + b), (int32_t)(n - kb - b), (int32_t)(m - b), Lb, Wb, ld, wit, abort, st);
+        return kp_launch(kp, st);
+    };
+    // Panels go in pairs: panel k, then its update of panel k+1's 64 rows, panel
+    // k+1, and ONE rank-128 trailing update (half the C traffic of two rank-64
+    // updates).  L of the pair = [A[R, P_k], A'[R, P_{k+1}]] where the second
+    // half is corrected for panel k by a 64-wide DMMA update: L1 -= L0 * W_k[:, P_{k+1}].
+    const bool pairs = env_long("MCND_K2_PAIRS", 1) != 0;
+    int64_t k = 0;
+    while (k < n_panels) {
+        const int64_t kb = k * b, m = n - kb;
+        if (pairs && k + 1 < n_panels) {
+            e = run_kp(kb, gp0, Wb);
+            if (e == cudaSuccess) e = k2_gather_fix(ws, ld, (int32_t)(kb + b), (int32_t)b, 64, gp0, Lb, abort, st);
+            if (e == cudaSuccess)
+                e = k2_gemm(ws, ld, (int32_t)(kb + b), (int32_t)b, (int32_t)(m - b), 64, Lb, 64, Wb, ld, wit, abort, st);
+            if (e == cudaSuccess) e = run_kp(kb + b, gp1, Wb + b * ld);
+            if (e == cudaSuccess) e = k2_pair_prep(gp0, gp1, (int32_t)m, Wb, ld, Wp, gpair, abort, st);
+            const int32_t nr = (int32_t)(n - kb - 2 * b);
+            if (e == cudaSuccess) e = k2_gather_fix(ws, ld, (int32_t)(kb + 2 * b), nr, 128, gpair, Lb, abort, st);
+            if (e == cudaSuccess)  // L[:, 64:128] -= L[:, 0:64] * Wp   (no witness: L is scratch)
+                e = k2_gemm(Lb + b, 2 * b, 0, nr, (int32_t)b, 64, Lb, 2 * b, Wp, b, nullptr, abort, st);
+            if (e == cudaSuccess)
+                e = k2_gemm(ws, ld, (int32_t)(kb + 2 * b), nr, (int32_t)(m - 2 * b), 128, Lb, 2 * b, Wb, ld, wit, abort, st);
+            k += 2;
+        } else {
+            e = run_kp(kb, gp0, Wb);
+            if (e == cudaSuccess) e = k2_gather_fix(ws, ld, (int32_t)(kb + b), (int32_t)(n - kb - b), 64, gp0, Lb, abort, st);
+            if (e == cudaSuccess)
+                e = k2_gemm(ws, ld, (int32_t)(kb + b), (int32_t)(n - kb - b), (int32_t)(m - b), 64, Lb, 64, Wb, ld, wit, abort, st);
+            k += 1;
+        }
         if (e != cudaSuccess) return fail(MCND_ECUDA, "K2 panel kernels: %s", cudaGetErrorString(e));
     }
     // 3. unblocked tail (publishes the final 1x1)

@@ -74,13 +74,15 @@ size_t k1_smem_bytes(int chunk);
 
 // ---- K2: blocked rank-b condensation (k2_blocked.cu) ----
 constexpr int kK2B = 64;  // panel height b (rank of the trailing update)
-struct K2Panel {
-    int32_t l[kK2B];           // pivot position at its own step (layout s)
-    int32_t p[kK2B];           // pivot column in panel-start positions
-    double T[kK2B][kK2B];      // T[t][s] = u_t(p_s) for t < s (unit upper triangular)
-    int32_t n_moved;           // final positions whose source column moved
-    int32_t moved_c[kK2B];
-    int32_t moved_src[kK2B];
+// Gather descriptor of a trailing update: the K multiplier columns P (positions
+// in the layout the trailing rows are in) and the final columns whose source
+// column moved (composition of the column exchanges of condense.py:104-107).
+struct K2Gather {
+    int32_t P[2 * kK2B];
+    int32_t l[kK2B];           // pivot positions of the producing panel (layout of each step)
+    int32_t n_moved;
+    int32_t moved_c[2 * kK2B];
+    int32_t moved_src[2 * kK2B];
 };
 // Column-distributed panel factorisation (k2_panel.cu).  Every exchanged
 // value travels in a 16-byte record {value, tag|aux} written with ONE 16-byte
@@ -98,7 +100,7 @@ struct KPParams {
     uint32_t tag0;            // record tag of step s is tag0 + s (unique per call and panel)
     double* W;                // out: T^{-1} U, 64 x (m - 64), row stride ldw
     int64_t ldw;
-    K2Panel* pan;             // out: panel-start pivot columns, moved columns
+    K2Gather* pan;            // out: panel-start pivot columns (P[0..63]), moved columns
     unsigned* abort;
     double2* cand;            // [64][G]   {candidate value, pos | tag}
     double2* wrec;            // [64][G]   {running max of the pivot row, tag}
@@ -113,10 +115,19 @@ size_t kp_smem_bytes(int cw);
 
 // All launches are asynchronous on `s`; `abort` (device) short-circuits every
 // kernel once a panel pivot failed the witness test.
-cudaError_t k2_gather_fix(double* ws, int64_t ld, int32_t rbase, int32_t nrows, const K2Panel* pan, double* L,
-                          const unsigned* abort, cudaStream_t s);
-cudaError_t k2_gemm(double* ws, int64_t ld, int32_t rbase, int32_t M, int32_t N2, const double* L, const double* W,
-                    int64_t ldw, double* row_wit, const unsigned* abort, cudaStream_t s);
+// Per trailing row: L[r, 0:K] = A[r, P[0:K]], then A[r, c] = A[r, src] for the moved columns.
+cudaError_t k2_gather_fix(double* ws, int64_t ld, int32_t rbase, int32_t nrows, int32_t K, const K2Gather* gp,
+                          double* L, const unsigned* abort, cudaStream_t s);
+// Panel pair (two 64-row panels, one rank-128 trailing update): from the two panels'
+// descriptors build the composite gather descriptor, Wp[s][s'] = W0[s][P1[s']] and
+// permute W0's columns into the final layout of the pair (one CTA).
+cudaError_t k2_pair_prep(const K2Gather* g0, const K2Gather* g1, int32_t m, double* Wc, int64_t ldw, double* Wp,
+                         K2Gather* gpair, const unsigned* abort, cudaStream_t s);
+
+// C[M x N2] (rows rbase.. of ws) -= L[M x K] W[K x N2], K in {64, 128}; L row stride ldl;
+// row_wit (nullable) receives the running max |C| per row.
+cudaError_t k2_gemm(double* ws, int64_t ld, int32_t rbase, int32_t M, int32_t N2, int32_t K, const double* L,
+                    int64_t ldl, const double* W, int64_t ldw, double* row_wit, const unsigned* abort, cudaStream_t s);
 
 cudaError_t k3_launch(const double* a, int64_t batch, int64_t n, int64_t stride, bool fast,
                       int32_t* sign, double* log_abs, double* pivots, cudaStream_t s);
