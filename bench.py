@@ -5,8 +5,8 @@ Default workload (BASELINE.json metric): C3, one dense N=8000 FP64 matrix with
 iid U[-1,1] entries (numpy PCG64 seed 3), log-determinant by condensation.
 A "step" is one full log-determinant of that matrix.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3|c1|c2|c4]
-                    [--fast] [--impl mc|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3|c1|c2|c4|c5]
+                    [--method unblocked|blocked] [--fast] [--impl mc|reference]
 
 value      effective GFLOP/s = (2 N^3 / 3) / (device time per step), input resident
            in HBM, CUDA events on the launching stream (max over ranks).
@@ -44,7 +44,9 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "c4"])
+    ap.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--method", default=None, choices=["unblocked", "blocked"],
+                    help="condensation variant (default: unblocked for c1-c3, blocked for c5)")
     ap.add_argument("--fast", action="store_true", help="FMA update (default: reference-exact arithmetic)")
     ap.add_argument("--impl", default="mc", choices=["mc", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -72,7 +74,14 @@ def workload(cfg: str):
         return "C3 dense U[-1,1] N=8000 seed 3", M.config_uniform(8000, 3), 8000
     if cfg == "c4":
         return "C4 batched 4096 x SPD 64x64 seed 4", M.config_batched_spd(4096, 64, 4), 64
+    if cfg == "c5":
+        return ("C5 SPD X X^T/N + 1e-2 I, N=32768 (X from a seeded CUDA generator, seed 5)",
+                M.config_spd_device(32768, 5), 32768)
     raise ValueError(cfg)
+
+
+FP64_PEAK_TFLOPS = 35.47  # cuBLAS DGEMM 8192^3 measured on this pool (profiles/r1_fp64_peak.json);
+#                           DMMA-only register microbenchmark: 37.0 (profiles/r1_dmma_peak.txt)
 
 
 def peaks():
@@ -147,15 +156,14 @@ def cpu_baseline(a: np.ndarray, budget_s: float):
     n = a.shape[0]
     threads = os.cpu_count() or 1
     O.condense_prefix(a[:64, :64], 8, threads)  # load + spin up the thread pool
-    t0 = time.perf_counter()
-    probe = 4
-    O.condense_prefix(a, probe, threads)
-    t_probe = time.perf_counter() - t0
-    per_step = max(t_probe / probe, 1e-6)
-    steps = int(min(n - 1, max(probe, budget_s / per_step)))
-    t0 = time.perf_counter()
-    O.condense_prefix(a, steps, threads)
-    t = time.perf_counter() - t0
+    steps = min(n - 1, 16)
+    for _ in range(3):  # grow the prefix until it takes about budget_s
+        t0 = time.perf_counter()
+        O.condense_prefix(a, steps, threads)
+        t = time.perf_counter() - t0
+        if t >= 0.5 * budget_s or steps == n - 1:
+            break
+        steps = int(min(n - 1, max(steps + 1, steps * 0.9 * budget_s / max(t, 1e-3))))
     m = np.arange(n, 1, -1, dtype=np.float64)  # active size at each step
     w_all = float(np.sum((m - 1) ** 2))
     w_pre = float(np.sum((m[:steps] - 1) ** 2))
@@ -178,6 +186,8 @@ def run_reference(args):
     if rank != 0:
         return
     name, a, n = workload(args.config)
+    if not isinstance(a, np.ndarray):  # C5 is generated on the GPU; the CPU port gets a host copy
+        a = a.cpu().numpy()
     if a.ndim == 3:
         from oracle import mcnd_oracle as O
 
@@ -211,6 +221,8 @@ def run_reference(args):
 
 
 def metric_name(cfg):
+    if cfg == "c5":
+        return "effective GFLOP/s (2N^3/3) of the blocked condensation log-determinant, N=32768 FP64 (time-to-logdet in ms_per_step)"
     if cfg == "c4":
         return "effective GFLOP/s (2n^3/3 per matrix), batched 4096 x 64x64 SPD FP64 logdet"
     return "effective GFLOP/s (2N^3/3) of the condensation log-determinant, FP64 (time-to-logdet in ms_per_step)"
@@ -235,34 +247,46 @@ def run_single(args):
     name, a, n = workload(args.config)
     if a.ndim == 3:
         return run_batched(args, name, a, n)
-    d = torch.from_numpy(a).cuda()
-    h = torch.empty(a.shape, dtype=torch.float64, pin_memory=True)
-    h.numpy()[...] = a
-    hv = h.numpy()
+    # default: the blocked rank-64 variant where the unblocked rank-1 chain is HBM-bound
+    # (north_star (2)); C1 stays unblocked (L2/latency-bound, 8 MB).  The other variant
+    # is measured too and reported under "alt" (unblocked = bitwise-reference arithmetic).
+    method = args.method or ("unblocked" if n < 2048 else "blocked")
+    fn = mc.logdet_blocked if method == "blocked" else mc.logdet_condensation
+    if isinstance(a, np.ndarray):
+        d = torch.from_numpy(a).cuda()
+    else:
+        d, a = a, None
+    try:
+        h = torch.empty(tuple(d.shape), dtype=torch.float64, pin_memory=True)
+        h.copy_(d)
+        hv = h.numpy()
+    except Exception:  # not enough pinned host memory: e2e from pageable memory
+        hv = d.cpu().numpy()
+    if a is None and not args.no_cpu_baseline:
+        a = hv
     stream = torch.cuda.current_stream()
 
     for _ in range(args.warmup):
-        res = mc.logdet_condensation(d, fast=args.fast)
+        res = fn(d, fast=args.fast)
     torch.cuda.synchronize()
     kernel_ms = []
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         ev0.record(stream)
         for _ in range(args.steps):
-            res, piv, cols, kms = mc.logdet_condensation(d, fast=args.fast, return_pivots=True)
+            res, piv, cols, kms = fn(d, fast=args.fast, return_pivots=True)
             kernel_ms.append(kms)
         ev1.record(stream)
         torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1) / args.steps
 
     # e2e: public API on a pinned HOST matrix (H2D + condensation + D2H + host fold)
-    for _ in range(1):
-        mc.logdet_condensation(hv, fast=args.fast)
+    fn(hv, fast=args.fast)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(args.steps):
-        res_e2e = mc.logdet_condensation(hv, fast=args.fast)
+        res_e2e = fn(hv, fast=args.fast)
     e1.record(stream)
     torch.cuda.synchronize()
     ms_e2e = e0.elapsed_time(e1) / args.steps
@@ -270,9 +294,19 @@ def run_single(args):
 
     kms = statistics.mean(kernel_ms)
     hbm, peak_kind = peaks()
-    B = algorithmic_bytes(n)
-    achieved = B / (kms * 1e-3) / 1e9
-    parity = check_parity(args.config, res, args.fast)
+    if method == "blocked":
+        achieved = flops(n) / (kms * 1e-3) / 1e12  # the pivot chain, not DMMA, bounds small N
+        roof = {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
+                "peak_kind": "measured here (cuBLAS DGEMM, FP64 DMMA)", "unit": "TFLOP/s",
+                "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic_from_profiles(args.config + "_blocked"),
+                "algorithmic_flops_per_launch": flops(n)}
+    else:
+        B = algorithmic_bytes(n)
+        achieved = B / (kms * 1e-3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
+                "frac": achieved / hbm, "traffic": traffic_from_profiles(args.config),
+                "algorithmic_bytes_per_launch": B}
+    parity = check_parity(args.config, res, args.fast or method == "blocked")
     line = {
         "metric": metric_name(args.config),
         "value": flops(n) / (ms * 1e-3) / 1e9,
@@ -288,28 +322,49 @@ def run_single(args):
         "vs_baseline": (PAPER_TABLE3_N8000[1] / (ms / 1e3)) if args.config == "c3" else None,
         "vs_baseline_note": "paper Table 3 (PAPER.md:193): N=8000, 1 CPU processor, 170.80 s" if args.config == "c3" else None,
         "dtype": "f64",
-        "data": "synthetic (numpy PCG64 seed, BASELINE recipe)",
-        "config": {"workload": name, "n": n, "mode": "fast-fma" if args.fast else "reference-exact",
+        "data": "synthetic (seeded, BASELINE recipe)",
+        "config": {"workload": name, "n": n, "method": method,
+                   "mode": "fast-fma" if args.fast else "reference-exact",
                    "l2": "input larger than L2 (%.0f MB vs 126 MB); workspace re-read from the caller's matrix each step" % (8 * n * n / 1e6),
-                   "parallelism": "1 GPU, 1 persistent CTA per SM"},
+                   "parallelism": "1 GPU"},
         "result": {"sign": res.sign, "log_abs": res.log_abs, "parity": parity},
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
-                     "frac": achieved / hbm, "traffic": traffic_from_profiles(args.config),
-                     "algorithmic_bytes_per_launch": B},
+        "roofline": roof,
         "e2e": {"value": flops(n) / (ms_e2e * 1e-3) / 1e9, "unit": "GFLOP/s", "ms_per_step": ms_e2e,
                 "h2d_bytes_per_step": 8 * n * n, "d2h_bytes_per_step": 12 * n + 16},
-        "gpu_launches": args.steps,
+        "gpu_launches": args.steps * (1 if method == "unblocked" else blocked_launches(n)),
         "clocks": clk.summary(),
     }
-    if not args.no_cpu_baseline:
+    if args.method is None and args.config in ("c2", "c3"):
+        other = mc.logdet_condensation if method == "blocked" else mc.logdet_blocked
+        other(d, fast=args.fast)
+        oms = []
+        for _ in range(max(2, min(args.steps, 4))):
+            r2, _, _, k2 = other(d, fast=args.fast, return_pivots=True)
+            oms.append(k2)
+        okms = statistics.mean(oms)
+        omethod = "unblocked" if method == "blocked" else "blocked"
+        alt = {"method": omethod, "kernel_ms": okms, "value": flops(n) / (okms * 1e-3) / 1e9, "unit": "GFLOP/s",
+               "result": {"sign": r2.sign, "log_abs": r2.log_abs,
+                          "parity": check_parity(args.config, r2, args.fast or omethod == "blocked")}}
+        if omethod == "unblocked":
+            B = algorithmic_bytes(n)
+            alt["roofline"] = {"bound": "hbm", "achieved": B / (okms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
+                               "frac": B / (okms * 1e-3) / 1e9 / hbm, "traffic": traffic_from_profiles(args.config)}
+        line["alt"] = alt
+    if not args.no_cpu_baseline and a is not None:
         line["cpu_baseline"] = cpu_baseline(a, args.cpu_seconds)
     print(json.dumps(line), flush=True)
 
 
+def blocked_launches(n, b=64, tail=1024):
+    """Kernels one blocked logdet launches: init + per panel pair 7 (KP, gather, GEMM,
+    KP, pair-prep, gather, L-correction GEMM, trailing GEMM = 8) / single panel 3 + tail."""
+    panels = (n - tail) // b if n - tail >= b else 0
+    return 1 + (panels // 2) * 8 + (panels % 2) * 3 + 1
+
+
 def check_parity(cfg, res, fast):
     """Compare with the reference's golden (when committed) -- reported, not asserted."""
-    import glob
-
     names = {"c1": "c1_normal_1000_s1", "c3": "c3_uniform_8000_s3"}
     nm = names.get(cfg)
     if not nm:
