@@ -59,8 +59,8 @@ __device__ __forceinline__ double2 get(const double2* p) { return __ldcg(p); }
 #define KP_TRACE 0  // microbenchmark knob: record per-step phase timestamps of CTA 0
 #endif
 #if KP_TRACE
-__device__ unsigned long long g_kp_trace[64][6];
-#define KP_MARK(s, k) do { if (blockIdx.x == 0 && threadIdx.x == 0) g_kp_trace[s][k] = globaltimer(); } while (0)
+__device__ unsigned long long g_kp_trace[64][8];
+#define KP_MARK(s, k) do { if (blockIdx.x == 0 && threadIdx.x == 0) g_kp_trace[s][k] = clock64(); } while (0)
 #else
 #define KP_MARK(s, k) do { } while (0)
 #endif
@@ -69,7 +69,9 @@ __global__ void __launch_bounds__(kThreads, 1) kp_panel_kernel(const KPParams p)
     extern __shared__ __align__(16) double S[];  // [kB][cw]
     __shared__ double sT[kB][kB + 1];
     __shared__ double s_mult[kB], s_last[kB];
-    __shared__ double s_rmax[kB];
+    __shared__ double s_rmax[kB], s_rmax2[kB];
+    __shared__ double s_lv[2], s_lm[2];
+    __shared__ int s_li[2];
     __shared__ int s_l[kB];
     __shared__ double s_cv, s_win_v, s_win_w;
     __shared__ int s_cpos, s_win_l, s_win_g, s_stop;
@@ -106,7 +108,7 @@ __global__ void __launch_bounds__(kThreads, 1) kp_panel_kernel(const KPParams p)
             const int oi = __shfl_xor_sync(hm, bi, o);
             if (beats(ov, oi, bv, bi)) { bv = ov; bi = oi; }
         }
-        if (j == 0) s_rmax[r] = mx;
+        if (j == 0) { s_rmax[r] = mx; s_rmax2[r] = 0.0; }
         if (r == 0 && j == 0) { s_cv = bv; s_cpos = bi; }
     }
     __syncthreads();
@@ -209,6 +211,7 @@ __global__ void __launch_bounds__(kThreads, 1) kp_panel_kernel(const KPParams p)
             if (tid < kB) s_mult[tid] = r.x;
             else s_last[tid - kB] = r.x;
         }
+        KP_MARK(s, 7);
         for (int c = tid; c < wn; c += kThreads)
             if (lo + c != l) S[s * cw + c] = __ddiv_rn(S[s * cw + c], v);
         __syncthreads();
@@ -229,13 +232,14 @@ __global__ void __launch_bounds__(kThreads, 1) kp_panel_kernel(const KPParams p)
         KP_MARK(s, 3);
         if (s + 1 == kB) break;
         const double* us = S + s * cw;
-        // ---- D1. lookahead (warp 0): update row s+1, its running max and next candidate
-        if (warp == 0) {
+        // ---- D1. lookahead (warps 0-1): update row s+1, its running max, next candidate
+        constexpr int kLA = 64;  // lookahead threads
+        if (tid < kLA) {
             const double mu = s_mult[s + 1];
             double* row = S + (s + 1) * cw;
             double mx = 0.0, bv = 0.0;
             int bi = INT_MAX;
-            for (int c = lane; c < wn; c += 32) {
+            for (int c = tid; c < wn; c += kLA) {
                 const double y = __dsub_rn(row[c], __dmul_rn(mu, us[c]));
                 row[c] = y;
                 mx = fmax(mx, fabs(y));
@@ -248,49 +252,55 @@ __global__ void __launch_bounds__(kThreads, 1) kp_panel_kernel(const KPParams p)
                 const int oi = __shfl_xor_sync(kFull, bi, o);
                 if (beats(ov, oi, bv, bi)) { bv = ov; bi = oi; }
             }
-            if (lane == 0) {
-                s_rmax[s + 1] = fmax(s_rmax[s + 1], mx);
-                s_cv = bv;
-                s_cpos = bi;
+            if (lane == 0) { s_lv[warp] = bv; s_li[warp] = bi; s_lm[warp] = mx; }
+            asm volatile("bar.sync 1, %0;" ::"n"(kLA));
+            if (tid == 0) {
+                double v0 = s_lv[0];
+                int i0 = s_li[0];
+                if (beats(s_lv[1], s_li[1], v0, i0)) { v0 = s_lv[1]; i0 = s_li[1]; }
+                s_cv = v0;
+                s_cpos = i0;
+                s_rmax[s + 1] = fmax(fmax(s_rmax[s + 1], s_rmax2[s + 1]), fmax(s_lm[0], s_lm[1]));
             }
         }
         __syncthreads();
+        KP_MARK(s, 5);
         const int pos = s_cpos;                                   // candidate column of pivot s+1
         const int pc = (pos != INT_MAX) ? pos - lo : -1;          // local
         const int lc = (ms - 2 >= lo && ms - 2 - lo < wn) ? ms - 2 - lo : -1;  // new last column, local
         const unsigned tag1 = tag + 1u;
-        if (warp == 0) {
-            // ---- D2. publish pivot s+1's proposal: rows > s+1 get columns pc / lc updated here
-            for (int r = lane; r < kB; r += 32) {
-                const double mu = s_mult[r];
-                double* row = S + r * cw;
-                double mx = 0.0;
-                double xc = 0.0, xl = 0.0;
-                if (pc >= 0) {
-                    xc = row[pc];
-                    if (r > s + 1) { xc = __dsub_rn(xc, __dmul_rn(mu, us[pc])); row[pc] = xc; mx = fabs(xc); }
-                }
-                if (lc >= 0) {
-                    if (lc == pc) xl = xc;
-                    else {
-                        xl = row[lc];
-                        if (r > s + 1) { xl = __dsub_rn(xl, __dmul_rn(mu, us[lc])); row[lc] = xl; mx = fmax(mx, fabs(xl)); }
-                    }
-                    put(p.lastbuf + (s + 1) * kB + r, pack(xl, tag1, 0));
-                }
-                put(p.colbuf + ((int64_t)(s + 1) * G + g) * kB + r, pack(xc, tag1, 0));
-                if (r > s + 1) atomicMax(reinterpret_cast<unsigned long long*>(s_rmax) + r,
-                                         (unsigned long long)__double_as_longlong(mx));
+        if (tid < kLA) {
+            // ---- D2. publish pivot s+1's proposal (one row per thread): rows > s+1 get
+            //          columns pc / lc updated here (E skips them); their maxima go to
+            //          s_rmax2 (single writer, no atomics)
+            const int r = tid;
+            const double mu = s_mult[r];
+            double* row = S + r * cw;
+            double mx = 0.0, xc = 0.0, xl = 0.0;
+            if (pc >= 0) {
+                xc = row[pc];
+                if (r > s + 1) { xc = __dsub_rn(xc, __dmul_rn(mu, us[pc])); row[pc] = xc; mx = fabs(xc); }
             }
-            if (lane == 0) put(p.cand + (s + 1) * G + g, pack(s_cv, tag1, pos));
-            if (lane == 1) put(p.wrec + (s + 1) * G + g, pack(s_rmax[s + 1], tag1, 0));
+            if (lc >= 0) {
+                if (lc == pc) xl = xc;
+                else {
+                    xl = row[lc];
+                    if (r > s + 1) { xl = __dsub_rn(xl, __dmul_rn(mu, us[lc])); row[lc] = xl; mx = fmax(mx, fabs(xl)); }
+                }
+                put(p.lastbuf + (s + 1) * kB + r, pack(xl, tag1, 0));
+            }
+            put(p.colbuf + ((int64_t)(s + 1) * G + g) * kB + r, pack(xc, tag1, 0));
+            if (r > s + 1) s_rmax2[r] = fmax(s_rmax2[r], mx);
+            if (r == 1) put(p.wrec + (s + 1) * G + g, pack(s_rmax[s + 1], tag1, 0));
+            if (r == 0) put(p.cand + (s + 1) * G + g, pack(s_cv, tag1, pos));
+            KP_MARK(s, 6);
         } else {
-            // ---- E. bulk (warps 1..31): rows > s+1, all columns except pc / lc, with the
+            // ---- E. bulk (warps 2..31): rows > s+1, all columns except pc / lc, with the
             //         reference's two roundings (condense.py:118); per-row maxima by a
             //         two-segment warp reduction
             const int total = (kB - 2 - s) * wn;
-            constexpr int kBulk = kThreads - 32;
-            for (int e0 = (warp - 1) * 32; e0 < total; e0 += kBulk) {
+            constexpr int kBulk = kThreads - kLA;
+            for (int e0 = tid - kLA - lane; e0 < total; e0 += kBulk) {
                 const int e = e0 + lane;
                 double mx = 0.0;
                 int r = INT_MAX;

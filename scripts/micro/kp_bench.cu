@@ -15,11 +15,11 @@ int main(int argc, char** argv) {
     std::mt19937_64 rng(1);
     std::uniform_real_distribution<double> U(-1, 1);
     for (auto& x : h) x = U(rng);
-    double *ws, *wit, *W; PivRec* rec; K2Panel* pan; unsigned* abort; double2 *cand, *wrec, *colb, *lastb; K1Err* err;
+    double *ws, *wit, *W; PivRec* rec; K2Gather* pan; unsigned* abort; double2 *cand, *wrec, *colb, *lastb; K1Err* err;
     cudaMalloc(&ws, h.size() * 8); cudaMemcpy(ws, h.data(), h.size() * 8, cudaMemcpyHostToDevice);
     cudaMalloc(&wit, 64 * 8); cudaMemset(wit, 0, 64 * 8);
     cudaMalloc(&W, (size_t)64 * ld * 8);
-    cudaMalloc(&rec, 64 * sizeof(PivRec)); cudaMalloc(&pan, sizeof(K2Panel)); cudaMalloc(&abort, 4); cudaMemset(abort, 0, 4);
+    cudaMalloc(&rec, 64 * sizeof(PivRec)); cudaMalloc(&pan, sizeof(K2Gather)); cudaMalloc(&abort, 4); cudaMemset(abort, 0, 4);
     cudaMalloc(&cand, 64 * kKPMaxG * 16); cudaMalloc(&wrec, 64 * kKPMaxG * 16); cudaMalloc(&colb, (size_t)64 * kKPMaxG * 64 * 16);
     cudaMalloc(&lastb, 64 * 64 * 16); cudaMalloc(&err, sizeof(K1Err)); cudaMemset(err, 0, sizeof(K1Err));
     cudaMemset(cand, 0, 64 * kKPMaxG * 16); cudaMemset(wrec, 0, 64 * kKPMaxG * 16);
