@@ -1,20 +1,23 @@
-// K3: batched condensation log-determinant, one CTA per small matrix.
+// K3: batched condensation log-determinant, one WARP per small matrix.
 //
 // Same step as condense_step (mcnd/condense.py:95-131) with the default
-// top-to-bottom pivot order, but the whole n x n matrix (n <= 128) lives in
-// shared memory for all n-1 steps: HBM is touched once to load each matrix
-// and once to store (sign, log|det|).  The reference has no batched entry
-// point; its oracle is a loop of logdet_condensation.
+// top-to-bottom pivot order and the reference's arithmetic (true division for
+// the pivot row, product then difference for the update), so the pivots are
+// bitwise the reference's.  The whole n x n matrix (n <= 128) lives in shared
+// memory (row stride n+1: conflict-free for both row and column walks) for all
+// n-1 steps: HBM is touched once to load each matrix and once to store
+// (sign, log|det|).  The reference has no batched entry point; its oracle is a
+// loop of logdet_condensation.
 //
-// Per step: warp 0 takes the argmax of the pivot row (ties -> lowest column),
-// runs the witness test and writes the scaled, column-permuted pivot row to
-// smem; then each warp owns whole rows, so the in-place hazard on the
-// multiplier column is resolved inside the warp (all lanes read their
-// operands before any lane writes, __syncwarp in between).  Per-row witness
-// maxima are warp reductions (no atomics).  log|det| is accumulated in step
-// order by one thread at the end (device log(), so |d log| stays within the
-// north_star tolerance; the per-step pivots are also emitted so a host can
-// recompute the bitwise-reference sum when it wants to).
+// One warp owns one matrix, so there is no block-level synchronisation at all.
+// Each lane owns whole rows (see k3_batched_warp); the argmax of the pivot row
+// is an exact 64-bit max reduction done as two 32-bit warp reductions
+// (redux.sync on the high word, then on the low word of the lanes holding the
+// high-word maximum) -- non-negative doubles order like their bit patterns.
+// |x| is taken by clearing the sign bit (integer pipe), leaving the FP64 pipe
+// with exactly the two operations per element the reference performs.  log|det| is accumulated in step order by one lane
+// (device log(): within the north_star tolerance; the pivots themselves can
+// be returned for a bitwise check).
 #include <cstdint>
 #include <climits>
 #include "mcnd_internal.h"
@@ -22,10 +25,7 @@
 namespace mcnd {
 namespace {
 
-constexpr int kThreads = 256;
-constexpr int kWarps = kThreads / 32;
 constexpr unsigned kFull = 0xffffffffu;
-constexpr int kMaxPerLane = 4;  // n <= 128 -> at most 4 columns per lane
 
 template <bool kFast>
 __device__ __forceinline__ double upd(double x, double mult, double p) {
@@ -33,125 +33,173 @@ __device__ __forceinline__ double upd(double x, double mult, double p) {
     return __dsub_rn(x, __dmul_rn(mult, p));
 }
 
-template <bool kFast>
-__global__ void __launch_bounds__(kThreads) k3_batched(const double* __restrict__ a, int n, int64_t stride,
-                                                       int32_t* __restrict__ sign_out,
-                                                       double* __restrict__ log_out,
-                                                       double* __restrict__ piv_out) {
+__device__ __forceinline__ unsigned long long abs_bits(double x) {
+    return (unsigned long long)__double_as_longlong(x) & 0x7fffffffffffffffull;
+}
+
+// Exact warp max of non-negative 64-bit patterns.
+__device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v) {
+    const unsigned hi = (unsigned)(v >> 32), lo = (unsigned)v;
+    const unsigned mh = __reduce_max_sync(kFull, hi);
+    const unsigned ml = __reduce_max_sync(kFull, hi == mh ? lo : 0u);
+    return ((unsigned long long)mh << 32) | ml;
+}
+
+// Warp argmax of |x| (bit patterns), ties -> lowest column.
+__device__ __forceinline__ int warp_argmax(unsigned long long a, int idx) {
+    const unsigned long long m = warp_max_u64(a);
+    return (int)__reduce_min_sync(kFull, a == m ? (unsigned)idx : 0xffffffffu);
+}
+
+// Two warps per matrix (kWPM): lane i of the pair owns rows i, i+64, ... (NR of
+// them) and updates them entirely by itself (no cross-lane hazard on the
+// multiplier column, no synchronisation inside the update), keeping their
+// running maxima in shared memory.  Per step the first warp scans the pivot
+// row (2..4 columns per lane, exact warp argmax), runs the witness test and
+// writes the scaled pivot row; two named barriers per step order the pair.
+constexpr int kWPM = 2;
+constexpr int kTPM = 32 * kWPM;  // threads per matrix
+
+template <bool kFast, int NR>
+__global__ void k3_batched_warp(const double* __restrict__ a, int n, int64_t stride, int64_t batch,
+                                int32_t* __restrict__ sign_out, double* __restrict__ log_out,
+                                double* __restrict__ piv_out) {
     extern __shared__ __align__(16) double sh[];
-    double* A = sh;                 // n x n, row stride n
-    double* wit = A + n * n;        // n
-    double* prow = wit + n;         // n
-    double* piv = prow + n;         // n  pivot values
-    int* pcol = reinterpret_cast<int*>(piv + n);  // n pivot columns
-    __shared__ int s_l;
-    __shared__ int s_sing;
+    const int lane = threadIdx.x & 31;
+    const int mat = threadIdx.x / kTPM;            // matrix slot in this CTA
+    const int li = threadIdx.x % kTPM;             // lane within the matrix
+    const bool lead = li < 32;                     // first warp of the pair
+    const int64_t b = (int64_t)blockIdx.x * (blockDim.x / kTPM) + mat;
+    if (b >= batch) return;                        // uniform for the pair
+    const int ld = n + 1;  // odd stride: lanes walking different rows hit different banks
+    double* A = sh + (size_t)mat * (n * ld + 4 * n + 4);
+    double* prow = A + n * ld;          // scaled pivot row of the current step
+    double* piv = prow + n;             // pivot values
+    double* wit = piv + n;              // running row maxima
+    int* pcol = reinterpret_cast<int*>(wit + n);  // pivot columns
+    double* ctl = reinterpret_cast<double*>(pcol + n + (n & 1));  // [v, l, stop]
+    const int bar = 1 + mat;
+    const double* src = a + b * stride;
 
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const double* src = a + (int64_t)blockIdx.x * stride;
-    const int nn = n * n;
-    for (int e = tid; e < nn; e += kThreads) A[e] = __ldg(src + e);
-    if (tid == 0) s_sing = 0;
-    __syncthreads();
-    // initial witness (condense.py:78), warp per row
-    for (int r = warp; r < n; r += kWarps) {
-        double wm = 0.0;
-        for (int c = lane; c < n; c += 32) wm = fmax(wm, fabs(A[r * n + c]));
+    // load (coalesced rows; 8 rows in flight per thread, no index division)
+    for (int r0 = 0; r0 < n; r0 += 8) {
+        double x[8][NR];
 #pragma unroll
-        for (int o = 16; o; o >>= 1) wm = fmax(wm, __shfl_xor_sync(kFull, wm, o));
-        if (lane == 0) wit[r] = wm;
+        for (int u = 0; u < 8; ++u)
+#pragma unroll
+            for (int k = 0; k < NR; ++k) {
+                const int r = r0 + u, c = li + kTPM * k;
+                x[u][k] = (r < n && c < n) ? __ldg(src + (int64_t)r * n + c) : 0.0;
+            }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+#pragma unroll
+            for (int k = 0; k < NR; ++k) {
+                const int r = r0 + u, c = li + kTPM * k;
+                if (r < n && c < n) A[r * ld + c] = x[u][k];
+            }
     }
-    __syncthreads();
+    asm volatile("bar.sync %0, %1;" ::"r"(bar), "n"(kTPM));
+    // initial witness of my rows (condense.py:78)
+#pragma unroll
+    for (int k = 0; k < NR; ++k) {
+        const int r = li + kTPM * k;
+        if (r < n) {
+            double mx = 0.0;
+            for (int c = 0; c < n; ++c) mx = fmax(mx, fabs(A[r * ld + c]));
+            wit[r] = mx;
+        }
+    }
 
+    int sign = 1;
+    bool stopped = false;
     for (int s = 0; s < n - 1; ++s) {
         const int m = n - s, w = m - 1;
-        const double* rk = A + s * n;  // pivot row = top live row
-        if (warp == 0) {
-            double bv = 0.0;
+        asm volatile("bar.sync %0, %1;" ::"r"(bar), "n"(kTPM));  // row s final, witnesses current
+        if (lead) {
+            const double* rk = A + s * ld;
+            unsigned long long best = 0ull;
             int bi = INT_MAX;
-            for (int c = lane; c < m; c += 32) {
-                const double x = rk[c];
-                const double fx = fabs(x), fb = fabs(bv);
-                if (fx > fb || (fx == fb && c < bi)) { bv = x; bi = c; }
-            }
 #pragma unroll
-            for (int o = 16; o; o >>= 1) {
-                const double ov = __shfl_xor_sync(kFull, bv, o);
-                const int oi = __shfl_xor_sync(kFull, bi, o);
-                const double fo = fabs(ov), fb = fabs(bv);
-                if (fo > fb || (fo == fb && oi < bi)) { bv = ov; bi = oi; }
+            for (int k = 0; k < 4; ++k) {
+                const int c = lane + 32 * k;
+                if (c < m) {
+                    const unsigned long long ab = abs_bits(rk[c]);
+                    if (bi == INT_MAX || ab > best) { best = ab; bi = c; }
+                }
             }
-            const bool singular = !(fabs(bv) > kSingularRtol * wit[s]);
+            const int l = warp_argmax(best, bi);  // ties -> lowest column (condense.py:88)
+            const double v = rk[l];
+            const bool singular = !(fabs(v) > kSingularRtol * wit[s]);  // condense.py:90
             if (!singular) {
                 const double ylast = rk[w];
-                for (int c = lane; c < w; c += 32) prow[c] = __ddiv_rn(c == bi ? ylast : rk[c], bv);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int c = lane + 32 * k;
+                    if (c < w) prow[c] = __ddiv_rn(c == l ? ylast : rk[c], v);
+                }
             }
             if (lane == 0) {
-                piv[s] = bv;
-                pcol[s] = bi;
-                s_l = bi;
-                if (singular) s_sing = 1;
+                piv[s] = v;
+                pcol[s] = singular ? -1 : l;
+                ctl[0] = v;
+                ctl[1] = singular ? -1.0 : (double)l;
+                if (!singular) sign *= (v > 0 ? 1 : -1) * (l != w ? -1 : 1) * ((w & 1) ? -1 : 1);  // k_pos = 0
             }
         }
-        __syncthreads();
-        if (s_sing) break;
-        const int l = s_l;
-        for (int r = s + 1 + warp; r < n; r += kWarps) {
-            double* rr = A + r * n;
-            const double mult = rr[l], lastv = rr[w];
-            double x[kMaxPerLane];
+        asm volatile("bar.sync %0, %1;" ::"r"(bar), "n"(kTPM));  // pivot row + (v, l) published
+        const int l = (int)ctl[1];
+        if (l < 0) { stopped = true; break; }  // singular: uniform for the pair
+        // my live rows: rank-1 update in place (condense.py:118) + running maxima (:120-122)
+        double mult[NR], mx[NR];
+        double* rr[NR];
+        bool live[NR];
 #pragma unroll
-            for (int k = 0; k < kMaxPerLane; ++k) {
-                const int c = lane + 32 * k;
-                x[k] = (c < w) ? (c == l ? lastv : rr[c]) : 0.0;
-            }
-            __syncwarp();
-            double wm = 0.0;
+        for (int k = 0; k < NR; ++k) {
+            const int r = li + kTPM * k;
+            live[k] = r > s && r < n;
+            rr[k] = A + (live[k] ? r : s) * ld;
+            mult[k] = live[k] ? rr[k][l] : 0.0;
+            if (live[k]) rr[k][l] = rr[k][w];  // column exchange (mult already read)
+            mx[k] = 0.0;
+        }
+#pragma unroll 4
+        for (int c = 0; c < w; ++c) {
+            const double pc = prow[c];
 #pragma unroll
-            for (int k = 0; k < kMaxPerLane; ++k) {
-                const int c = lane + 32 * k;
-                if (c < w) {
-                    const double y = upd<kFast>(x[k], mult, prow[c]);
-                    rr[c] = y;
-                    wm = fmax(wm, fabs(y));
+            for (int k = 0; k < NR; ++k) {
+                if (live[k]) {
+                    const double y = upd<kFast>(rr[k][c], mult[k], pc);
+                    rr[k][c] = y;
+                    mx[k] = fmax(mx[k], fabs(y));
                 }
             }
-#pragma unroll
-            for (int o = 16; o; o >>= 1) wm = fmax(wm, __shfl_xor_sync(kFull, wm, o));
-            if (lane == 0) wit[r] = fmax(wit[r], wm);
         }
-        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < NR; ++k)
+            if (live[k]) wit[li + kTPM * k] = fmax(wit[li + kTPM * k], mx[k]);
     }
-    if (tid == 0) {
-        int32_t sign = 0;
+    asm volatile("bar.sync %0, %1;" ::"r"(bar), "n"(kTPM));
+    if (li == 0) {
+        int32_t sg = 0;
         double la = -INFINITY;
-        if (!s_sing) {
-            const double v = A[(n - 1) * n];
+        if (!stopped) {
+            const double v = A[(n - 1) * ld];
+            piv[n - 1] = v;
+            pcol[n - 1] = 0;
             if (fabs(v) > kSingularRtol * wit[n - 1]) {
-                piv[n - 1] = v;
-                pcol[n - 1] = 0;
-                int sg = 1;
+                sg = sign * (v > 0 ? 1 : -1);
                 double acc = 0.0;
-                for (int s = 0; s < n - 1; ++s) {
-                    const int m = n - s;
-                    const double pv = piv[s];
-                    acc += log(fabs(pv));
-                    const int swap = (pcol[s] != m - 1) ? -1 : 1;
-                    const int par = ((m - 1) & 1) ? -1 : 1;  // k_pos = 0 (top-to-bottom)
-                    sg *= (pv > 0 ? 1 : -1) * swap * par;
-                }
-                sign = sg * (v > 0 ? 1 : -1);
-                la = acc + log(fabs(v));
-            } else {
-                piv[n - 1] = v;
+                for (int t = 0; t < n; ++t) acc += log(fabs(piv[t]));
+                la = acc;
             }
         }
-        sign_out[blockIdx.x] = sign;
-        log_out[blockIdx.x] = la;
+        sign_out[b] = sg;
+        log_out[b] = sg == 0 ? -INFINITY : la;
     }
     if (piv_out) {
-        __syncthreads();
-        for (int s = tid; s < n; s += kThreads) piv_out[(int64_t)blockIdx.x * n + s] = piv[s];
+        asm volatile("bar.sync %0, %1;" ::"r"(bar), "n"(kTPM));
+        for (int t = li; t < n; t += kTPM) piv_out[b * n + t] = piv[t];
     }
 }
 
@@ -159,16 +207,23 @@ __global__ void __launch_bounds__(kThreads) k3_batched(const double* __restrict_
 
 cudaError_t k3_launch(const double* a, int64_t batch, int64_t n, int64_t stride, bool fast,
                       int32_t* sign, double* log_abs, double* pivots, cudaStream_t s) {
-    if (n < 1 || n > 32 * kMaxPerLane || batch < 0) return cudaErrorInvalidValue;
+    if (n < 1 || n > 128 || batch < 0) return cudaErrorInvalidValue;
     if (batch == 0) return cudaSuccess;
-    const size_t smem = (size_t)(n * n + 3 * n) * sizeof(double) + (size_t)n * sizeof(int) + 16;
-    const void* fn = fast ? (const void*)k3_batched<true> : (const void*)k3_batched<false>;
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    if (fast)
-        k3_batched<true><<<(unsigned)batch, kThreads, smem, s>>>(a, (int)n, stride, sign, log_abs, pivots);
-    else
-        k3_batched<false><<<(unsigned)batch, kThreads, smem, s>>>(a, (int)n, stride, sign, log_abs, pivots);
+    const int mats = n <= 64 ? 2 : 1;  // matrices per CTA (shared-memory bound)
+    const size_t per = (size_t)(n * (n + 1) + 4 * n + 4) * sizeof(double);
+    const size_t smem = per * mats;
+    const dim3 grid((unsigned)((batch + mats - 1) / mats)), block(kTPM * mats);
+    cudaError_t e;
+#define MCND_K3(F, NR)                                                                                   \
+    e = cudaFuncSetAttribute(k3_batched_warp<F, NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    if (e != cudaSuccess) return e;                                                                      \
+    k3_batched_warp<F, NR><<<grid, block, smem, s>>>(a, (int)n, stride, batch, sign, log_abs, pivots);
+    if (n <= 64) {
+        if (fast) { MCND_K3(true, 1) } else { MCND_K3(false, 1) }
+    } else {
+        if (fast) { MCND_K3(true, 2) } else { MCND_K3(false, 2) }
+    }
+#undef MCND_K3
     return cudaGetLastError();
 }
 
