@@ -128,12 +128,14 @@ int mcnd_dist_mc_parallel(void* handle, const double* d_rows, int64_t n, int64_t
                           double* rem_row, double* rem_wit, double* device_ms);
 void mcnd_dist_destroy(void* handle);
 
-/* ---- batched: one CTA per small matrix (no reference counterpart; oracle = a loop
+/* ---- batched: two warps per small matrix (no reference counterpart; oracle = a loop
  * of logdet_condensation).  d_sign/d_log_abs: DEVICE outputs (batch entries);
- * d_pivots: optional DEVICE batch x n pivot values (for bitwise checks). n <= 128. */
+ * d_pivots: optional DEVICE batch x n pivot values (for bitwise checks); d_nonfinite:
+ * optional DEVICE flag set nonzero when any entry is NaN/Inf (the host entry point
+ * turns it into MCND_EINVAL, like matrix.py:39-40). n <= 128.  Asynchronous. */
 int mcnd_logdet_batched_dev(const double* d_a, int64_t batch, int64_t n, int64_t stride,
                             uint32_t flags, void* stream, int32_t* d_sign, double* d_log_abs,
-                            double* d_pivots);
+                            double* d_pivots, uint32_t* d_nonfinite);
 /* host in / host out */
 int mcnd_logdet_batched(const double* h_a, int64_t batch, int64_t n, int64_t stride,
                         uint32_t flags, void* stream, int32_t* h_sign, double* h_log_abs);

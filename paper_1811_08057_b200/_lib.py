@@ -73,7 +73,7 @@ def load(path: str | None = None):
             f = getattr(lib, name)
             f.argtypes = [P, i64, i64, i32, u32, P, LD, CS, P, P, P]
             f.restype = ctypes.c_int
-        lib.mcnd_logdet_batched_dev.argtypes = [P, i64, i64, i64, u32, P, P, P, P]
+        lib.mcnd_logdet_batched_dev.argtypes = [P, i64, i64, i64, u32, P, P, P, P, P]
         lib.mcnd_logdet_batched_dev.restype = ctypes.c_int
         lib.mcnd_logdet_batched.argtypes = [P, i64, i64, i64, u32, P, P, P]
         lib.mcnd_logdet_batched.restype = ctypes.c_int

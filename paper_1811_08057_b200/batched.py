@@ -27,24 +27,24 @@ def logdet_batched(a, *, fast: bool = False, return_pivots: bool = False):
         if a.dim() != 3 or a.shape[1] != a.shape[2]:
             raise ValueError("expected a (B, n, n) batch of square matrices")
         a = a.to(torch.float64).contiguous()
-        if not bool(torch.isfinite(a).all()):
-            raise ValueError("matrix entries must be finite (no NaN/Inf)")
         b, n, _ = a.shape
         signs = torch.empty(b, dtype=torch.int32, device=a.device)
         logs = torch.empty(b, dtype=torch.float64, device=a.device)
         piv = torch.empty((b, n), dtype=torch.float64, device=a.device) if return_pivots else None
+        flag = torch.zeros(1, dtype=torch.int32, device=a.device)
         stream = torch.cuda.current_stream(a.device).cuda_stream
         rc = lib.mcnd_logdet_batched_dev(a.data_ptr(), b, n, n * n, flags, stream, signs.data_ptr(),
-                                         logs.data_ptr(), piv.data_ptr() if piv is not None else None)
+                                         logs.data_ptr(), piv.data_ptr() if piv is not None else None,
+                                         flag.data_ptr())
         _lib.check(rc)
+        if int(flag.item()):  # finiteness is checked on the device, fused into the load
+            raise ValueError("matrix entries must be finite (no NaN/Inf)")
         return (signs, logs, piv) if return_pivots else (signs, logs)
     a = np.ascontiguousarray(a, dtype=np.float64)
     if a.ndim != 3 or a.shape[1] != a.shape[2]:
         raise ValueError("expected a (B, n, n) batch of square matrices")
     if a.shape[1] == 0:
         raise ValueError("matrix dimensions must be positive")
-    if not np.isfinite(a).all():
-        raise ValueError("matrix entries must be finite (no NaN/Inf)")
     b, n, _ = a.shape
     signs = np.zeros(b, dtype=np.int32)
     logs = np.zeros(b, dtype=np.float64)

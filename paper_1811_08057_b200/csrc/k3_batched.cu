@@ -63,7 +63,7 @@ constexpr int kTPM = 32 * kWPM;  // threads per matrix
 template <bool kFast, int NR>
 __global__ void k3_batched_warp(const double* __restrict__ a, int n, int64_t stride, int64_t batch,
                                 int32_t* __restrict__ sign_out, double* __restrict__ log_out,
-                                double* __restrict__ piv_out) {
+                                double* __restrict__ piv_out, unsigned* __restrict__ nonfinite) {
     extern __shared__ __align__(16) double sh[];
     const int lane = threadIdx.x & 31;
     const int mat = threadIdx.x / kTPM;            // matrix slot in this CTA
@@ -91,13 +91,18 @@ __global__ void k3_batched_warp(const double* __restrict__ a, int n, int64_t str
                 const int r = r0 + u, c = li + kTPM * k;
                 x[u][k] = (r < n && c < n) ? __ldg(src + (int64_t)r * n + c) : 0.0;
             }
+        bool bad = false;
 #pragma unroll
         for (int u = 0; u < 8; ++u)
 #pragma unroll
             for (int k = 0; k < NR; ++k) {
                 const int r = r0 + u, c = li + kTPM * k;
-                if (r < n && c < n) A[r * ld + c] = x[u][k];
+                if (r < n && c < n) {
+                    A[r * ld + c] = x[u][k];
+                    bad |= !isfinite(x[u][k]);
+                }
             }
+        if (bad && nonfinite) atomicOr(nonfinite, 1u);  // matrix.py:39-40, checked on device
     }
     asm volatile("bar.sync %0, %1;" ::"r"(bar), "n"(kTPM));
     // initial witness of my rows (condense.py:78)
@@ -206,7 +211,7 @@ __global__ void k3_batched_warp(const double* __restrict__ a, int n, int64_t str
 }  // namespace
 
 cudaError_t k3_launch(const double* a, int64_t batch, int64_t n, int64_t stride, bool fast,
-                      int32_t* sign, double* log_abs, double* pivots, cudaStream_t s) {
+                      int32_t* sign, double* log_abs, double* pivots, unsigned* nonfinite, cudaStream_t s) {
     if (n < 1 || n > 128 || batch < 0) return cudaErrorInvalidValue;
     if (batch == 0) return cudaSuccess;
     const int mats = n <= 64 ? 2 : 1;  // matrices per CTA (shared-memory bound)
@@ -217,7 +222,7 @@ cudaError_t k3_launch(const double* a, int64_t batch, int64_t n, int64_t stride,
 #define MCND_K3(F, NR)                                                                                   \
     e = cudaFuncSetAttribute(k3_batched_warp<F, NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
     if (e != cudaSuccess) return e;                                                                      \
-    k3_batched_warp<F, NR><<<grid, block, smem, s>>>(a, (int)n, stride, batch, sign, log_abs, pivots);
+    k3_batched_warp<F, NR><<<grid, block, smem, s>>>(a, (int)n, stride, batch, sign, log_abs, pivots, nonfinite);
     if (n <= 64) {
         if (fast) { MCND_K3(true, 1) } else { MCND_K3(false, 1) }
     } else {

@@ -1106,12 +1106,13 @@ void mcnd_dist_destroy(void* handle) {
 }
 
 int mcnd_logdet_batched_dev(const double* d_a, int64_t batch, int64_t n, int64_t stride, uint32_t flags,
-                            void* stream, int32_t* d_sign, double* d_log_abs, double* d_pivots) {
+                            void* stream, int32_t* d_sign, double* d_log_abs, double* d_pivots,
+                            uint32_t* d_nonfinite) {
     if (batch < 0 || n < 1 || n > 128) return fail(MCND_EINVAL, "batched kernel needs 1 <= n <= 128 (got %lld)", (long long)n);
     if (stride < n * n) return fail(MCND_EINVAL, "stride < n*n");
     if (batch > 0 && (!d_a || !d_sign || !d_log_abs)) return fail(MCND_EINVAL, "null pointer");
     cudaError_t e = k3_launch(d_a, batch, n, stride, (flags & MCND_FLAG_FAST) != 0, d_sign, d_log_abs, d_pivots,
-                              (cudaStream_t)stream);
+                              d_nonfinite, (cudaStream_t)stream);
     if (e != cudaSuccess) return fail(MCND_ECUDA, "batched kernel: %s", cudaGetErrorString(e));
     return MCND_OK;
 }
@@ -1127,20 +1128,27 @@ int mcnd_logdet_batched(const double* h_a, int64_t batch, int64_t n, int64_t str
     if (!B) return code;
     cudaStream_t st = (cudaStream_t)stream;
     const size_t in_bytes = (size_t)batch * stride * sizeof(double);
-    const size_t out_bytes = align_up((size_t)batch * sizeof(double), 256) + (size_t)batch * sizeof(int32_t);
+    const size_t o_sign = align_up((size_t)batch * sizeof(double), 256);
+    const size_t o_flag = o_sign + align_up((size_t)batch * sizeof(int32_t), 256);
     int rc = ensure_dev(&B->din, &B->din_bytes, in_bytes);
     if (rc) return rc;
-    rc = ensure_dev(&B->dws, &B->dws_bytes, out_bytes);
+    rc = ensure_dev(&B->dws, &B->dws_bytes, o_flag + 256);
+    if (rc) return rc;
+    rc = ensure_pinned(&B->hpin, &B->hpin_bytes, 256);
     if (rc) return rc;
     double* d_log = (double*)B->dws;
-    int32_t* d_sign = (int32_t*)((char*)B->dws + align_up((size_t)batch * sizeof(double), 256));
+    int32_t* d_sign = (int32_t*)((char*)B->dws + o_sign);
+    unsigned* d_flag = (unsigned*)((char*)B->dws + o_flag);
+    CUDA_TRY(cudaMemsetAsync(d_flag, 0, sizeof(unsigned), st));
     CUDA_TRY(cudaMemcpyAsync(B->din, h_a, in_bytes, cudaMemcpyHostToDevice, st));
     cudaError_t e = k3_launch((const double*)B->din, batch, n, stride, (flags & MCND_FLAG_FAST) != 0, d_sign, d_log,
-                              nullptr, st);
+                              nullptr, d_flag, st);
     if (e != cudaSuccess) return fail(MCND_ECUDA, "batched kernel: %s", cudaGetErrorString(e));
     CUDA_TRY(cudaMemcpyAsync(h_log_abs, d_log, (size_t)batch * sizeof(double), cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaMemcpyAsync(h_sign, d_sign, (size_t)batch * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(B->hpin, d_flag, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
+    if (*(unsigned*)B->hpin) return fail(MCND_EINVAL, "matrix entries must be finite (no NaN/Inf)");
     return MCND_OK;
 }
 

@@ -129,7 +129,8 @@ cudaError_t k2_pair_prep(const K2Gather* g0, const K2Gather* g1, int32_t m, doub
 cudaError_t k2_gemm(double* ws, int64_t ld, int32_t rbase, int32_t M, int32_t N2, int32_t K, const double* L,
                     int64_t ldl, const double* W, int64_t ldw, double* row_wit, const unsigned* abort, cudaStream_t s);
 
+// nonfinite (nullable, device): set to nonzero if any input entry is NaN/Inf.
 cudaError_t k3_launch(const double* a, int64_t batch, int64_t n, int64_t stride, bool fast,
-                      int32_t* sign, double* log_abs, double* pivots, cudaStream_t s);
+                      int32_t* sign, double* log_abs, double* pivots, unsigned* nonfinite, cudaStream_t s);
 
 }  // namespace mcnd

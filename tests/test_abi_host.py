@@ -77,7 +77,7 @@ def test_abi_rejects_bad_arguments_without_gpu():
     out = _lib.McndLogDet()
     rc = lib.mcnd_logdet_condensation_dev(None, 4, 4, None, 0, 0, None, ctypes.byref(out), None, None)
     assert rc == _lib.MCND_EINVAL
-    rc = lib.mcnd_logdet_batched_dev(None, 1, 200, 40000, 0, None, None, None, None)
+    rc = lib.mcnd_logdet_batched_dev(None, 1, 200, 40000, 0, None, None, None, None, None)
     assert rc == _lib.MCND_EINVAL
     assert "n <= 128" in _lib.last_error()
 

@@ -362,3 +362,17 @@ def test_blocked_c5_32768_vs_cusolver(mc):
     got = mc.logdet_blocked(a)
     assert got.sign == int(s_ref.item())
     assert abs(got.log_abs - float(l_ref)) <= tol(32768, float(l_ref)), (got.log_abs, float(l_ref))
+
+
+def test_batched_nonfinite_detected_on_device(mc):
+    import torch
+
+    a = np.stack([np.eye(64)] * 5)
+    a[3, 7, 9] = np.nan
+    with pytest.raises(ValueError, match="finite"):
+        mc.logdet_batched(a)
+    with pytest.raises(ValueError, match="finite"):
+        mc.logdet_batched(torch.from_numpy(a).cuda())
+    a[3, 7, 9] = 0.0
+    s, l = mc.logdet_batched(a)
+    assert list(s) == [1] * 5 and list(l) == [0.0] * 5
