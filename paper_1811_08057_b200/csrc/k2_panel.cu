@@ -68,10 +68,11 @@ __device__ unsigned long long g_kp_trace[64][8];
 __global__ void __launch_bounds__(kThreads, 1) kp_panel_kernel(const KPParams p) {
     extern __shared__ __align__(16) double S[];  // [kB][cw]
     __shared__ double sT[kB][kB + 1];
-    __shared__ double s_mult[kB], s_last[kB];
+    __shared__ double s_mult2[2][kB], s_last2[2][kB];  // by step parity: warp 0 fetches step s
+                                                       // while the bulk of step s-1 still reads
     __shared__ double s_rmax[kB], s_rmax2[kB];
-    __shared__ double s_lv[2], s_lm[2];
-    __shared__ int s_li[2];
+    __shared__ double s_lv[4], s_lm[4];
+    __shared__ int s_li[4];
     __shared__ int s_l[kB];
     __shared__ double s_cv, s_win_v, s_win_w;
     __shared__ int s_cpos, s_win_l, s_win_g, s_stop;
@@ -125,6 +126,8 @@ __global__ void __launch_bounds__(kThreads, 1) kp_panel_kernel(const KPParams p)
     for (int s = 0; s < kB; ++s) {
         const int ms = m - s;  // active width before pivot s
         const unsigned tag = p.tag0 + (unsigned)s;
+        double* const s_mult = s_mult2[s & 1];
+        double* const s_last = s_last2[s & 1];
         KP_MARK(s, 0);
         // ---- A. reduce the G proposals for pivot s: warp 0 polls all tagged records
         if (warp == 0) {
@@ -173,11 +176,34 @@ __global__ void __launch_bounds__(kThreads, 1) kp_panel_kernel(const KPParams p)
                 if (beats(ov, oi, bv, bi)) { bv = ov; bi = oi; bg = og; }
                 bw = fmax(bw, ow);
             }
+            bw = fmax(bw, p.wit[p.row0 + s]);
+            // the winner's column (multipliers of rows > s, T entries of rows < s) and the
+            // last active column: fetched right here by warp 0, two rows per lane
+            if (fabs(bv) > kSingularRtol * bw) {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int r = lane + 32 * h;
+                    const double2* pm = p.colbuf + ((int64_t)s * G + bg) * kB + r;
+                    const double2* pl = p.lastbuf + s * kB + r;
+                    double2 cm = get(pm), cl = get(pl);
+                    while (tag_of(cm) != tag || tag_of(cl) != tag) {
+                        if (globaltimer() - t_start > p.timeout_ns) {
+                            atomicExch(&p.err->error, 1u);
+                            s_stop = 1;
+                            break;
+                        }
+                        cm = get(pm);
+                        cl = get(pl);
+                    }
+                    s_mult[r] = cm.x;
+                    s_last[r] = cl.x;
+                }
+            }
             if (lane == 0) {
                 s_win_v = bv;
                 s_win_l = bi;
                 s_win_g = bg;
-                s_win_w = fmax(bw, p.wit[p.row0 + s]);
+                s_win_w = bw;
             }
         }
         __syncthreads();
@@ -195,33 +221,16 @@ __global__ void __launch_bounds__(kThreads, 1) kp_panel_kernel(const KPParams p)
             return;
         }
         const int wn = max(0, min(wc, ms - 1 - lo));  // my active columns after the step
-        // ---- B. fetch the winner column (multipliers / T entries) and the last column,
-        //         meanwhile scale row s (true division, condense.py:110) away from column l
-        if (tid < 2 * kB) {
-            const double2* src = (tid < kB) ? p.colbuf + ((int64_t)s * G + s_win_g) * kB + tid
-                                            : p.lastbuf + s * kB + (tid - kB);
-            double2 r = get(src);
-            while (tag_of(r) != tag) {
-                if (globaltimer() - t_start > p.timeout_ns) {
-                    atomicExch(&p.err->error, 1u);
-                    break;
-                }
-                r = get(src);
-            }
-            if (tid < kB) s_mult[tid] = r.x;
-            else s_last[tid - kB] = r.x;
-        }
         KP_MARK(s, 7);
-        for (int c = tid; c < wn; c += kThreads)
-            if (lo + c != l) S[s * cw + c] = __ddiv_rn(S[s * cw + c], v);
-        __syncthreads();
-        KP_MARK(s, 2);
-        // ---- C. column exchange (condense.py:104-107): position l takes the last
-        //         column on every row (one element per row); the pivot record
+        // ---- B. column exchange (condense.py:104-107): position l takes the last column
+        //         on every row (one element per row); row s scaled by true division
+        //         (condense.py:110); T column; the pivot record
         if (tid < kB) {
             if (l >= lo && l - lo < wn) S[tid * cw + (l - lo)] = (tid == s) ? __ddiv_rn(s_last[s], v) : s_last[tid];
             if (tid < s) sT[tid][s] = s_mult[tid];  // T[t][s] = u_t(p_s), t < s
         }
+        for (int c = tid; c < wn; c += kThreads)
+            if (lo + c != l) S[s * cw + c] = __ddiv_rn(S[s * cw + c], v);
         if (g == 0 && tid == 0) {
             p.rec[s].v = v;
             p.rec[s].l = l;
@@ -229,17 +238,19 @@ __global__ void __launch_bounds__(kThreads, 1) kp_panel_kernel(const KPParams p)
         }
         if (tid == 0) s_l[s] = l;
         __syncthreads();
+        KP_MARK(s, 2);
         KP_MARK(s, 3);
         if (s + 1 == kB) break;
         const double* us = S + s * cw;
-        // ---- D1. lookahead (warps 0-1): update row s+1, its running max, next candidate
-        constexpr int kLA = 64;  // lookahead threads
-        if (tid < kLA) {
+        // ---- D1. lookahead (warps 0-3): update row s+1, its running max, next candidate
+        constexpr int kLA = 64;   // publishing threads (D2)
+        constexpr int kD1 = 128;  // row s+1 update threads
+        if (tid < kD1) {
             const double mu = s_mult[s + 1];
             double* row = S + (s + 1) * cw;
             double mx = 0.0, bv = 0.0;
             int bi = INT_MAX;
-            for (int c = tid; c < wn; c += kLA) {
+            for (int c = tid; c < wn; c += kD1) {
                 const double y = __dsub_rn(row[c], __dmul_rn(mu, us[c]));
                 row[c] = y;
                 mx = fmax(mx, fabs(y));
@@ -253,14 +264,18 @@ __global__ void __launch_bounds__(kThreads, 1) kp_panel_kernel(const KPParams p)
                 if (beats(ov, oi, bv, bi)) { bv = ov; bi = oi; }
             }
             if (lane == 0) { s_lv[warp] = bv; s_li[warp] = bi; s_lm[warp] = mx; }
-            asm volatile("bar.sync 1, %0;" ::"n"(kLA));
+            asm volatile("bar.sync 1, %0;" ::"n"(kD1));
             if (tid == 0) {
-                double v0 = s_lv[0];
+                double v0 = s_lv[0], m0 = s_lm[0];
                 int i0 = s_li[0];
-                if (beats(s_lv[1], s_li[1], v0, i0)) { v0 = s_lv[1]; i0 = s_li[1]; }
+#pragma unroll
+                for (int k = 1; k < kD1 / 32; ++k) {
+                    if (beats(s_lv[k], s_li[k], v0, i0)) { v0 = s_lv[k]; i0 = s_li[k]; }
+                    m0 = fmax(m0, s_lm[k]);
+                }
                 s_cv = v0;
                 s_cpos = i0;
-                s_rmax[s + 1] = fmax(fmax(s_rmax[s + 1], s_rmax2[s + 1]), fmax(s_lm[0], s_lm[1]));
+                s_rmax[s + 1] = fmax(fmax(s_rmax[s + 1], s_rmax2[s + 1]), m0);
             }
         }
         __syncthreads();
