@@ -23,6 +23,7 @@
 // sum to coef U = A[r, P] T^{-1} U = L W.  Rounding differs (tolerance parity).
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include "mcnd_internal.h"
 
 namespace mcnd {
@@ -50,7 +51,7 @@ __global__ void k2_gather_fix_kernel(double* __restrict__ ws, int64_t ld, int32_
     for (int k = 0; k < KL; ++k) v[k] = (lane + 32 * k < nm) ? row[gp->moved_src[lane + 32 * k]] : 0.0;
     __syncwarp();
 #pragma unroll
-    for (int k = 0; k < KL; ++k) L[(int64_t)i * K + lane + 32 * k] = x[k];
+    for (int k = 0; k < KL; ++k) L[(int64_t)i * K + lane + 32 * k] = -x[k];  // stored negated: C + L W
 #pragma unroll
     for (int k = 0; k < KL; ++k)
         if (lane + 32 * k < nm) row[gp->moved_c[lane + 32 * k]] = v[k];
@@ -74,7 +75,7 @@ __global__ void k2_pair_prep_kernel(const K2Gather* __restrict__ g0, const K2Gat
     // (a) Wp[s][s'] = W_k[s][P1[s']] (before W_k's columns are permuted)
     for (int e = tid; e < kK2B * kK2B; e += blockDim.x) {
         const int sr = e / kK2B, sp = e % kK2B;
-        Wp[sr * kK2B + sp] = Wc[(int64_t)sr * ldw + g1->P[sp]];
+        Wp[sr * kK2B + sp] = -Wc[(int64_t)sr * ldw + g1->P[sp]];  // negated: (-L1) = (-X) + (-L0)(-Wp)
     }
     // (b) composite gather columns: panel k's pivots, then panel k+1's pivots mapped to width m
     if (tid < kK2B) {
@@ -114,13 +115,14 @@ __global__ void k2_pair_prep_kernel(const K2Gather* __restrict__ g0, const K2Gat
     }
 }
 
-// ---- DMMA GEMM: C[M x N2] (rows rbase.., in ws) -= L[M x K] * W[K x N2], K = 64 or 128 ----
+// ---- DMMA GEMM: C[M x N2] (rows rbase.., in ws) += NL[M x K] * W[K x N2], K = 64 or 128, where
+// NL = -L is stored negated by the gather so the DMMA operands carry no negation (keeps the
+// A-operand register reuse cache usable) ----
 constexpr int BM = 64, BN = 128, BKS = 64;   // tile rows / cols, K per pipeline stage
 constexpr int LDLS = BKS + 4;                // padded smem strides (conflict-free fragment loads)
 constexpr int LDWS = BN + 8;
 constexpr int kStage = BM * LDLS + BKS * LDWS;  // doubles per stage buffer
-constexpr int kGThreads = 512;               // 16 warps: 2 (M) x 8 (N), warp tile 32 x 16
-constexpr int WN = 8, WTN = 16, NJ = WTN / 8;
+// warps: 2 (M) x WN (N); WN = 8 -> 512 threads, warp tile 32 x 16; WN = 4 -> 256 threads, 32 x 32
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -141,13 +143,14 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 // registers during tile t; stores are streaming and fire-and-forget.  Row
 // maxima (the running witness) stay in registers and are flushed with one
 // atomicMax per row-block change (skipped when wit == nullptr).
-template <int K>
-__global__ void __launch_bounds__(kGThreads, 1) k2_gemm_kernel(double* __restrict__ ws, int64_t ld, int32_t rbase,
+template <int K, int WN>
+__global__ void __launch_bounds__(64 * WN, 1) k2_gemm_kernel(double* __restrict__ ws, int64_t ld, int32_t rbase,
                                                                int32_t M, int32_t N2, const double* __restrict__ L,
                                                                int64_t ldl, const double* __restrict__ W, int64_t ldw,
                                                                unsigned long long* __restrict__ wit,
                                                                const unsigned* __restrict__ abort) {
     constexpr int NS = K / BKS;  // stages per tile
+    constexpr int kGThreads = 64 * WN, WTN = BN / WN, NJ = WTN / 8;
     extern __shared__ __align__(16) double sh[];
     if (*(volatile const unsigned*)abort) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -226,7 +229,7 @@ __global__ void __launch_bounds__(kGThreads, 1) k2_gemm_kernel(double* __restric
         for (int k0 = 0; k0 < BKS; k0 += 4) {
             double a[4], b[NJ];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) a[i] = -ls[(wm * 32 + i * 8 + g) * LDLS + k0 + q];
+            for (int i = 0; i < 4; ++i) a[i] = ls[(wm * 32 + i * 8 + g) * LDLS + k0 + q];
 #pragma unroll
             for (int jj = 0; jj < NJ; ++jj) b[jj] = wsm[(k0 + q) * LDWS + wn * WTN + jj * 8 + g];
 #pragma unroll
@@ -271,6 +274,140 @@ __global__ void __launch_bounds__(kGThreads, 1) k2_gemm_kernel(double* __restric
     }
 }
 
+// ---- multistage variant: 2 CTAs per SM, K consumed in stages of 16 through a
+// 4-deep cp.async ring (CUTLASS-style multistage mainloop).  The C tile is loaded
+// into the accumulators at the start of each tile: its latency is hidden by the
+// other CTA on the SM, so a CTA-wide barrier never idles the whole SM's tensor
+// pipe.  Persistent over a contiguous, row-block-major tile range per CTA so the
+// witness maxima are flushed once per row block.
+constexpr int MS_BK = 16, MS_ST = 4;          // K per stage, ring depth
+constexpr int MS_LDL = MS_BK + 4;             // 20 doubles: conflict-free A fragments
+constexpr int MS_STAGE = BM * MS_LDL + MS_BK * LDWS;
+constexpr int MS_THREADS = 256;               // 8 warps: 2 (M) x 4 (N), warp tile 32 x 32
+
+template <int K>
+__global__ void __launch_bounds__(MS_THREADS, 2) k2_gemm_ms_kernel(double* __restrict__ ws, int64_t ld, int32_t rbase,
+                                                                   int32_t M, int32_t N2, const double* __restrict__ L,
+                                                                   int64_t ldl, const double* __restrict__ W, int64_t ldw,
+                                                                   unsigned long long* __restrict__ wit,
+                                                                   const unsigned* __restrict__ abort) {
+    constexpr int KS = K / MS_BK;  // stages per tile
+    constexpr int WN = 4, NJ = 4;
+    extern __shared__ __align__(16) double sh[];
+    if (*(volatile const unsigned*)abort) return;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm = warp / WN, wn = warp % WN;
+    const int g = lane >> 2, q = lane & 3;
+    const int ntn = (N2 + BN - 1) / BN, ntm = (M + BM - 1) / BM;
+    const int64_t T = (int64_t)ntn * ntm;
+    const int64_t t_begin = T * blockIdx.x / gridDim.x, t_end = T * (blockIdx.x + 1) / gridDim.x;
+    if (t_begin >= t_end) return;
+    const int64_t nst = (t_end - t_begin) * KS;
+
+    auto load_stage = [&](int64_t j) {
+        if (j < nst) {
+            const int64_t t = t_begin + j / KS;
+            const int kk = (int)(j % KS) * MS_BK;
+            const int row0 = (int)(t / ntn) * BM, col0 = (int)(t % ntn) * BN;
+            double* ls = sh + (int)(j % MS_ST) * MS_STAGE;
+            double* wsm = ls + BM * MS_LDL;
+            for (int i = tid; i < BM * (MS_BK / 2); i += MS_THREADS) {
+                const int r = i / (MS_BK / 2), c2 = i % (MS_BK / 2);
+                double* dst = ls + r * MS_LDL + 2 * c2;
+                if (row0 + r < M) cp_async16(dst, L + (int64_t)(row0 + r) * ldl + kk + 2 * c2);
+                else { dst[0] = 0.0; dst[1] = 0.0; }
+            }
+            for (int i = tid; i < MS_BK * (BN / 2); i += MS_THREADS) {
+                const int k = i / (BN / 2), c2 = i % (BN / 2);
+                const int col = col0 + 2 * c2;
+                double* dst = wsm + k * LDWS + 2 * c2;
+                if (col < N2) cp_async16(dst, W + (int64_t)(kk + k) * ldw + col);
+                else { dst[0] = 0.0; dst[1] = 0.0; }
+            }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");  // (possibly empty) group keeps the count
+    };
+
+#pragma unroll
+    for (int j = 0; j < MS_ST - 1; ++j) load_stage(j);
+    double rmx[4] = {0.0, 0.0, 0.0, 0.0};
+    double acc[4][NJ][2];
+    for (int64_t j = 0; j < nst; ++j) {
+        const int64_t t = t_begin + j / KS;
+        const int ks = (int)(j % KS);
+        const int row0 = (int)(t / ntn) * BM, col0 = (int)(t % ntn) * BN;
+        if (ks == 0) {  // C tile -> accumulators (acc = C - L W)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int r = row0 + wm * 32 + i * 8 + g;
+                const double* crow = ws + (int64_t)(rbase + r) * ld;
+#pragma unroll
+                for (int jj = 0; jj < NJ; ++jj) {
+                    const int c = col0 + wn * 32 + jj * 8 + 2 * q;
+                    if (r < M && c < N2) {
+                        const double2 v = __ldcs(reinterpret_cast<const double2*>(crow + c));
+                        acc[i][jj][0] = v.x;
+                        acc[i][jj][1] = v.y;
+                    } else {
+                        acc[i][jj][0] = 0.0;
+                        acc[i][jj][1] = 0.0;
+                    }
+                }
+            }
+        }
+        asm volatile("cp.async.wait_group %0;" ::"n"(MS_ST - 2) : "memory");
+        __syncthreads();  // stage j landed; buffer (j-1) % MS_ST is free
+        load_stage(j + MS_ST - 1);
+        const double* ls = sh + (int)(j % MS_ST) * MS_STAGE;
+        const double* wsm = ls + BM * MS_LDL;
+#pragma unroll
+        for (int k0 = 0; k0 < MS_BK; k0 += 4) {
+            double a[4], b[NJ];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) a[i] = ls[(wm * 32 + i * 8 + g) * MS_LDL + k0 + q];
+#pragma unroll
+            for (int jj = 0; jj < NJ; ++jj) b[jj] = wsm[(k0 + q) * LDWS + wn * 32 + jj * 8 + g];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int jj = 0; jj < NJ; ++jj) dmma(acc[i][jj][0], acc[i][jj][1], a[i], b[jj]);
+        }
+        if (ks != KS - 1) continue;
+        const int bm = (int)(t / ntn);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int r = row0 + wm * 32 + i * 8 + g;
+            double* crow = ws + (int64_t)(rbase + r) * ld;
+#pragma unroll
+            for (int jj = 0; jj < NJ; ++jj) {
+                const int c = col0 + wn * 32 + jj * 8 + 2 * q;
+                if (r < M && c < N2) {
+                    if (c + 1 < N2) {
+                        __stcs(reinterpret_cast<double2*>(crow + c), make_double2(acc[i][jj][0], acc[i][jj][1]));
+                        rmx[i] = fmax(rmx[i], fmax(fabs(acc[i][jj][0]), fabs(acc[i][jj][1])));
+                    } else {
+                        crow[c] = acc[i][jj][0];
+                        rmx[i] = fmax(rmx[i], fabs(acc[i][jj][0]));
+                    }
+                }
+            }
+        }
+        const bool flush = (t + 1 == t_end) || ((int)((t + 1) / ntn) != bm);
+        if (flush && wit) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                double mx = rmx[i];
+                mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+                mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+                const int r = row0 + wm * 32 + i * 8 + g;
+                if (q == 0 && r < M) atomicMax(wit + rbase + r, (unsigned long long)__double_as_longlong(mx));
+                rmx[i] = 0.0;
+            }
+        }
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
 }  // namespace
 
 cudaError_t k2_gather_fix(double* ws, int64_t ld, int32_t rbase, int32_t nrows, int32_t K, const K2Gather* gp,
@@ -296,20 +433,44 @@ cudaError_t k2_gemm(double* ws, int64_t ld, int32_t rbase, int32_t M, int32_t N2
     if (K != 64 && K != 128) return cudaErrorInvalidValue;
     const size_t smem = (size_t)2 * kStage * sizeof(double);
     static int sms = 0;
+    static long wn = 8;
     if (!sms) {
-        cudaError_t e = cudaFuncSetAttribute(k2_gemm_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(k2_gemm_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
+        const void* fns[] = {(const void*)k2_gemm_kernel<64, 8>, (const void*)k2_gemm_kernel<128, 8>,
+                             (const void*)k2_gemm_kernel<64, 4>, (const void*)k2_gemm_kernel<128, 4>};
+        for (const void* f : fns) {
+            cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e != cudaSuccess) return e;
+        }
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (const char* v = std::getenv("MCND_K2_GEMM_WN")) wn = std::strtol(v, nullptr, 10) == 4 ? 4 : 8;
     }
     const int64_t tiles = (int64_t)((N2 + BN - 1) / BN) * ((M + BM - 1) / BM);
     const int grid = (int)std::min<int64_t>(tiles, sms);
     auto* w = reinterpret_cast<unsigned long long*>(row_wit);
-    if (K == 64) k2_gemm_kernel<64><<<grid, kGThreads, smem, s>>>(ws, ld, rbase, M, N2, L, ldl, W, ldw, w, abort);
-    else k2_gemm_kernel<128><<<grid, kGThreads, smem, s>>>(ws, ld, rbase, M, N2, L, ldl, W, ldw, w, abort);
+    static long ms_mode = -1;
+    if (ms_mode < 0) {
+        const char* v = std::getenv("MCND_K2_GEMM_MS");
+        ms_mode = v ? std::strtol(v, nullptr, 10) : 1;
+        const size_t smem_ms = (size_t)MS_ST * MS_STAGE * sizeof(double);
+        cudaFuncSetAttribute(k2_gemm_ms_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_ms);
+        cudaFuncSetAttribute(k2_gemm_ms_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_ms);
+    }
+    if (ms_mode) {
+        const size_t smem_ms = (size_t)MS_ST * MS_STAGE * sizeof(double);
+        const int grid_ms = (int)std::min<int64_t>(tiles, 2 * (int64_t)sms);
+        if (K == 64) k2_gemm_ms_kernel<64><<<grid_ms, MS_THREADS, smem_ms, s>>>(ws, ld, rbase, M, N2, L, ldl, W, ldw, w, abort);
+        else k2_gemm_ms_kernel<128><<<grid_ms, MS_THREADS, smem_ms, s>>>(ws, ld, rbase, M, N2, L, ldl, W, ldw, w, abort);
+        return cudaGetLastError();
+    }
+    if (wn == 8) {
+        if (K == 64) k2_gemm_kernel<64, 8><<<grid, 512, smem, s>>>(ws, ld, rbase, M, N2, L, ldl, W, ldw, w, abort);
+        else k2_gemm_kernel<128, 8><<<grid, 512, smem, s>>>(ws, ld, rbase, M, N2, L, ldl, W, ldw, w, abort);
+    } else {
+        if (K == 64) k2_gemm_kernel<64, 4><<<grid, 256, smem, s>>>(ws, ld, rbase, M, N2, L, ldl, W, ldw, w, abort);
+        else k2_gemm_kernel<128, 4><<<grid, 256, smem, s>>>(ws, ld, rbase, M, N2, L, ldl, W, ldw, w, abort);
+    }
     return cudaGetLastError();
 }
 

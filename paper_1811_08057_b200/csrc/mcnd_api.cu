@@ -825,7 +825,7 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
             if (e == cudaSuccess) e = k2_pair_prep(gp0, gp1, (int32_t)m, Wb, ld, Wp, gpair, abort, st);
             const int32_t nr = (int32_t)(n - kb - 2 * b);
             if (e == cudaSuccess) e = k2_gather_fix(ws, ld, (int32_t)(kb + 2 * b), nr, 128, gpair, Lb, abort, st);
-            if (e == cudaSuccess)  // L[:, 64:128] -= L[:, 0:64] * Wp   (no witness: L is scratch)
+            if (e == cudaSuccess)  // NL[:, 64:128] += NL[:, 0:64] * (-Wp)   (NL = -L; no witness: scratch)
                 e = k2_gemm(Lb + b, 2 * b, 0, nr, (int32_t)b, 64, Lb, 2 * b, Wp, b, nullptr, abort, st);
             if (e == cudaSuccess)
                 e = k2_gemm(ws, ld, (int32_t)(kb + 2 * b), nr, (int32_t)(m - 2 * b), 128, Lb, 2 * b, Wb, ld, wit, abort, st);

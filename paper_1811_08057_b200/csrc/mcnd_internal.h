@@ -115,7 +115,7 @@ size_t kp_smem_bytes(int cw);
 
 // All launches are asynchronous on `s`; `abort` (device) short-circuits every
 // kernel once a panel pivot failed the witness test.
-// Per trailing row: L[r, 0:K] = A[r, P[0:K]], then A[r, c] = A[r, src] for the moved columns.
+// Per trailing row: L[r, 0:K] = -A[r, P[0:K]] (negated), then A[r, c] = A[r, src] for the moved columns.
 cudaError_t k2_gather_fix(double* ws, int64_t ld, int32_t rbase, int32_t nrows, int32_t K, const K2Gather* gp,
                           double* L, const unsigned* abort, cudaStream_t s);
 // Panel pair (two 64-row panels, one rank-128 trailing update): from the two panels'
@@ -124,7 +124,8 @@ cudaError_t k2_gather_fix(double* ws, int64_t ld, int32_t rbase, int32_t nrows, 
 cudaError_t k2_pair_prep(const K2Gather* g0, const K2Gather* g1, int32_t m, double* Wc, int64_t ldw, double* Wp,
                          K2Gather* gpair, const unsigned* abort, cudaStream_t s);
 
-// C[M x N2] (rows rbase.. of ws) -= L[M x K] W[K x N2], K in {64, 128}; L row stride ldl;
+// C[M x N2] (rows rbase.. of ws) += NL[M x K] W[K x N2], K in {64, 128}; NL (= -L, as written by
+// k2_gather_fix) row stride ldl;
 // row_wit (nullable) receives the running max |C| per row.
 cudaError_t k2_gemm(double* ws, int64_t ld, int32_t rbase, int32_t M, int32_t N2, int32_t K, const double* L,
                     int64_t ldl, const double* W, int64_t ldw, double* row_wit, const unsigned* abort, cudaStream_t s);
