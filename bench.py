@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--impl", default="mc", choices=["mc", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--force-dist", action="store_true",
+                    help="use the multi-GPU block-row driver even with one rank (test hook)")
     return ap.parse_args()
 
 
@@ -441,7 +443,7 @@ def main():
     if args.impl == "reference":
         return run_reference(args)
     rank, world, local = dist_env()
-    if world > 1:
+    if world > 1 or args.force_dist:
         from paper_1811_08057_b200 import dist
 
         return dist.bench_main(args)
