@@ -46,7 +46,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--method", default=None, choices=["unblocked", "blocked"],
-                    help="condensation variant (default: unblocked for c1-c3, blocked for c5)")
+                    help="condensation variant (default: unblocked for n < 2048 (c1, c2), blocked otherwise (c3, c5))")
     ap.add_argument("--fast", action="store_true", help="FMA update (default: reference-exact arithmetic)")
     ap.add_argument("--impl", default="mc", choices=["mc", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -20,8 +20,9 @@
 //
 // Because finished rows follow every column exchange, the winner column of
 // step s also carries T[t][s] = u_t(p_s) for t < s, and at the end the chunk
-// holds U in the FINAL layout: W = T^{-1} U is a back substitution in shared
-// memory, written straight to global.  CTA 0 derives the panel-start column
+// holds U in the FINAL layout.  Column s of T^{-1} is formed as soon as column s
+// of T arrives (off the critical path, one row per thread), so W = T^{-1} U at the
+// end is a register-blocked product written straight to global.  CTA 0 derives the panel-start column
 // of each pivot and the <= b moved columns for the trailing-row gather.
 #include <cstdint>
 #include <climits>
@@ -31,7 +32,11 @@ namespace mcnd {
 namespace {
 
 constexpr int kB = kK2B;
-constexpr int kThreads = 1024;
+#ifndef KP_THREADS
+#define KP_THREADS 512
+#endif
+constexpr int kThreads = KP_THREADS;
+constexpr int kTPR = kThreads / kK2B;  // threads per panel row in the load pass (8 or 16)
 constexpr unsigned kFull = 0xffffffffu;
 
 __device__ __forceinline__ bool beats(double av, int ai, double bv, int bi) {
@@ -55,19 +60,52 @@ __device__ __forceinline__ int aux_of(double2 r) { return (int)(unsigned)__doubl
 __device__ __forceinline__ void put(double2* p, double2 v) { __stcg(p, v); }
 __device__ __forceinline__ double2 get(const double2* p) { return __ldcg(p); }
 
+// Exact warp max of non-negative 64-bit patterns (|double| bits order like the values).
+__device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v) {
+    const unsigned hi = (unsigned)(v >> 32), lo = (unsigned)v;
+    const unsigned mh = __reduce_max_sync(kFull, hi);
+    const unsigned ml = __reduce_max_sync(kFull, hi == mh ? lo : 0u);
+    return ((unsigned long long)mh << 32) | ml;
+}
+__device__ __forceinline__ unsigned long long abs_bits(double x) {
+    return (unsigned long long)__double_as_longlong(x) & 0x7fffffffffffffffull;
+}
+
+// Cluster transport (kCl): every record is pushed into the same shared-memory slot of
+// every CTA of the cluster (DSMEM), and read back from the local copy.
+__device__ __forceinline__ void st_cluster(const double2* local, unsigned rank, double2 v) {
+    const unsigned a = (unsigned)__cvta_generic_to_shared(local);
+    unsigned r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+    asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};" ::"r"(r), "d"(v.x), "d"(v.y) : "memory");
+}
+__device__ __forceinline__ double2 ld_shared_volatile(const double2* q) {
+    double2 v;
+    const unsigned a = (unsigned)__cvta_generic_to_shared(q);
+    asm volatile("ld.volatile.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// receive slots per CTA: cand[2][16], wrec[2][16], last[2][64], col[2][16][64] (by step parity)
+constexpr int kClMax = kKPClusterMax;
+constexpr int kRcSlots = 4 * kClMax + 2 * kK2B + 2 * kClMax * kK2B;
+
 #ifndef KP_TRACE
 #define KP_TRACE 0  // microbenchmark knob: record per-step phase timestamps of CTA 0
 #endif
 #if KP_TRACE
-__device__ unsigned long long g_kp_trace[64][8];
+__device__ unsigned long long g_kp_trace[64][12];
 #define KP_MARK(s, k) do { if (blockIdx.x == 0 && threadIdx.x == 0) g_kp_trace[s][k] = clock64(); } while (0)
 #else
 #define KP_MARK(s, k) do { } while (0)
 #endif
 
+template <bool kCl>
 __global__ void __launch_bounds__(kThreads, 1) kp_panel_kernel(const KPParams p) {
     extern __shared__ __align__(16) double S[];  // [kB][cw]
-    __shared__ double sT[kB][kB + 1];
+    __shared__ double sTi[kB][kB + 1];  // T^{-1}, built one column per step
     __shared__ double s_mult2[2][kB], s_last2[2][kB];  // by step parity: warp 0 fetches step s
                                                        // while the bulk of step s-1 still reads
     __shared__ double s_rmax[kB], s_rmax2[kB];
@@ -82,28 +120,66 @@ __global__ void __launch_bounds__(kThreads, 1) kp_panel_kernel(const KPParams p)
     const int lo = g * cw;
     const int wc = max(0, min(cw, m - lo));  // my columns at panel start
     const unsigned long long t_start = globaltimer();
-    if (*(volatile const unsigned*)p.abort) return;
+    KP_MARK(0, 8);
+    if (*(volatile const unsigned*)p.abort) return;  // uniform: set only by earlier launches
+    // Record slots: global [step][CTA] history (grid variant) or parity-double-buffered
+    // local slots filled by DSMEM pushes (cluster variant: a step-s+1 push can only be
+    // issued after every CTA has consumed its step-s-1 records, see A below).
+    double2* const rc = reinterpret_cast<double2*>(S + kB * cw);
+    auto CAND = [&](int s, int h) -> double2* { return kCl ? rc + (s & 1) * kClMax + h : p.cand + s * G + h; };
+    auto WREC = [&](int s, int h) -> double2* {
+        return kCl ? rc + 2 * kClMax + (s & 1) * kClMax + h : p.wrec + s * G + h;
+    };
+    auto LAST = [&](int s, int r) -> double2* { return kCl ? rc + 4 * kClMax + (s & 1) * kB + r : p.lastbuf + s * kB + r; };
+    auto COL = [&](int s, int h, int r) -> double2* {
+        return kCl ? rc + 4 * kClMax + 2 * kB + ((s & 1) * kClMax + h) * kB + r : p.colbuf + ((int64_t)s * G + h) * kB + r;
+    };
+    auto PUT = [&](double2* q, double2 v) {
+        if constexpr (kCl) {
+            for (int h = 0; h < G; ++h) st_cluster(q, (unsigned)h, v);
+        } else {
+            put(q, v);
+        }
+    };
+    auto GET = [&](const double2* q) -> double2 {
+        if constexpr (kCl) return ld_shared_volatile(q);
+        else return get(q);
+    };
+    if constexpr (kCl)
+        for (int e = tid; e < kRcSlots; e += kThreads) rc[e] = make_double2(0.0, 0.0);
 
     // ---- load my chunk of the 64 panel rows; running max per row; candidate of row 0
-    for (int e = tid; e < kB * wc; e += kThreads) {
-        const int r = e / wc, c = e - r * wc;
-        S[r * cw + c] = p.ws[(int64_t)(p.row0 + r) * p.ld + lo + c];
+    for (int r = warp; r < kB; r += kThreads / 32) {  // row per warp, 16-byte loads (ld, lo, cw even)
+        const double* src = p.ws + (int64_t)(p.row0 + r) * p.ld + lo;
+        for (int c = 2 * lane; c < wc; c += 64) {
+            if (c + 1 < wc) {
+                const unsigned d = (unsigned)__cvta_generic_to_shared(S + r * cw + c);
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src + c) : "memory");
+            } else {
+                S[r * cw + c] = __ldcg(src + c);
+            }
+        }
     }
+    for (int e = tid; e < kB * (kB + 1); e += kThreads) {
+        const int t = e / (kB + 1), j = e - t * (kB + 1);
+        sTi[t][j] = (t == j) ? 1.0 : 0.0;
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
     if (tid == 0) s_stop = 0;
     if (g == 0 && tid == 0) p.pan->n_moved = 0;
     __syncthreads();
     {
-        const int r = tid >> 4, j = tid & 15;  // 64 rows x 16 threads (half warps)
-        const unsigned hm = 0xffffu << (lane & 16);
+        const int r = tid / kTPR, j = tid % kTPR;  // 64 rows x kTPR threads
+        const unsigned hm = ((1u << kTPR) - 1u) << (lane & (32 - kTPR));
         double mx = 0.0, bv = 0.0;
         int bi = INT_MAX;
-        for (int c = j; c < wc; c += 16) {
+        for (int c = j; c < wc; c += kTPR) {
             const double x = S[r * cw + c];
             mx = fmax(mx, fabs(x));
             if (r == 0 && beats(x, lo + c, bv, bi)) { bv = x; bi = lo + c; }
         }
 #pragma unroll
-        for (int o = 8; o; o >>= 1) {
+        for (int o = kTPR / 2; o; o >>= 1) {
             mx = fmax(mx, __shfl_xor_sync(hm, mx, o));
             const double ov = __shfl_xor_sync(hm, bv, o);
             const int oi = __shfl_xor_sync(hm, bi, o);
@@ -113,16 +189,18 @@ __global__ void __launch_bounds__(kThreads, 1) kp_panel_kernel(const KPParams p)
         if (r == 0 && j == 0) { s_cv = bv; s_cpos = bi; }
     }
     __syncthreads();
+    if constexpr (kCl) cluster_sync_all();  // every CTA's slots cleared before the first push
 
     // ---- publish the proposal for pivot 0 (row 0's candidate from the load pass)
     if (tid < kB) {
         const int pos = s_cpos;
-        put(p.colbuf + (int64_t)g * kB + tid, pack(pos != INT_MAX ? S[tid * cw + (pos - lo)] : 0.0, p.tag0, 0));
-        if (lo <= m - 1 && m - 1 < lo + wc) put(p.lastbuf + tid, pack(S[tid * cw + (m - 1 - lo)], p.tag0, 0));
-        if (tid == 0) put(p.cand + g, pack(s_cv, p.tag0, pos));
-        if (tid == 1) put(p.wrec + g, pack(s_rmax[0], p.tag0, 0));
+        PUT(COL(0, g, tid), pack(pos != INT_MAX ? S[tid * cw + (pos - lo)] : 0.0, p.tag0, 0));
+        if (lo <= m - 1 && m - 1 < lo + wc) PUT(LAST(0, tid), pack(S[tid * cw + (m - 1 - lo)], p.tag0, 0));
+        if (tid == 0) PUT(CAND(0, g), pack(s_cv, p.tag0, pos));
+        if (tid == 1) PUT(WREC(0, g), pack(s_rmax[0], p.tag0, 0));
     }
 
+    KP_MARK(0, 9);
     for (int s = 0; s < kB; ++s) {
         const int ms = m - s;  // active width before pivot s
         const unsigned tag = p.tag0 + (unsigned)s;
@@ -141,8 +219,8 @@ __global__ void __launch_bounds__(kThreads, 1) kp_panel_kernel(const KPParams p)
 #pragma unroll
                 for (int k = 0; k < kPer; ++k)
                     if (need & (1u << k)) {
-                        c[k] = get(p.cand + s * G + lane + 32 * k);
-                        w[k] = get(p.wrec + s * G + lane + 32 * k);
+                        c[k] = GET(CAND(s, lane + 32 * k));
+                        w[k] = GET(WREC(s, lane + 32 * k));
                     }
 #pragma unroll
                 for (int k = 0; k < kPer; ++k)
@@ -183,17 +261,17 @@ __global__ void __launch_bounds__(kThreads, 1) kp_panel_kernel(const KPParams p)
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                     const int r = lane + 32 * h;
-                    const double2* pm = p.colbuf + ((int64_t)s * G + bg) * kB + r;
-                    const double2* pl = p.lastbuf + s * kB + r;
-                    double2 cm = get(pm), cl = get(pl);
+                    const double2* pm = COL(s, bg, r);
+                    const double2* pl = LAST(s, r);
+                    double2 cm = GET(pm), cl = GET(pl);
                     while (tag_of(cm) != tag || tag_of(cl) != tag) {
                         if (globaltimer() - t_start > p.timeout_ns) {
                             atomicExch(&p.err->error, 1u);
                             s_stop = 1;
                             break;
                         }
-                        cm = get(pm);
-                        cl = get(pl);
+                        cm = GET(pm);
+                        cl = GET(pl);
                     }
                     s_mult[r] = cm.x;
                     s_last[r] = cl.x;
@@ -208,7 +286,7 @@ __global__ void __launch_bounds__(kThreads, 1) kp_panel_kernel(const KPParams p)
         }
         __syncthreads();
         KP_MARK(s, 1);
-        if (s_stop) return;
+        if (s_stop) goto finish;
         const double v = s_win_v;
         const int l = s_win_l;
         if (!(fabs(v) > kSingularRtol * s_win_w)) {  // condense.py:90 -> singular
@@ -218,74 +296,89 @@ __global__ void __launch_bounds__(kThreads, 1) kp_panel_kernel(const KPParams p)
                 p.rec[s].flag = p.epoch;
                 atomicExch(p.abort, 1u);
             }
-            return;
+            goto finish;
         }
         const int wn = max(0, min(wc, ms - 1 - lo));  // my active columns after the step
         KP_MARK(s, 7);
-        // ---- B. column exchange (condense.py:104-107): position l takes the last column
-        //         on every row (one element per row); row s scaled by true division
-        //         (condense.py:110); T column; the pivot record
-        if (tid < kB) {
-            if (l >= lo && l - lo < wn) S[tid * cw + (l - lo)] = (tid == s) ? __ddiv_rn(s_last[s], v) : s_last[tid];
-            if (tid < s) sT[tid][s] = s_mult[tid];  // T[t][s] = u_t(p_s), t < s
-        }
-        for (int c = tid; c < wn; c += kThreads)
-            if (lo + c != l) S[s * cw + c] = __ddiv_rn(S[s * cw + c], v);
-        if (g == 0 && tid == 0) {
-            p.rec[s].v = v;
-            p.rec[s].l = l;
-            p.rec[s].flag = p.epoch;
-        }
-        if (tid == 0) s_l[s] = l;
-        __syncthreads();
-        KP_MARK(s, 2);
-        KP_MARK(s, 3);
-        if (s + 1 == kB) break;
-        const double* us = S + s * cw;
-        // ---- D1. lookahead (warps 0-3): update row s+1, its running max, next candidate
+        // ---- B+D1. warps 0-3: row s scaled by true division (condense.py:110) with the
+        //      column exchange (condense.py:104-107) folded in, and -- lookahead -- row s+1
+        //      updated from it, its running max and the next candidate, published at once.
+        //      Warps 4-5 meanwhile: the exchange on the other rows, the T column, the record.
         constexpr int kLA = 64;   // publishing threads (D2)
-        constexpr int kD1 = 128;  // row s+1 update threads
+        constexpr int kD1 = 128;  // row s / s+1 threads
+        const int lx = (l >= lo && l - lo < wn) ? l - lo : -1;  // exchange target, local
+        const bool last_step = (s + 1 == kB);
+        const unsigned tag1 = tag + 1u;
         if (tid < kD1) {
-            const double mu = s_mult[s + 1];
-            double* row = S + (s + 1) * cw;
-            double mx = 0.0, bv = 0.0;
+            double* const rs = S + s * cw;
+            double* const row = S + (s + 1) * cw;
+            const double mu = last_step ? 0.0 : s_mult[s + 1];
+            // the row max IS |candidate|: one exact argmax (ties -> lowest column) via redux
+            unsigned long long bb = 0ull;
+            double bv = 0.0;
             int bi = INT_MAX;
             for (int c = tid; c < wn; c += kD1) {
-                const double y = __dsub_rn(row[c], __dmul_rn(mu, us[c]));
-                row[c] = y;
-                mx = fmax(mx, fabs(y));
-                if (beats(y, lo + c, bv, bi)) { bv = y; bi = lo + c; }
-            }
-#pragma unroll
-            for (int o = 16; o; o >>= 1) {
-                mx = fmax(mx, __shfl_xor_sync(kFull, mx, o));
-                const double ov = __shfl_xor_sync(kFull, bv, o);
-                const int oi = __shfl_xor_sync(kFull, bi, o);
-                if (beats(ov, oi, bv, bi)) { bv = ov; bi = oi; }
-            }
-            if (lane == 0) { s_lv[warp] = bv; s_li[warp] = bi; s_lm[warp] = mx; }
-            asm volatile("bar.sync 1, %0;" ::"n"(kD1));
-            if (tid == 0) {
-                double v0 = s_lv[0], m0 = s_lm[0];
-                int i0 = s_li[0];
-#pragma unroll
-                for (int k = 1; k < kD1 / 32; ++k) {
-                    if (beats(s_lv[k], s_li[k], v0, i0)) { v0 = s_lv[k]; i0 = s_li[k]; }
-                    m0 = fmax(m0, s_lm[k]);
+                const double q = __ddiv_rn(c == lx ? s_last[s] : rs[c], v);
+                rs[c] = q;
+                if (!last_step) {
+                    const double y = __dsub_rn(c == lx ? s_last[s + 1] : row[c], __dmul_rn(mu, q));
+                    row[c] = y;
+                    const unsigned long long yb = abs_bits(y);
+                    if (bi == INT_MAX || yb > bb) { bb = yb; bv = y; bi = lo + c; }
                 }
-                s_cv = v0;
-                s_cpos = i0;
-                s_rmax[s + 1] = fmax(fmax(s_rmax[s + 1], s_rmax2[s + 1]), m0);
+            }
+            KP_MARK(s, 3);
+            if (!last_step) {
+                const unsigned long long mb = warp_max_u64(bb);
+                const int wi = (int)__reduce_min_sync(kFull, bb == mb ? (unsigned)bi : 0xffffffffu);
+                if (bb == mb && bi == wi) { s_lv[warp] = bv; s_li[warp] = bi; s_lm[warp] = fabs(bv); }
+                if (lane == 0 && wi == INT_MAX) { s_lv[warp] = 0.0; s_li[warp] = INT_MAX; s_lm[warp] = 0.0; }
+                asm volatile("bar.sync 1, %0;" ::"n"(kD1));
+                KP_MARK(s, 5);
+                if (tid == 0) {
+                    double v0 = s_lv[0], m0 = s_lm[0];
+                    int i0 = s_li[0];
+#pragma unroll
+                    for (int k = 1; k < kD1 / 32; ++k) {
+                        if (beats(s_lv[k], s_li[k], v0, i0)) { v0 = s_lv[k]; i0 = s_li[k]; }
+                        m0 = fmax(m0, s_lm[k]);
+                    }
+                    s_cv = v0;
+                    s_cpos = i0;
+                    const double rm = fmax(fmax(s_rmax[s + 1], s_rmax2[s + 1]), m0);
+                    s_rmax[s + 1] = rm;
+                    // proposal of pivot s+1 goes out now; its column follows in D2
+                    PUT(WREC(s + 1, g), pack(rm, tag1, 0));
+                    PUT(CAND(s + 1, g), pack(v0, tag1, i0));
+                    KP_MARK(s, 6);
+                }
+            }
+        } else if (tid < kD1 + kB) {
+            const int r = tid - kD1;
+            if (lx >= 0 && r != s && r != s + 1) S[r * cw + lx] = s_last[r];
+            if (r < s) {  // T[t][s] = u_t(p_s) (t < s) arrives now: column s of T^{-1}, row r by thread r
+                double acc = 0.0;
+                for (int j = r; j < s; ++j) acc = fma(sTi[r][j], s_mult[j], acc);
+                sTi[r][s] = -acc;
+            }
+            if (r == 0) {
+                s_l[s] = l;
+                if (g == 0) {
+                    p.rec[s].v = v;
+                    p.rec[s].l = l;
+                    p.rec[s].flag = p.epoch;
+                }
             }
         }
         __syncthreads();
-        KP_MARK(s, 5);
+        KP_MARK(s, 2);
+        if (last_step) break;
+        const double* us = S + s * cw;
         const int pos = s_cpos;                                   // candidate column of pivot s+1
         const int pc = (pos != INT_MAX) ? pos - lo : -1;          // local
         const int lc = (ms - 2 >= lo && ms - 2 - lo < wn) ? ms - 2 - lo : -1;  // new last column, local
-        const unsigned tag1 = tag + 1u;
         if (tid < kLA) {
-            // ---- D2. publish pivot s+1's proposal (one row per thread): rows > s+1 get
+            // ---- D2. publish the candidate column of pivot s+1 (one row per thread): rows > s+1 get
             //          columns pc / lc updated here (E skips them); their maxima go to
             //          s_rmax2 (single writer, no atomics)
             const int r = tid;
@@ -302,64 +395,88 @@ __global__ void __launch_bounds__(kThreads, 1) kp_panel_kernel(const KPParams p)
                     xl = row[lc];
                     if (r > s + 1) { xl = __dsub_rn(xl, __dmul_rn(mu, us[lc])); row[lc] = xl; mx = fmax(mx, fabs(xl)); }
                 }
-                put(p.lastbuf + (s + 1) * kB + r, pack(xl, tag1, 0));
+                PUT(LAST(s + 1, r), pack(xl, tag1, 0));
             }
-            put(p.colbuf + ((int64_t)(s + 1) * G + g) * kB + r, pack(xc, tag1, 0));
+            PUT(COL(s + 1, g, r), pack(xc, tag1, 0));
             if (r > s + 1) s_rmax2[r] = fmax(s_rmax2[r], mx);
-            if (r == 1) put(p.wrec + (s + 1) * G + g, pack(s_rmax[s + 1], tag1, 0));
-            if (r == 0) put(p.cand + (s + 1) * G + g, pack(s_cv, tag1, pos));
-            KP_MARK(s, 6);
         } else {
-            // ---- E. bulk (warps 2..31): rows > s+1, all columns except pc / lc, with the
-            //         reference's two roundings (condense.py:118); per-row maxima by a
-            //         two-segment warp reduction
-            const int total = (kB - 2 - s) * wn;
-            constexpr int kBulk = kThreads - kLA;
-            for (int e0 = tid - kLA - lane; e0 < total; e0 += kBulk) {
-                const int e = e0 + lane;
-                double mx = 0.0;
-                int r = INT_MAX;
-                if (e < total) {
-                    r = s + 2 + e / wn;
-                    const int c = e - (r - s - 2) * wn;
-                    if (c != pc && c != lc) {
-                        const double y = __dsub_rn(S[r * cw + c], __dmul_rn(s_mult[r], us[c]));
-                        S[r * cw + c] = y;
-                        mx = fabs(y);
+            // ---- E. bulk (the other warps): rows > s+1, all columns except pc / lc, with
+            //         the reference's two roundings (condense.py:118).  Work units are
+            //         (row, 256-column segment) per warp, each lane two adjacent columns per
+            //         16-byte access; the segment's max is two redux ops + one shared
+            //         atomicMax.  Only the (rare) units holding pc or lc take the checked path.
+            constexpr int kSeg = 256;
+            const int nseg = (wn + kSeg - 1) / kSeg;
+            const int units = (kB - 2 - s) * nseg;
+            constexpr int kBulkWarps = (kThreads - kLA) / 32;
+            for (int u = warp - kLA / 32; u < units; u += kBulkWarps) {
+                const int q = u / nseg;
+                const int r = s + 2 + q;
+                const int c0 = (u - q * nseg) * kSeg;
+                const int c1 = min(wn, c0 + kSeg);
+                const double mu = s_mult[r];
+                double* row = S + r * cw;
+                unsigned long long mb = 0ull;
+                const bool chk = (pc >= c0 && pc < c1) || (lc >= c0 && lc < c1);
+#pragma unroll
+                for (int k = 0; k < kSeg / 64; ++k) {
+                    const int c = c0 + 64 * k + 2 * lane;
+                    if (c < c1) {
+                        const double2 x = *reinterpret_cast<const double2*>(row + c);
+                        const double2 pv = *reinterpret_cast<const double2*>(us + c);
+                        double2 y;
+                        y.x = __dsub_rn(x.x, __dmul_rn(mu, pv.x));
+                        y.y = __dsub_rn(x.y, __dmul_rn(mu, pv.y));  // c+1 may be a dropped column: harmless
+                        if (chk) {
+                            if (c == pc || c == lc) y.x = x.x;
+                            if (c + 1 == pc || c + 1 == lc || c + 1 >= c1) y.y = x.y;
+                        }
+                        *reinterpret_cast<double2*>(row + c) = y;
+                        const unsigned long long bx = (chk && (c == pc || c == lc)) ? 0ull : abs_bits(y.x);
+                        const unsigned long long by = (c + 1 >= c1 || (chk && (c + 1 == pc || c + 1 == lc))) ? 0ull : abs_bits(y.y);
+                        mb = max(mb, max(bx, by));
                     }
                 }
-                const int ra = __shfl_sync(kFull, r, 0);
-                double ma = (r == ra) ? mx : 0.0, mb = (r == ra) ? 0.0 : mx;
-#pragma unroll
-                for (int o = 16; o; o >>= 1) {
-                    ma = fmax(ma, __shfl_xor_sync(kFull, ma, o));
-                    mb = fmax(mb, __shfl_xor_sync(kFull, mb, o));
-                }
-                const int rb = __shfl_sync(kFull, r, 31);
-                if (lane == 0)
-                    atomicMax(reinterpret_cast<unsigned long long*>(s_rmax) + ra,
-                              (unsigned long long)__double_as_longlong(ma));
-                if (lane == 31 && rb != ra && rb != INT_MAX)
-                    atomicMax(reinterpret_cast<unsigned long long*>(s_rmax) + rb,
-                              (unsigned long long)__double_as_longlong(mb));
+                mb = warp_max_u64(mb);
+                if (lane == 0) atomicMax(reinterpret_cast<unsigned long long*>(s_rmax) + r, mb);
             }
         }
         KP_MARK(s, 4);
     }
     __syncthreads();
 
-    // ---- W = T^{-1} U on my final columns (T unit upper triangular), right-looking
+    KP_MARK(0, 10);
+    // ---- W = T^{-1} U on my final columns (T unit upper triangular)
+    {
     const int wf = max(0, min(wc, m - kB - lo));
-    for (int s = kB - 1; s >= 1; --s) {
-        for (int e = tid; e < s * wf; e += kThreads) {
-            const int t = e / wf, c = e - t * wf;
-            S[t * cw + c] = fma(-sT[t][s], S[s * cw + c], S[t * cw + c]);
+    // W = T^{-1} U straight to global: warp w owns rows 4w..4w+3, lane owns columns
+    // lane + 32k (k < 4) of each 128-column pass: T^{-1} reads are warp broadcasts, U
+    // reads and W stores are contiguous across the warp
+    for (int tb = warp; tb < kB / 4; tb += kThreads / 32) {
+        for (int c0 = 0; c0 < wf; c0 += 128) {
+            double acc[4][4] = {};
+            for (int j = 4 * tb; j < kB; ++j) {
+                double u[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int c = c0 + lane + 32 * k;
+                    u[k] = (c < wf) ? S[j * cw + c] : 0.0;
+                }
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const double a = sTi[4 * tb + i][j];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) acc[i][k] = fma(a, u[k], acc[i][k]);
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int c = c0 + lane + 32 * k;
+                    if (c < wf) p.W[(int64_t)(4 * tb + i) * p.ldw + lo + c] = acc[i][k];
+                }
         }
-        __syncthreads();
-    }
-    for (int e = tid; e < kB * wf; e += kThreads) {
-        const int t = e / wf, c = e - t * wf;
-        p.W[(int64_t)t * p.ldw + lo + c] = S[t * cw + c];
     }
     // ---- panel-start column of each pivot and the moved final columns (CTA 0)
     if (g == 0 && tid < kB) {
@@ -381,19 +498,71 @@ __global__ void __launch_bounds__(kThreads, 1) kp_panel_kernel(const KPParams p)
             }
         }
     }
+    }
+    KP_MARK(0, 11);
+finish:
+    if constexpr (kCl) cluster_sync_all();  // no CTA leaves while peers may still push into it
 }
 
 }  // namespace
 
-size_t kp_smem_bytes(int cw) { return (size_t)kB * cw * sizeof(double); }
+size_t kp_smem_bytes(int cw, bool cluster) {
+    return (size_t)kB * cw * sizeof(double) + (cluster ? kRcSlots * sizeof(double2) : 0);
+}
+
+int kp_cluster_fits(int G, int cw) {
+    if (G < 1 || G > kClMax) return 0;
+    const size_t smem = kp_smem_bytes(cw, true);
+    if (cudaFuncSetAttribute(kp_panel_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
+        cudaFuncSetAttribute(kp_panel_kernel<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)G;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3((unsigned)G);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, kp_panel_kernel<true>, &cfg) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
 
 cudaError_t kp_launch(const KPParams& p, cudaStream_t s) {
-    const size_t smem = kp_smem_bytes(p.cw);
-    cudaError_t e = cudaFuncSetAttribute(kp_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
+    const bool cl = p.cluster != 0;
+    const size_t smem = kp_smem_bytes(p.cw, cl);
     KPParams pc = p;
+    if (cl) {
+        cudaError_t e = cudaFuncSetAttribute(kp_panel_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(kp_panel_kernel<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (e != cudaSuccess) return e;
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = (unsigned)p.G;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.gridDim = dim3((unsigned)p.G);
+        cfg.blockDim = dim3(kThreads);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = s;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        return cudaLaunchKernelEx(&cfg, kp_panel_kernel<true>, pc);
+    }
+    cudaError_t e = cudaFuncSetAttribute(kp_panel_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
     void* args[] = {&pc};
-    return cudaLaunchCooperativeKernel((const void*)kp_panel_kernel, dim3(p.G), dim3(kThreads), args, smem, s);
+    return cudaLaunchCooperativeKernel((const void*)kp_panel_kernel<false>, dim3(p.G), dim3(kThreads), args, smem, s);
 }
 
 }  // namespace mcnd

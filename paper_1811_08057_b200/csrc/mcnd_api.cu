@@ -20,6 +20,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <deque>
+#include <map>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -65,6 +66,15 @@ struct Buffers {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     int sms = 0;
     uint32_t epoch = 0;
+    std::map<std::pair<int64_t, int64_t>, bool> kp_cluster_cache;  // (G, cw) -> co-residency
+    bool kp_cluster_ok(int64_t G, int64_t cw) {
+        const auto key = std::make_pair(G, cw);
+        auto it = kp_cluster_cache.find(key);
+        if (it != kp_cluster_cache.end()) return it->second;
+        const bool ok = kp_cluster_fits((int)G, (int)cw) > 0;
+        kp_cluster_cache[key] = ok;
+        return ok;
+    }
 };
 std::mutex g_mu;
 std::deque<Buffers> g_bufs;
@@ -789,15 +799,31 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
     kp.lastbuf = (double2*)(base + o_lastb);
     kp.err = err;
     kp.timeout_ns = 20ull * 1000000000ull;
-    auto run_kp = [&](int64_t kb, K2Gather* gp, double* Wout) -> cudaError_t {
-        const int64_t m = n - kb;
-        int64_t G = std::min<int64_t>({(int64_t)B->sms, (int64_t)kKPMaxG, std::max<int64_t>(1, m / 128)});
+    // Panel placement: one thread-block cluster of up to kKPClusterMax CTAs (records
+    // pushed over DSMEM) whenever the panel fits its shared memory, else the
+    // grid-wide cooperative variant (records through L2).
+    const int64_t g_cl = std::min<int64_t>(env_long("MCND_KP_CLUSTER", 0), kKPClusterMax);
+    auto split = [&](int64_t m, int64_t G, int64_t* cw_out) {
         int64_t cw = 0;
         for (;; --G) {
             cw = (int64_t)align_up((size_t)((m + G - 1) / G), 2);
             if (G == 1 || m - (G - 1) * cw >= b) break;
         }
-        if (kp_smem_bytes((int)cw) > 190 * 1024) return cudaErrorInvalidValue;
+        *cw_out = cw;
+        return G;
+    };
+    auto run_kp = [&](int64_t kb, K2Gather* gp, double* Wout) -> cudaError_t {
+        const int64_t m = n - kb;
+        int64_t cw = 0, G = 0;
+        kp.cluster = 0;
+        if (g_cl >= 2) {
+            G = split(m, std::min<int64_t>(g_cl, std::max<int64_t>(1, m / 64)), &cw);
+            kp.cluster = (G >= 2 && kp_smem_bytes((int)cw, true) <= 200 * 1024 && B->kp_cluster_ok(G, cw)) ? 1 : 0;
+        }
+        if (!kp.cluster) {
+            G = split(m, std::min<int64_t>({(int64_t)B->sms, (int64_t)kKPMaxG, std::max<int64_t>(1, m / 128)}), &cw);
+            if (kp_smem_bytes((int)cw, false) > 190 * 1024) return cudaErrorInvalidValue;
+        }
         kp.row0 = (int32_t)kb;
         kp.m = (int32_t)m;
         kp.G = (int32_t)G;

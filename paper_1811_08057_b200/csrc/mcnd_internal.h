@@ -108,10 +108,14 @@ struct KPParams {
     double2* lastbuf;         // [64][64]  {last active column values, tag}
     K1Err* err;
     unsigned long long timeout_ns;
+    int32_t cluster;          // 1: one thread-block cluster, records pushed over DSMEM (G <= kKPClusterMax)
 };
 constexpr int kKPMaxG = 160;
+constexpr int kKPClusterMax = 16;
 cudaError_t kp_launch(const KPParams& p, cudaStream_t s);
-size_t kp_smem_bytes(int cw);
+size_t kp_smem_bytes(int cw, bool cluster);
+// clusters of G CTAs (chunk width cw) that can be co-resident; 0 if the shape cannot launch
+int kp_cluster_fits(int G, int cw);
 
 // All launches are asynchronous on `s`; `abort` (device) short-circuits every
 // kernel once a panel pivot failed the witness test.

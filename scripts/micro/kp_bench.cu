@@ -1,5 +1,7 @@
 // Standalone run of the K2 panel kernel on a random 64 x m panel, with per-step phase trace.
+#ifndef KP_TRACE
 #define KP_TRACE 1
+#endif
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
@@ -9,6 +11,7 @@ using namespace mcnd;
 int main(int argc, char** argv) {
     const int m = argc > 1 ? atoi(argv[1]) : 16384;
     const int G = argc > 2 ? atoi(argv[2]) : 128;
+    const int cl = argc > 3 ? atoi(argv[3]) : 0;
     int cw = ((m + G - 1) / G + 1) / 2 * 2;
     const int64_t ld = (m + 15) / 16 * 16;
     std::vector<double> h((size_t)64 * ld);
@@ -27,7 +30,8 @@ int main(int argc, char** argv) {
     KPParams p{};
     p.ws = ws; p.ld = ld; p.row0 = 0; p.m = m; p.G = G; p.cw = cw; p.wit = wit; p.rec = rec; p.epoch = 1;
     p.W = W; p.ldw = ld; p.pan = pan; p.abort = abort; p.cand = cand; p.wrec = wrec; p.colbuf = colb; p.lastbuf = lastb;
-    p.err = err; p.timeout_ns = 5000000000ull;
+    p.err = err; p.timeout_ns = 5000000000ull; p.cluster = cl;
+    if (cl) printf("cluster fits: %d\n", kp_cluster_fits(G, cw));
     for (int it = 0; it < 3; ++it) {
         cudaMemcpy(ws, h.data(), h.size() * 8, cudaMemcpyHostToDevice);
         p.tag0 = (unsigned)(1000 + it * 100);
@@ -36,19 +40,40 @@ int main(int argc, char** argv) {
         cudaError_t e = kp_launch(p, 0);
         cudaEventRecord(e1); cudaEventSynchronize(e1);
         float ms; cudaEventElapsedTime(&ms, e0, e1);
-        printf("m=%d G=%d cw=%d: %.1f us (%.2f us/step) %s\n", m, G, cw, ms * 1e3, ms * 1e3 / 64, cudaGetErrorString(e));
+        printf("m=%d G=%d cl=%d cw=%d: %.1f us (%.2f us/step) %s\n", m, G, cl, cw, ms * 1e3, ms * 1e3 / 64, cudaGetErrorString(e));
     }
-    unsigned long long tr[64][6];
+    {   // cross-check against the other transport on the same input (same G, cw: bitwise)
+        std::vector<double> w1((size_t)64 * ld), w2((size_t)64 * ld);
+        std::vector<PivRec> r1(64), r2(64);
+        cudaMemcpy(w1.data(), W, w1.size() * 8, cudaMemcpyDeviceToHost);
+        cudaMemcpy(r1.data(), rec, 64 * sizeof(PivRec), cudaMemcpyDeviceToHost);
+        cudaMemcpy(ws, h.data(), h.size() * 8, cudaMemcpyHostToDevice);
+        cudaMemset(W, 0, (size_t)64 * ld * 8);
+        KPParams q = p; q.cluster = !cl; q.tag0 = 77777;
+        cudaError_t e = kp_launch(q, 0);
+        cudaDeviceSynchronize();
+        cudaMemcpy(w2.data(), W, w2.size() * 8, cudaMemcpyDeviceToHost);
+        cudaMemcpy(r2.data(), rec, 64 * sizeof(PivRec), cudaMemcpyDeviceToHost);
+        long dw = 0, dr = 0;
+        for (int t = 0; t < 64; ++t) for (int c = 0; c < m - 64; ++c) dw += w1[(size_t)t * ld + c] != w2[(size_t)t * ld + c];
+        for (int t = 0; t < 64; ++t) dr += (r1[t].v != r2[t].v) || (r1[t].l != r2[t].l);
+        printf("cross-check vs cluster=%d (%s): W mismatches %ld, pivot mismatches %ld, piv0 %.17g l0 %d\n", !cl,
+               cudaGetErrorString(e), dw, dr, r1[0].v, r1[0].l);
+    }
+#if KP_TRACE
+    unsigned long long tr[64][12];
     cudaMemcpyFromSymbol(tr, g_kp_trace, sizeof(tr));
-    double acc[5] = {0};
-    for (int s = 1; s < 63; ++s) {
-        acc[0] += (tr[s][1] - tr[s][0]) * 1e-3;  // publish + exchange
-        acc[1] += (tr[s][2] - tr[s][1]) * 1e-3;  // winner column fetch
-        acc[2] += (tr[s][3] - tr[s][2]) * 1e-3;  // row s scale
-        acc[3] += (tr[s][4] - tr[s][3]) * 1e-3;  // update
-        acc[4] += (tr[s + 1][0] - tr[s][4]) * 1e-3;
+    const int idx[7] = {0, 1, 3, 5, 6, 2, 4};
+    const char* nm[7] = {"A", "D1loop", "D1red", "combine+put", "sync", "D2", "tail"};
+    double acc[7] = {0};
+    for (int s = 1; s < 62; ++s) {
+        for (int k = 0; k < 6; ++k) acc[k] += (double)(tr[s][idx[k + 1]] - tr[s][idx[k]]);
+        acc[6] += (double)(tr[s + 1][0] - tr[s][0]);
     }
-    printf("per step (us): exchange %.2f  fetch %.2f  scale %.2f  update %.2f  loop %.2f\n", acc[0] / 62, acc[1] / 62,
-           acc[2] / 62, acc[3] / 62, acc[4] / 62);
+    printf("per step (cycles):");
+    for (int k = 0; k < 7; ++k) printf(" %s %.0f", k == 6 ? "total" : nm[k], acc[k] / 61);
+    printf("\n");
+    printf("  prologue %llu cycles, loop %llu, W %llu\n", tr[0][9] - tr[0][8], tr[0][10] - tr[0][9], tr[0][11] - tr[0][10]);
+#endif
     return 0;
 }

@@ -330,6 +330,18 @@ def test_blocked_vs_oracle(mc, env_knob, tail):
         assert np.allclose(piv, ref.pivots, rtol=1e-8, atol=1e-12)
 
 
+def test_blocked_cluster_transport_identical(mc, env_knob):
+    """The panel kernel's DSMEM (thread-block cluster) transport performs exactly
+    the grid transport's arithmetic: identical pivots and log|det|."""
+    a = np.random.default_rng(21).uniform(-1, 1, (1500, 1500))
+    env_knob("MCND_KP_CLUSTER", 0)
+    ref = mc.logdet_blocked(a, return_pivots=True)
+    env_knob("MCND_KP_CLUSTER", 16)
+    got = mc.logdet_blocked(a, return_pivots=True)
+    assert got[0] == ref[0]
+    assert np.array_equal(got[1], ref[1]) and np.array_equal(got[2], ref[2])
+
+
 def test_blocked_singular_and_edges(mc, env_knob):
     env_knob("MCND_K2_TAIL", 2)
     from paper_1811_08057_b200 import matrix as M
