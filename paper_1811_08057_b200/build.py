@@ -18,7 +18,7 @@ NVCC_FLAGS = [
     "-O3", "-lineinfo", "-std=c++17",
     "-Xcompiler", "-fPIC,-ffp-contract=off,-fno-fast-math",
     "-Xptxas", "-O3",
-]
+] + [f"-D{d}" for d in os.environ.get("MCND_BUILD_DEFINES", "").split() if d]
 
 
 def nvcc() -> str:

@@ -285,22 +285,32 @@ constexpr int MS_LDL = MS_BK + 4;             // 20 doubles: conflict-free A fra
 constexpr int MS_STAGE = BM * MS_LDL + MS_BK * LDWS;
 constexpr int MS_THREADS = 256;               // 8 warps: 2 (M) x 4 (N), warp tile 32 x 32
 
-template <int K>
-__global__ void __launch_bounds__(MS_THREADS, 2) k2_gemm_ms_kernel(double* __restrict__ ws, int64_t ld, int32_t rbase,
+// SUB = 2: a "fat" CTA of two independent 256-thread sub-CTAs (own smem ring, own named
+// barrier) that fills a whole SM, so a grid of B fat CTAs occupies exactly B SMs and
+// leaves the rest free for the panel kernel running concurrently on another stream.
+template <int K, int SUB>
+__global__ void __launch_bounds__(MS_THREADS * SUB, 2 / SUB) k2_gemm_ms_kernel(double* __restrict__ ws, int64_t ld, int32_t rbase,
                                                                    int32_t M, int32_t N2, const double* __restrict__ L,
                                                                    int64_t ldl, const double* __restrict__ W, int64_t ldw,
                                                                    unsigned long long* __restrict__ wit,
                                                                    const unsigned* __restrict__ abort) {
     constexpr int KS = K / MS_BK;  // stages per tile
     constexpr int WN = 4, NJ = 4;
-    extern __shared__ __align__(16) double sh[];
+    extern __shared__ __align__(16) double sh_all[];
     if (*(volatile const unsigned*)abort) return;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int sub = SUB == 2 ? (int)(threadIdx.x >= MS_THREADS) : 0;
+    double* const sh = sh_all + sub * (MS_ST * MS_STAGE);
+    auto sync = [&]() {
+        if constexpr (SUB == 1) __syncthreads();
+        else asm volatile("bar.sync %0, %1;" ::"r"(1 + sub), "n"(MS_THREADS) : "memory");
+    };
+    const int tid = (int)threadIdx.x - sub * MS_THREADS, lane = tid & 31, warp = tid >> 5;
     const int wm = warp / WN, wn = warp % WN;
     const int g = lane >> 2, q = lane & 3;
     const int ntn = (N2 + BN - 1) / BN, ntm = (M + BM - 1) / BM;
     const int64_t T = (int64_t)ntn * ntm;
-    const int64_t t_begin = T * blockIdx.x / gridDim.x, t_end = T * (blockIdx.x + 1) / gridDim.x;
+    const int64_t vb = (int64_t)blockIdx.x * SUB + sub, vg = (int64_t)gridDim.x * SUB;
+    const int64_t t_begin = T * vb / vg, t_end = T * (vb + 1) / vg;
     if (t_begin >= t_end) return;
     const int64_t nst = (t_end - t_begin) * KS;
 
@@ -356,7 +366,7 @@ __global__ void __launch_bounds__(MS_THREADS, 2) k2_gemm_ms_kernel(double* __res
             }
         }
         asm volatile("cp.async.wait_group %0;" ::"n"(MS_ST - 2) : "memory");
-        __syncthreads();  // stage j landed; buffer (j-1) % MS_ST is free
+        sync();  // stage j landed; buffer (j-1) % MS_ST is free
         load_stage(j + MS_ST - 1);
         const double* ls = sh + (int)(j % MS_ST) * MS_STAGE;
         const double* wsm = ls + BM * MS_LDL;
@@ -428,7 +438,8 @@ cudaError_t k2_pair_prep(const K2Gather* g0, const K2Gather* g1, int32_t m, doub
 }
 
 cudaError_t k2_gemm(double* ws, int64_t ld, int32_t rbase, int32_t M, int32_t N2, int32_t K, const double* L,
-                    int64_t ldl, const double* W, int64_t ldw, double* row_wit, const unsigned* abort, cudaStream_t s) {
+                    int64_t ldl, const double* W, int64_t ldw, double* row_wit, const unsigned* abort, cudaStream_t s,
+                    int sm_budget) {
     if (M <= 0 || N2 <= 0) return cudaSuccess;
     if (K != 64 && K != 128) return cudaErrorInvalidValue;
     const size_t smem = (size_t)2 * kStage * sizeof(double);
@@ -454,14 +465,23 @@ cudaError_t k2_gemm(double* ws, int64_t ld, int32_t rbase, int32_t M, int32_t N2
         const char* v = std::getenv("MCND_K2_GEMM_MS");
         ms_mode = v ? std::strtol(v, nullptr, 10) : 1;
         const size_t smem_ms = (size_t)MS_ST * MS_STAGE * sizeof(double);
-        cudaFuncSetAttribute(k2_gemm_ms_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_ms);
-        cudaFuncSetAttribute(k2_gemm_ms_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_ms);
+        cudaFuncSetAttribute(k2_gemm_ms_kernel<64, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_ms);
+        cudaFuncSetAttribute(k2_gemm_ms_kernel<128, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_ms);
+        cudaFuncSetAttribute(k2_gemm_ms_kernel<64, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * (int)smem_ms);
+        cudaFuncSetAttribute(k2_gemm_ms_kernel<128, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * (int)smem_ms);
+    }
+    if (sm_budget > 0) {  // fat CTAs on at most sm_budget SMs
+        const size_t smem_ms = (size_t)MS_ST * MS_STAGE * sizeof(double);
+        const int grid_f = (int)std::min<int64_t>((tiles + 1) / 2, sm_budget);
+        if (K == 64) k2_gemm_ms_kernel<64, 2><<<grid_f, 2 * MS_THREADS, 2 * smem_ms, s>>>(ws, ld, rbase, M, N2, L, ldl, W, ldw, w, abort);
+        else k2_gemm_ms_kernel<128, 2><<<grid_f, 2 * MS_THREADS, 2 * smem_ms, s>>>(ws, ld, rbase, M, N2, L, ldl, W, ldw, w, abort);
+        return cudaGetLastError();
     }
     if (ms_mode) {
         const size_t smem_ms = (size_t)MS_ST * MS_STAGE * sizeof(double);
         const int grid_ms = (int)std::min<int64_t>(tiles, 2 * (int64_t)sms);
-        if (K == 64) k2_gemm_ms_kernel<64><<<grid_ms, MS_THREADS, smem_ms, s>>>(ws, ld, rbase, M, N2, L, ldl, W, ldw, w, abort);
-        else k2_gemm_ms_kernel<128><<<grid_ms, MS_THREADS, smem_ms, s>>>(ws, ld, rbase, M, N2, L, ldl, W, ldw, w, abort);
+        if (K == 64) k2_gemm_ms_kernel<64, 1><<<grid_ms, MS_THREADS, smem_ms, s>>>(ws, ld, rbase, M, N2, L, ldl, W, ldw, w, abort);
+        else k2_gemm_ms_kernel<128, 1><<<grid_ms, MS_THREADS, smem_ms, s>>>(ws, ld, rbase, M, N2, L, ldl, W, ldw, w, abort);
         return cudaGetLastError();
     }
     if (wn == 8) {

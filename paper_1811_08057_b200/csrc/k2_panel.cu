@@ -50,15 +50,42 @@ __device__ __forceinline__ unsigned long long globaltimer() {
     return t;
 }
 
+// Record = {value, tag:32 | check:16 | aux:16}.  The 16-bit check (a hash of the
+// value bits) detects a torn 16-byte read (new tag, stale value): such a record is
+// treated as not yet arrived.  aux carries a candidate position (< 2^16 - 1).
+__device__ __forceinline__ unsigned h16(double v) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+    const unsigned x = (unsigned)b ^ (unsigned)(b >> 32) ^ 0x9e3779b9u;
+    return (x ^ (x >> 16)) & 0xffffu;
+}
 __device__ __forceinline__ double2 pack(double v, unsigned tag, int aux) {
-    return make_double2(v, __longlong_as_double((long long)(((unsigned long long)tag << 32) | (unsigned)aux)));
+    const unsigned a16 = (aux == INT_MAX) ? 0xffffu : ((unsigned)aux & 0xffffu);
+    return make_double2(v, __longlong_as_double((long long)(((unsigned long long)tag << 32) | (h16(v) << 16) | a16)));
 }
 __device__ __forceinline__ unsigned tag_of(double2 r) {
     return (unsigned)((unsigned long long)__double_as_longlong(r.y) >> 32);
 }
-__device__ __forceinline__ int aux_of(double2 r) { return (int)(unsigned)__double_as_longlong(r.y); }
-__device__ __forceinline__ void put(double2* p, double2 v) { __stcg(p, v); }
-__device__ __forceinline__ double2 get(const double2* p) { return __ldcg(p); }
+__device__ __forceinline__ int aux_of(double2 r) {
+    const unsigned a16 = (unsigned)__double_as_longlong(r.y) & 0xffffu;
+    return a16 == 0xffffu ? INT_MAX : (int)a16;
+}
+__device__ __forceinline__ bool rec_ok(double2 r, unsigned tag, unsigned* torn) {
+    if (tag_of(r) != tag) return false;
+    if ((((unsigned)__double_as_longlong(r.y) >> 16) & 0xffffu) == h16(r.x)) return true;
+    atomicAdd(torn, 1u);
+    return false;
+}
+// Record traffic goes through L2 with relaxed gpu-scope accesses.  The polling
+// loads MUST be asm volatile: a plain __ldcg in a spin loop may legally be hoisted
+// by the compiler (it did, depending on the surrounding code), hanging the panel.
+__device__ __forceinline__ void put(double2* p, double2 v) {
+    asm volatile("st.relaxed.gpu.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
+}
+__device__ __forceinline__ double2 get(const double2* p) {
+    double2 v;
+    asm volatile("ld.relaxed.gpu.global.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p) : "memory");
+    return v;
+}
 
 // Exact warp max of non-negative 64-bit patterns (|double| bits order like the values).
 __device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v) {
@@ -224,9 +251,25 @@ __global__ void __launch_bounds__(kThreads, 1) kp_panel_kernel(const KPParams p)
                     }
 #pragma unroll
                 for (int k = 0; k < kPer; ++k)
-                    if ((need & (1u << k)) && tag_of(c[k]) == tag && tag_of(w[k]) == tag) need &= ~(1u << k);
+                    if ((need & (1u << k)) && rec_ok(c[k], tag, &p.err->pad) && rec_ok(w[k], tag, &p.err->pad))
+                        need &= ~(1u << k);
                 if (__all_sync(kFull, need == 0)) break;
                 if (globaltimer() - t_start > p.timeout_ns) {
+#ifdef KP_DEBUG
+                    for (int k = 0; k < kPer; ++k)
+                        if (need & (1u << k))
+                            printf("KP timeout A: g=%d s=%d row0=%d m=%d G=%d cw=%d waiting rec %d: cand tag %x wrec tag %x want %x\n",
+                                   g, s, p.row0, m, G, cw, lane + 32 * k, tag_of(c[k]), tag_of(w[k]), tag);
+#endif
+                    {
+                        const unsigned nb = __ballot_sync(kFull, need != 0);
+                        if (lane == (int)(__ffs(nb) - 1) && atomicCAS(&p.err->dbg[0], 0u, 1u) == 0u) {
+                            int k = __ffs(need) - 1;
+                            p.err->dbg[1] = (unsigned)g; p.err->dbg[2] = (unsigned)s; p.err->dbg[3] = (unsigned)(lane + 32 * k);
+                            p.err->dbg[4] = tag_of(c[k]); p.err->dbg[5] = tag_of(w[k]); p.err->dbg[6] = tag;
+                            p.err->dbg[7] = (unsigned)G;
+                        }
+                    }
                     if (lane == 0) {
                         atomicExch(&p.err->error, 1u);
                         atomicExch(&p.err->err_step, (unsigned)(p.row0 + s));
@@ -264,9 +307,19 @@ __global__ void __launch_bounds__(kThreads, 1) kp_panel_kernel(const KPParams p)
                     const double2* pm = COL(s, bg, r);
                     const double2* pl = LAST(s, r);
                     double2 cm = GET(pm), cl = GET(pl);
-                    while (tag_of(cm) != tag || tag_of(cl) != tag) {
+                    while (!rec_ok(cm, tag, &p.err->pad) || !rec_ok(cl, tag, &p.err->pad)) {
                         if (globaltimer() - t_start > p.timeout_ns) {
+#ifdef KP_DEBUG
+                            printf("KP timeout col: g=%d s=%d row0=%d m=%d G=%d r=%d bg=%d bi=%d coltag %x lasttag %x want %x\n",
+                                   g, s, p.row0, m, G, r, bg, bi, tag_of(cm), tag_of(cl), tag);
+#endif
+                            if (atomicCAS(&p.err->dbg[0], 0u, 2u) == 0u) {
+                                p.err->dbg[1] = (unsigned)g; p.err->dbg[2] = (unsigned)s; p.err->dbg[3] = (unsigned)bg;
+                                p.err->dbg[4] = tag_of(cm); p.err->dbg[5] = tag_of(cl); p.err->dbg[6] = tag;
+                                p.err->dbg[7] = (unsigned)r;
+                            }
                             atomicExch(&p.err->error, 1u);
+                            atomicExch(&p.err->err_step, (unsigned)(p.row0 + s));
                             s_stop = 1;
                             break;
                         }
@@ -427,14 +480,15 @@ __global__ void __launch_bounds__(kThreads, 1) kp_panel_kernel(const KPParams p)
                         double2 y;
                         y.x = __dsub_rn(x.x, __dmul_rn(mu, pv.x));
                         y.y = __dsub_rn(x.y, __dmul_rn(mu, pv.y));  // c+1 may be a dropped column: harmless
-                        if (chk) {
-                            if (c == pc || c == lc) y.x = x.x;
-                            if (c + 1 == pc || c + 1 == lc || c + 1 >= c1) y.y = x.y;
+                        if (!chk) {
+                            *reinterpret_cast<double2*>(row + c) = y;
+                            mb = max(mb, max(abs_bits(y.x), c + 1 < c1 ? abs_bits(y.y) : 0ull));
+                        } else {
+                            // pc / lc belong to D2, which is updating them right now: never write
+                            // them back (not even unchanged), element-wise stores only
+                            if (c != pc && c != lc) { row[c] = y.x; mb = max(mb, abs_bits(y.x)); }
+                            if (c + 1 < c1 && c + 1 != pc && c + 1 != lc) { row[c + 1] = y.y; mb = max(mb, abs_bits(y.y)); }
                         }
-                        *reinterpret_cast<double2*>(row + c) = y;
-                        const unsigned long long bx = (chk && (c == pc || c == lc)) ? 0ull : abs_bits(y.x);
-                        const unsigned long long by = (c + 1 >= c1 || (chk && (c + 1 == pc || c + 1 == lc))) ? 0ull : abs_bits(y.y);
-                        mb = max(mb, max(bx, by));
                     }
                 }
                 mb = warp_max_u64(mb);

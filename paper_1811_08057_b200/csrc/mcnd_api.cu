@@ -64,6 +64,8 @@ struct Buffers {
     void* din = nullptr;   size_t din_bytes = 0;    // H2D staging for host-input calls
     void* hpin = nullptr;  size_t hpin_bytes = 0;   // pinned metadata / result staging
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    cudaStream_t side = nullptr;                 // K2: trailing updates overlapped with the next panels
+    cudaEvent_t ev_a = nullptr, ev_b = nullptr;  // K2: stream joins
     int sms = 0;
     uint32_t epoch = 0;
     std::map<std::pair<int64_t, int64_t>, bool> kp_cluster_cache;  // (G, cw) -> co-residency
@@ -84,6 +86,10 @@ int init_buffers(Buffers& b, int dev) {
     cudaDeviceGetAttribute(&b.sms, cudaDevAttrMultiProcessorCount, dev);
     if (cudaEventCreate(&b.ev0) != cudaSuccess || cudaEventCreate(&b.ev1) != cudaSuccess)
         return fail(MCND_ECUDA, "cudaEventCreate failed");
+    if (cudaEventCreateWithFlags(&b.ev_a, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&b.ev_b, cudaEventDisableTiming) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&b.side, cudaStreamNonBlocking) != cudaSuccess)
+        return fail(MCND_ECUDA, "cudaEventCreate/cudaStreamCreate failed");
     return MCND_OK;
 }
 
@@ -701,8 +707,8 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
     const size_t o_ws = take((size_t)n * ld * sizeof(double));
     const size_t o_wit = take((size_t)n * sizeof(double));
     const size_t o_rec = take((size_t)n * sizeof(PivRec));
-    const size_t o_L = take((size_t)std::max<int64_t>(n, 1) * 2 * b * sizeof(double));
-    const size_t o_W = take((size_t)2 * b * ld * sizeof(double));
+    const size_t o_L = take((size_t)2 * std::max<int64_t>(n, 1) * 2 * b * sizeof(double));  // x2: by pair parity
+    const size_t o_W = take((size_t)2 * 2 * b * ld * sizeof(double));
     const size_t o_pan = take(3 * sizeof(K2Gather));
     const size_t o_Wp = take((size_t)b * b * sizeof(double));
     const size_t o_cand = take((size_t)64 * kKPMaxG * sizeof(double2));
@@ -812,6 +818,10 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
         *cw_out = cw;
         return G;
     };
+    auto kp_grid = [&](int64_t m) {
+        int64_t cw = 0;
+        return split(m, std::min<int64_t>({(int64_t)B->sms, (int64_t)kKPMaxG, std::max<int64_t>(1, m / 128)}), &cw);
+    };
     auto run_kp = [&](int64_t kb, K2Gather* gp, double* Wout) -> cudaError_t {
         const int64_t m = n - kb;
         int64_t cw = 0, G = 0;
@@ -838,33 +848,90 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
     // k+1, and ONE rank-128 trailing update (half the C traffic of two rank-64
     // updates).  L of the pair = [A[R, P_k], A'[R, P_{k+1}]] where the second
     // half is corrected for panel k by a 64-wide DMMA update: L1 -= L0 * W_k[:, P_{k+1}].
+    //
+    // Look-ahead: the trailing update is split.  The rows the NEXT pair factors are
+    // updated first on the caller's stream; the remaining rows go to a side stream as
+    // "fat" GEMM CTAs on (SMs - panel CTAs) SMs, running while the next two panels
+    // are factored on the SMs left free.  The next pair's own trailing gather waits
+    // for that side update (one event each way).  L and W are double-buffered by
+    // pair parity so the side GEMM can read pair q's while pair q+1 writes its own.
     const bool pairs = env_long("MCND_K2_PAIRS", 1) != 0;
+    const bool overlap = pairs && env_long("MCND_K2_OVERLAP", 1) != 0;
+    const int64_t min_budget = env_long("MCND_K2_MIN_BUDGET", B->sms / 4);
+    bool side_pending = false;
+    cudaStream_t side = B->side;
+    auto join_side = [&]() -> cudaError_t {
+        if (!side_pending) return cudaSuccess;
+        side_pending = false;
+        return cudaStreamWaitEvent(st, B->ev_b, 0);
+    };
     int64_t k = 0;
+    int par = 0;
     while (k < n_panels) {
         const int64_t kb = k * b, m = n - kb;
+        double* const Wq = Wb + (size_t)par * 2 * b * ld;
+        double* const Lq = Lb + (size_t)par * std::max<int64_t>(n, 1) * 2 * b;
         if (pairs && k + 1 < n_panels) {
-            e = run_kp(kb, gp0, Wb);
-            if (e == cudaSuccess) e = k2_gather_fix(ws, ld, (int32_t)(kb + b), (int32_t)b, 64, gp0, Lb, abort, st);
+            e = run_kp(kb, gp0, Wq);
+            if (e == cudaSuccess) e = k2_gather_fix(ws, ld, (int32_t)(kb + b), (int32_t)b, 64, gp0, Lq, abort, st);
             if (e == cudaSuccess)
-                e = k2_gemm(ws, ld, (int32_t)(kb + b), (int32_t)b, (int32_t)(m - b), 64, Lb, 64, Wb, ld, wit, abort, st);
-            if (e == cudaSuccess) e = run_kp(kb + b, gp1, Wb + b * ld);
-            if (e == cudaSuccess) e = k2_pair_prep(gp0, gp1, (int32_t)m, Wb, ld, Wp, gpair, abort, st);
+                e = k2_gemm(ws, ld, (int32_t)(kb + b), (int32_t)b, (int32_t)(m - b), 64, Lq, 64, Wq, ld, wit, abort, st);
+            if (e == cudaSuccess) e = run_kp(kb + b, gp1, Wq + b * ld);
+            if (e == cudaSuccess) e = k2_pair_prep(gp0, gp1, (int32_t)m, Wq, ld, Wp, gpair, abort, st);
+            if (e == cudaSuccess) e = join_side();  // trailing rows final for the previous pair
             const int32_t nr = (int32_t)(n - kb - 2 * b);
-            if (e == cudaSuccess) e = k2_gather_fix(ws, ld, (int32_t)(kb + 2 * b), nr, 128, gpair, Lb, abort, st);
+            if (e == cudaSuccess) e = k2_gather_fix(ws, ld, (int32_t)(kb + 2 * b), nr, 128, gpair, Lq, abort, st);
             if (e == cudaSuccess)  // NL[:, 64:128] += NL[:, 0:64] * (-Wp)   (NL = -L; no witness: scratch)
-                e = k2_gemm(Lb + b, 2 * b, 0, nr, (int32_t)b, 64, Lb, 2 * b, Wp, b, nullptr, abort, st);
+                e = k2_gemm(Lq + b, 2 * b, 0, nr, (int32_t)b, 64, Lq, 2 * b, Wp, b, nullptr, abort, st);
+            // rows the next unit factors: a pair (128), a last single panel (64), or the tail (all)
+            const int64_t k2 = k + 2;
+            int64_t ahead = (k2 + 1 < n_panels) ? 2 * b : (k2 < n_panels ? b : nr);
+            int64_t budget = 0;
+            if (overlap && ahead < nr) {
+                // worth it only if the side GEMM on the SMs the next panels leave free
+                // finishes within (next pair's panel work + the full-machine GEMM):
+                // ~20 TF/s DMMA on all SMs, ~0.55 ms of panel work per pair
+                budget = (int64_t)B->sms - kp_grid(n - k2 * b);
+                const double t_full = 2.0 * (double)(nr - ahead) * (double)(m - 2 * b) * 128.0 / 20e12;
+                const double t_side = budget > 0 ? t_full * (double)B->sms / (double)budget : 1e30;
+                if (budget < min_budget || t_side > t_full + 0.55e-3) ahead = nr;
+            } else {
+                ahead = nr;
+            }
+            if (e == cudaSuccess && ahead < nr) {  // side stream: from here on L and W of this pair are final
+                e = cudaEventRecord(B->ev_a, st);
+                if (e == cudaSuccess) e = cudaStreamWaitEvent(side, B->ev_a, 0);
+            }
             if (e == cudaSuccess)
-                e = k2_gemm(ws, ld, (int32_t)(kb + 2 * b), nr, (int32_t)(m - 2 * b), 128, Lb, 2 * b, Wb, ld, wit, abort, st);
+                e = k2_gemm(ws, ld, (int32_t)(kb + 2 * b), (int32_t)ahead, (int32_t)(m - 2 * b), 128, Lq, 2 * b, Wq, ld,
+                            wit, abort, st);
+            if (e == cudaSuccess && ahead < nr) {
+                if (e == cudaSuccess)
+                    e = k2_gemm(ws, ld, (int32_t)(kb + 2 * b + ahead), (int32_t)(nr - ahead), (int32_t)(m - 2 * b), 128,
+                                Lq + ahead * 2 * b, 2 * b, Wq, ld, wit, abort, side, (int)budget);
+                if (e == cudaSuccess) e = cudaEventRecord(B->ev_b, side);
+                side_pending = (e == cudaSuccess);
+            }
             k += 2;
+            par ^= 1;
         } else {
-            e = run_kp(kb, gp0, Wb);
-            if (e == cudaSuccess) e = k2_gather_fix(ws, ld, (int32_t)(kb + b), (int32_t)(n - kb - b), 64, gp0, Lb, abort, st);
+            e = run_kp(kb, gp0, Wq);
+            if (e == cudaSuccess) e = join_side();
             if (e == cudaSuccess)
-                e = k2_gemm(ws, ld, (int32_t)(kb + b), (int32_t)(n - kb - b), (int32_t)(m - b), 64, Lb, 64, Wb, ld, wit, abort, st);
+                e = k2_gather_fix(ws, ld, (int32_t)(kb + b), (int32_t)(n - kb - b), 64, gp0, Lq, abort, st);
+            if (e == cudaSuccess)
+                e = k2_gemm(ws, ld, (int32_t)(kb + b), (int32_t)(n - kb - b), (int32_t)(m - b), 64, Lq, 64, Wq, ld, wit,
+                            abort, st);
             k += 1;
+            par ^= 1;
         }
-        if (e != cudaSuccess) return fail(MCND_ECUDA, "K2 panel kernels: %s", cudaGetErrorString(e));
+        if (e != cudaSuccess) {
+            join_side();
+            return fail(MCND_ECUDA, "K2 panel kernels: %s", cudaGetErrorString(e));
+        }
     }
+    e = join_side();
+    if (e != cudaSuccess) return fail(MCND_ECUDA, "K2 stream join: %s", cudaGetErrorString(e));
     // 3. unblocked tail (publishes the final 1x1)
     p.in_place = 1; p.wit_in = wit; p.row_pstep = d_iota;
     p.ncol0 = (int32_t)mt; p.n_steps = (int32_t)(mt - 1); p.seq = d_iota + kb_end; p.pstep_offset = (int32_t)kb_end;
@@ -882,8 +949,12 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
     float ms = 0.f;
     cudaEventElapsedTime(&ms, B->ev0, B->ev1);
     out->device_ms = ms;
+    if (h_err->pad && std::getenv("MCND_DEBUG")) std::fprintf(stderr, "mcnd: %u torn panel records re-read\n", h_err->pad);
     if (h_err->nonfinite) return fail(MCND_EINVAL, "matrix entries must be finite (no NaN/Inf)");
-    if (h_err->error) return fail(MCND_EDEVICE, "device timeout waiting for pivot %u", h_err->err_step);
+    if (h_err->error)
+        return fail(MCND_EDEVICE, "device timeout waiting for pivot %u [%u g=%u s=%u i=%u tags %x %x want %x G/r=%u]",
+                    h_err->err_step, h_err->dbg[0], h_err->dbg[1], h_err->dbg[2], h_err->dbg[3], h_err->dbg[4],
+                    h_err->dbg[5], h_err->dbg[6], h_err->dbg[7]);
     int64_t sing = -1;
     for (int64_t t = 0; t < n; ++t) {
         if (h_rec[t].flag != epoch || h_rec[t].l < 0) { sing = t; break; }

@@ -26,6 +26,7 @@ struct K1Err {
     unsigned err_step;
     unsigned nonfinite; // nonzero: the input held NaN/Inf (-> ValueError)
     unsigned pad;
+    unsigned dbg[8];    // diagnostics of the first timeout (panel kernel)
 };
 
 // Persistent, barrier-free condensation kernel parameters (k1_condense.cu).
@@ -131,8 +132,10 @@ cudaError_t k2_pair_prep(const K2Gather* g0, const K2Gather* g1, int32_t m, doub
 // C[M x N2] (rows rbase.. of ws) += NL[M x K] W[K x N2], K in {64, 128}; NL (= -L, as written by
 // k2_gather_fix) row stride ldl;
 // row_wit (nullable) receives the running max |C| per row.
+// sm_budget > 0: at most that many SMs, one "fat" CTA each (the rest stay free).
 cudaError_t k2_gemm(double* ws, int64_t ld, int32_t rbase, int32_t M, int32_t N2, int32_t K, const double* L,
-                    int64_t ldl, const double* W, int64_t ldw, double* row_wit, const unsigned* abort, cudaStream_t s);
+                    int64_t ldl, const double* W, int64_t ldw, double* row_wit, const unsigned* abort, cudaStream_t s,
+                    int sm_budget = 0);
 
 // nonfinite (nullable, device): set to nonzero if any input entry is NaN/Inf.
 cudaError_t k3_launch(const double* a, int64_t batch, int64_t n, int64_t stride, bool fast,

@@ -1,0 +1,10 @@
+"""Blocked K2 on C3 (N=8000 U[-1,1] seed 3), run twice (warm + profiled by ncu -c)."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import paper_1811_08057_b200 as mc
+from paper_1811_08057_b200 import matrix as M
+a = torch.from_numpy(M.config_uniform(8000, 3)).cuda()
+for _ in range(2):
+    print(mc.logdet_blocked(a, return_pivots=True)[3])
+torch.cuda.synchronize()

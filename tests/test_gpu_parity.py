@@ -342,6 +342,25 @@ def test_blocked_cluster_transport_identical(mc, env_knob):
     assert np.array_equal(got[1], ref[1]) and np.array_equal(got[2], ref[2])
 
 
+@pytest.mark.parametrize("n", [4000, 8000])
+def test_blocked_lookahead_identical(mc, env_knob, n):
+    """The look-ahead schedule (trailing update split over two streams, side GEMM
+    concurrent with the next panels) performs exactly the serial schedule's
+    arithmetic: identical pivots, repeatedly (catches timing-dependent races
+    between the panel kernel's phases that only show under concurrency)."""
+    import torch
+    from paper_1811_08057_b200 import matrix as M
+
+    a = torch.from_numpy(M.config_uniform(n, 3)).cuda()
+    env_knob("MCND_K2_OVERLAP", 0)
+    ref = mc.logdet_blocked(a, return_pivots=True)
+    env_knob("MCND_K2_OVERLAP", 1)
+    for _ in range(3):
+        got = mc.logdet_blocked(a, return_pivots=True)
+        assert got[0] == ref[0]
+        assert np.array_equal(got[1], ref[1]) and np.array_equal(got[2], ref[2])
+
+
 def test_blocked_singular_and_edges(mc, env_knob):
     env_knob("MCND_K2_TAIL", 2)
     from paper_1811_08057_b200 import matrix as M
