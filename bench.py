@@ -272,12 +272,14 @@ def run_single(args):
         res = fn(d, fast=args.fast)
     torch.cuda.synchronize()
     kernel_ms = []
+    launches = 0
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         ev0.record(stream)
         for _ in range(args.steps):
             res, piv, cols, kms = fn(d, fast=args.fast, return_pivots=True)
             kernel_ms.append(kms)
+            launches += mc._lib.LAST_LAUNCHES  # counted by the library per call
         ev1.record(stream)
         torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1) / args.steps
@@ -333,7 +335,7 @@ def run_single(args):
         "roofline": roof,
         "e2e": {"value": flops(n) / (ms_e2e * 1e-3) / 1e9, "unit": "GFLOP/s", "ms_per_step": ms_e2e,
                 "h2d_bytes_per_step": 8 * n * n, "d2h_bytes_per_step": 12 * n + 16},
-        "gpu_launches": args.steps * (1 if method == "unblocked" else blocked_launches(n)),
+        "gpu_launches": launches,
         "clocks": clk.summary(),
     }
     if args.method is None and args.config in ("c2", "c3"):
@@ -356,13 +358,6 @@ def run_single(args):
     if not args.no_cpu_baseline and a is not None:
         line["cpu_baseline"] = cpu_baseline(a, args.cpu_seconds)
     print(json.dumps(line), flush=True)
-
-
-def blocked_launches(n, b=64, tail=1024):
-    """Kernels one blocked logdet launches: init + per panel pair 7 (KP, gather, GEMM,
-    KP, pair-prep, gather, L-correction GEMM, trailing GEMM = 8) / single panel 3 + tail."""
-    panels = (n - tail) // b if n - tail >= b else 0
-    return 1 + (panels // 2) * 8 + (panels % 2) * 3 + 1
 
 
 def check_parity(cfg, res, fast):

@@ -52,6 +52,7 @@ typedef struct mcnd_logdet {
     int64_t invalid_row;     /* the offending row id (MCND_EPIVOT)              */
     double device_ms;        /* device time of the condensation (CUDA events)   */
     int64_t steps;           /* condensation steps executed                      */
+    int64_t launches;        /* GPU kernels this call launched (0 if not counted) */
 } mcnd_logdet;
 
 /* Communication accounting of the block-row driver (runtime.py:47-66). */

@@ -27,7 +27,8 @@ FLAG_GROUPS = 2
 class McndLogDet(ctypes.Structure):
     _fields_ = [("sign", ctypes.c_int32), ("singular", ctypes.c_int32), ("log_abs", ctypes.c_double),
                 ("singular_step", ctypes.c_int64), ("invalid_step", ctypes.c_int64),
-                ("invalid_row", ctypes.c_int64), ("device_ms", ctypes.c_double), ("steps", ctypes.c_int64)]
+                ("invalid_row", ctypes.c_int64), ("device_ms", ctypes.c_double), ("steps", ctypes.c_int64),
+                ("launches", ctypes.c_int64)]
 
 
 class McndCommStats(ctypes.Structure):
@@ -37,6 +38,7 @@ class McndCommStats(ctypes.Structure):
 
 
 _lock = threading.Lock()
+LAST_LAUNCHES = 0  # GPU kernels launched by the most recent single-matrix call (bench accounting)
 _lib = None
 
 EXPORTS = (

@@ -111,6 +111,7 @@ def logdet_condensation(a, pivot_sequence: Optional[Sequence[int]] = None, *, fa
             a.ctypes.data, n, n, None if seq is None else seq.ctypes.data, slen, flags, None,
             ctypes.byref(out), piv.ctypes.data, cols.ctypes.data)
     _lib.check(rc)
+    _lib.LAST_LAUNCHES = int(out.launches)
     res = SINGULAR if out.singular else LogDet(int(out.sign), float(out.log_abs))
     if return_pivots:
         steps = int(out.steps)
@@ -144,6 +145,7 @@ def logdet_blocked(a, *, fast: bool = False, return_pivots: bool = False):
         rc = lib.mcnd_logdet_blocked(a.ctypes.data, n, n, flags, None, ctypes.byref(out), piv.ctypes.data,
                                      cols.ctypes.data)
     _lib.check(rc)
+    _lib.LAST_LAUNCHES = int(out.launches)
     res = SINGULAR if out.singular else LogDet(int(out.sign), float(out.log_abs))
     if return_pivots:
         k = int(out.steps) + (0 if out.singular else 1)

@@ -522,6 +522,7 @@ int serial_dev(const double* d_a, int64_t n, int64_t lda, const int64_t* seq_in,
                       nullptr);
     if (rc) return rc;
     out->device_ms = run.device_ms;
+    out->launches = 1;
     if (pivots_out) for (size_t t = 0; t < run.piv_val.size(); ++t) pivots_out[t] = run.piv_val[t];
     if (cols_out) for (size_t t = 0; t < run.piv_col.size(); ++t) cols_out[t] = run.piv_col[t];
     if (run.singular_at >= 0) {
@@ -659,6 +660,7 @@ int parallel_dev(const double* d_a, int64_t n, int64_t lda, int32_t p, uint32_t 
                       p, &rem, &rem_wit);
     if (rc) return rc;
     out->device_ms = run.device_ms;
+    out->launches = 1;
     if (owners_out) for (size_t t = 0; t < owner.size(); ++t) owners_out[t] = owner[t];
     return fold_parallel(n, p, run.piv_val.data(), run.piv_col.data(), run.singular_at, rem.data(), rem_wit.data(),
                          out, stats, payload_out, row_updates_out);
@@ -691,7 +693,7 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
     if (!B) return code;
     const bool fast = (flags & MCND_FLAG_FAST) != 0;
     const int64_t b = kK2B;
-    int64_t m_tail = env_long("MCND_K2_TAIL", 1024);
+    int64_t m_tail = env_long("MCND_K2_TAIL", 256);
     if (m_tail < 2) m_tail = 2;
     const int64_t n_panels = (n - m_tail >= b) ? (n - m_tail) / b : 0;
     const int64_t kb_end = n_panels * b;
@@ -867,6 +869,7 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
     };
     int64_t k = 0;
     int par = 0;
+    int64_t n_launch = 1;  // kernels launched by this call (K1 init so far)
     while (k < n_panels) {
         const int64_t kb = k * b, m = n - kb;
         double* const Wq = Wb + (size_t)par * 2 * b * ld;
@@ -911,7 +914,9 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
                                 Lq + ahead * 2 * b, 2 * b, Wq, ld, wit, abort, side, (int)budget);
                 if (e == cudaSuccess) e = cudaEventRecord(B->ev_b, side);
                 side_pending = (e == cudaSuccess);
+                ++n_launch;
             }
+            n_launch += 8;  // 2 panels, gather, update of panel k+1, pair prep, gather, L correction, trailing
             k += 2;
             par ^= 1;
         } else {
@@ -922,6 +927,7 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
             if (e == cudaSuccess)
                 e = k2_gemm(ws, ld, (int32_t)(kb + b), (int32_t)(n - kb - b), (int32_t)(m - b), 64, Lq, 64, Wq, ld, wit,
                             abort, st);
+            n_launch += 3;
             k += 1;
             par ^= 1;
         }
@@ -939,6 +945,7 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
     e = k1_launch(p, fast, st);
     if (e != cudaSuccess) return fail(MCND_ECUDA, "K2 tail launch: %s", cudaGetErrorString(e));
     CUDA_TRY(cudaEventRecord(B->ev1, st));
+    out->launches = n_launch + 1;
 
     PivRec* h_rec = (PivRec*)B->hpin;
     K1Err* h_err = (K1Err*)((char*)B->hpin + align_up((size_t)n * sizeof(PivRec), 64));
