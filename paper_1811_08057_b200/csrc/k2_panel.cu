@@ -24,6 +24,7 @@
 // of T arrives (off the critical path, one row per thread), so W = T^{-1} U at the
 // end is a register-blocked product written straight to global.  CTA 0 derives the panel-start column
 // of each pivot and the <= b moved columns for the trailing-row gather.
+#include <algorithm>
 #include <cstdint>
 #include <climits>
 #include "mcnd_internal.h"
@@ -69,8 +70,12 @@ __device__ __forceinline__ int aux_of(double2 r) {
     const unsigned a16 = (unsigned)__double_as_longlong(r.y) & 0xffffu;
     return a16 == 0xffffu ? INT_MAX : (int)a16;
 }
+#ifndef KP_HASH
+#define KP_HASH 1
+#endif
 __device__ __forceinline__ bool rec_ok(double2 r, unsigned tag, unsigned* torn) {
     if (tag_of(r) != tag) return false;
+    if (!KP_HASH) return true;
     if ((((unsigned)__double_as_longlong(r.y) >> 16) & 0xffffu) == h16(r.x)) return true;
     atomicAdd(torn, 1u);
     return false;
@@ -78,13 +83,30 @@ __device__ __forceinline__ bool rec_ok(double2 r, unsigned tag, unsigned* torn) 
 // Record traffic goes through L2 with relaxed gpu-scope accesses.  The polling
 // loads MUST be asm volatile: a plain __ldcg in a spin loop may legally be hoisted
 // by the compiler (it did, depending on the surrounding code), hanging the panel.
+#ifndef KP_LDMODE
+#define KP_LDMODE 0  // microbenchmark knob: 0 relaxed.gpu, 1 __ldcg/__stcg, 2 asm volatile .cg
+#endif
 __device__ __forceinline__ void put(double2* p, double2 v) {
+#if KP_LDMODE == 1
+    __stcg(p, v);
+#elif KP_LDMODE == 2
+    asm volatile("st.global.cg.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
+#else
     asm volatile("st.relaxed.gpu.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
+#endif
 }
 __device__ __forceinline__ double2 get(const double2* p) {
+#if KP_LDMODE == 1
+    return __ldcg(p);
+#else
     double2 v;
+#if KP_LDMODE == 2
+    asm volatile("ld.global.cg.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p) : "memory");
+#else
     asm volatile("ld.relaxed.gpu.global.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p) : "memory");
+#endif
     return v;
+#endif
 }
 
 // Exact warp max of non-negative 64-bit patterns (|double| bits order like the values).
@@ -119,6 +141,11 @@ __device__ __forceinline__ void cluster_sync_all() {
 constexpr int kClMax = kKPClusterMax;
 constexpr int kRcSlots = 4 * kClMax + 2 * kK2B + 2 * kClMax * kK2B;
 
+// Span log of the panel launches (CTA 0: globaltimer at entry and exit), read by
+// mcnd_debug_kp_spans() for schedule analysis; two stores per panel.
+__device__ unsigned long long g_kp_span[4096][2];
+__device__ unsigned g_kp_span_n;
+
 #ifndef KP_TRACE
 #define KP_TRACE 0  // microbenchmark knob: record per-step phase timestamps of CTA 0
 #endif
@@ -136,8 +163,9 @@ __global__ void __launch_bounds__(kThreads, 1) kp_panel_kernel(const KPParams p)
     __shared__ double s_mult2[2][kB], s_last2[2][kB];  // by step parity: warp 0 fetches step s
                                                        // while the bulk of step s-1 still reads
     __shared__ double s_rmax[kB], s_rmax2[kB];
-    __shared__ double s_lv[4], s_lm[4];
-    __shared__ int s_li[4];
+    __shared__ double s_wit0[kB];  // witnesses the panel rows carry in (constant during the panel)
+    __shared__ double s_lv[8], s_lm[8];
+    __shared__ int s_li[8];
     __shared__ int s_l[kB];
     __shared__ double s_cv, s_win_v, s_win_w;
     __shared__ int s_cpos, s_win_l, s_win_g, s_stop;
@@ -148,6 +176,11 @@ __global__ void __launch_bounds__(kThreads, 1) kp_panel_kernel(const KPParams p)
     const int wc = max(0, min(cw, m - lo));  // my columns at panel start
     const unsigned long long t_start = globaltimer();
     KP_MARK(0, 8);
+    unsigned span_slot = 0;
+    if (g == 0 && tid == 0) {
+        span_slot = atomicAdd(&g_kp_span_n, 1u) & 4095u;
+        g_kp_span[span_slot][0] = t_start;
+    }
     if (*(volatile const unsigned*)p.abort) return;  // uniform: set only by earlier launches
     // Record slots: global [step][CTA] history (grid variant) or parity-double-buffered
     // local slots filled by DSMEM pushes (cluster variant: a step-s+1 push can only be
@@ -172,6 +205,10 @@ __global__ void __launch_bounds__(kThreads, 1) kp_panel_kernel(const KPParams p)
         if constexpr (kCl) return ld_shared_volatile(q);
         else return get(q);
     };
+    auto GET1 = [&](const double2* q) -> double2 {  // one-shot read (never inside a spin loop)
+        if constexpr (kCl) return ld_shared_volatile(q);
+        else return __ldcg(q);
+    };
     if constexpr (kCl)
         for (int e = tid; e < kRcSlots; e += kThreads) rc[e] = make_double2(0.0, 0.0);
 
@@ -193,6 +230,7 @@ __global__ void __launch_bounds__(kThreads, 1) kp_panel_kernel(const KPParams p)
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
     if (tid == 0) s_stop = 0;
+    if (tid < kB) s_wit0[tid] = p.wit[p.row0 + tid];
     if (g == 0 && tid == 0) p.pan->n_moved = 0;
     __syncthreads();
     {
@@ -278,44 +316,53 @@ __global__ void __launch_bounds__(kThreads, 1) kp_panel_kernel(const KPParams p)
                     break;
                 }
             }
-            double bv = 0.0, bw = 0.0;
+            if (s > 0) KP_MARK(s, 8);
+            // exact argmax of |value| (ties -> lowest column) and max of the running row
+            // maxima: per-lane scan, then redux on the 64-bit |x| patterns
+            unsigned long long kb = 0ull, wb = 0ull;
             int bi = INT_MAX, bg = 0;
+            double bv = 0.0;
 #pragma unroll
             for (int k = 0; k < kPer; ++k) {
                 const int h = lane + 32 * k;
                 if (h < G) {
-                    if (beats(c[k].x, aux_of(c[k]), bv, bi)) { bv = c[k].x; bi = aux_of(c[k]); bg = h; }
-                    bw = fmax(bw, w[k].x);
+                    const unsigned long long xb = abs_bits(c[k].x);
+                    const int xi = aux_of(c[k]);
+                    if (xb > kb || (xb == kb && xi < bi)) { kb = xb; bi = xi; bv = c[k].x; bg = h; }
+                    wb = max(wb, abs_bits(w[k].x));
                 }
             }
-#pragma unroll
-            for (int o = 16; o; o >>= 1) {
-                const double ov = __shfl_xor_sync(kFull, bv, o);
-                const int oi = __shfl_xor_sync(kFull, bi, o);
-                const int og = __shfl_xor_sync(kFull, bg, o);
-                const double ow = __shfl_xor_sync(kFull, bw, o);
-                if (beats(ov, oi, bv, bi)) { bv = ov; bi = oi; bg = og; }
-                bw = fmax(bw, ow);
-            }
-            bw = fmax(bw, p.wit[p.row0 + s]);
+            const unsigned long long mb = warp_max_u64(kb);
+            const unsigned wi = __reduce_min_sync(kFull, kb == mb ? (unsigned)bi : 0xffffffffu);
+            const int src = __ffs(__ballot_sync(kFull, kb == mb && (unsigned)bi == wi)) - 1;
+            bv = __shfl_sync(kFull, bv, src);
+            bi = __shfl_sync(kFull, bi, src);
+            bg = __shfl_sync(kFull, bg, src);
+            double bw = fmax(__longlong_as_double((long long)warp_max_u64(wb)), s_wit0[s]);
             // the winner's column (multipliers of rows > s, T entries of rows < s) and the
             // last active column: fetched right here by warp 0, two rows per lane
+            if (s > 0) KP_MARK(s, 9);
             if (fabs(bv) > kSingularRtol * bw) {
+                // all four records in flight at once (one round trip); first a plain L2 read
+                // (usually already there), strong re-polls only for what had not arrived
+                double2 cm[2], cl[2];
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    cm[h] = GET1(COL(s, bg, lane + 32 * h));
+                    cl[h] = GET1(LAST(s, lane + 32 * h));
+                }
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                     const int r = lane + 32 * h;
-                    const double2* pm = COL(s, bg, r);
-                    const double2* pl = LAST(s, r);
-                    double2 cm = GET(pm), cl = GET(pl);
-                    while (!rec_ok(cm, tag, &p.err->pad) || !rec_ok(cl, tag, &p.err->pad)) {
+                    while (!rec_ok(cm[h], tag, &p.err->pad) || !rec_ok(cl[h], tag, &p.err->pad)) {
                         if (globaltimer() - t_start > p.timeout_ns) {
 #ifdef KP_DEBUG
                             printf("KP timeout col: g=%d s=%d row0=%d m=%d G=%d r=%d bg=%d bi=%d coltag %x lasttag %x want %x\n",
-                                   g, s, p.row0, m, G, r, bg, bi, tag_of(cm), tag_of(cl), tag);
+                                   g, s, p.row0, m, G, r, bg, bi, tag_of(cm[h]), tag_of(cl[h]), tag);
 #endif
                             if (atomicCAS(&p.err->dbg[0], 0u, 2u) == 0u) {
                                 p.err->dbg[1] = (unsigned)g; p.err->dbg[2] = (unsigned)s; p.err->dbg[3] = (unsigned)bg;
-                                p.err->dbg[4] = tag_of(cm); p.err->dbg[5] = tag_of(cl); p.err->dbg[6] = tag;
+                                p.err->dbg[4] = tag_of(cm[h]); p.err->dbg[5] = tag_of(cl[h]); p.err->dbg[6] = tag;
                                 p.err->dbg[7] = (unsigned)r;
                             }
                             atomicExch(&p.err->error, 1u);
@@ -323,13 +370,14 @@ __global__ void __launch_bounds__(kThreads, 1) kp_panel_kernel(const KPParams p)
                             s_stop = 1;
                             break;
                         }
-                        cm = GET(pm);
-                        cl = GET(pl);
+                        cm[h] = GET(COL(s, bg, r));
+                        cl[h] = GET(LAST(s, r));
                     }
-                    s_mult[r] = cm.x;
-                    s_last[r] = cl.x;
+                    s_mult[r] = cm[h].x;
+                    s_last[r] = cl[h].x;
                 }
             }
+            if (s > 0) KP_MARK(s, 10);
             if (lane == 0) {
                 s_win_v = bv;
                 s_win_l = bi;
@@ -353,12 +401,15 @@ __global__ void __launch_bounds__(kThreads, 1) kp_panel_kernel(const KPParams p)
         }
         const int wn = max(0, min(wc, ms - 1 - lo));  // my active columns after the step
         KP_MARK(s, 7);
-        // ---- B+D1. warps 0-3: row s scaled by true division (condense.py:110) with the
+        // ---- B+D1. warps 0-7: row s scaled by true division (condense.py:110) with the
         //      column exchange (condense.py:104-107) folded in, and -- lookahead -- row s+1
         //      updated from it, its running max and the next candidate, published at once.
-        //      Warps 4-5 meanwhile: the exchange on the other rows, the T column, the record.
+        //      The next 2 warps meanwhile: the exchange on the other rows, the T^{-1} column, the record.
         constexpr int kLA = 64;   // publishing threads (D2)
-        constexpr int kD1 = 128;  // row s / s+1 threads
+#ifndef KP_D1
+#define KP_D1 256
+#endif
+        constexpr int kD1 = KP_D1;  // row s / s+1 threads (<= 256)
         const int lx = (l >= lo && l - lo < wn) ? l - lo : -1;  // exchange target, local
         const bool last_step = (s + 1 == kB);
         const unsigned tag1 = tag + 1u;
@@ -554,11 +605,22 @@ __global__ void __launch_bounds__(kThreads, 1) kp_panel_kernel(const KPParams p)
     }
     }
     KP_MARK(0, 11);
+    if (g == 0 && tid == 0) g_kp_span[span_slot][1] = globaltimer();
 finish:
     if constexpr (kCl) cluster_sync_all();  // no CTA leaves while peers may still push into it
 }
 
 }  // namespace
+
+int kp_debug_spans(unsigned long long* out, int max_spans) {
+    unsigned n = 0;
+    if (cudaMemcpyFromSymbol(&n, g_kp_span_n, sizeof(n)) != cudaSuccess) return -1;
+    const int k = (int)std::min<unsigned>(std::min<unsigned>(n, 4096u), (unsigned)max_spans);
+    if (k > 0 && cudaMemcpyFromSymbol(out, g_kp_span, (size_t)k * 2 * sizeof(unsigned long long)) != cudaSuccess) return -1;
+    const unsigned zero = 0;
+    cudaMemcpyToSymbol(g_kp_span_n, &zero, sizeof(zero));
+    return k;
+}
 
 size_t kp_smem_bytes(int cw, bool cluster) {
     return (size_t)kB * cw * sizeof(double) + (cluster ? kRcSlots * sizeof(double2) : 0);

@@ -820,9 +820,13 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
         *cw_out = cw;
         return G;
     };
+    // ~192 columns per panel CTA: the pivot latency is flat up to ~200 columns
+    // (`scripts/micro/kp_bench.cu`), and fewer panel CTAs leave more SMs to the
+    // overlapped trailing GEMM
+    const int64_t kp_cols = std::max<int64_t>(64, env_long("MCND_KP_COLS", 192));
     auto kp_grid = [&](int64_t m) {
         int64_t cw = 0;
-        return split(m, std::min<int64_t>({(int64_t)B->sms, (int64_t)kKPMaxG, std::max<int64_t>(1, m / 128)}), &cw);
+        return split(m, std::min<int64_t>({(int64_t)B->sms, (int64_t)kKPMaxG, std::max<int64_t>(1, m / kp_cols)}), &cw);
     };
     auto run_kp = [&](int64_t kb, K2Gather* gp, double* Wout) -> cudaError_t {
         const int64_t m = n - kb;
@@ -833,7 +837,7 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
             kp.cluster = (G >= 2 && kp_smem_bytes((int)cw, true) <= 200 * 1024 && B->kp_cluster_ok(G, cw)) ? 1 : 0;
         }
         if (!kp.cluster) {
-            G = split(m, std::min<int64_t>({(int64_t)B->sms, (int64_t)kKPMaxG, std::max<int64_t>(1, m / 128)}), &cw);
+            G = split(m, std::min<int64_t>({(int64_t)B->sms, (int64_t)kKPMaxG, std::max<int64_t>(1, m / kp_cols)}), &cw);
             if (kp_smem_bytes((int)cw, false) > 190 * 1024) return cudaErrorInvalidValue;
         }
         kp.row0 = (int32_t)kb;
@@ -870,22 +874,37 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
     int64_t k = 0;
     int par = 0;
     int64_t n_launch = 1;  // kernels launched by this call (K1 init so far)
+    // debug timeline (MCND_DEBUG_TIMELINE=1): an event after every critical-stream step,
+    // per-label device time printed to stderr at the end of the call
+    const bool dbg_tl = env_long("MCND_DEBUG_TIMELINE", 0) != 0;
+    std::vector<std::pair<const char*, cudaEvent_t>> tl;
+    auto mark = [&](const char* label) {
+        if (!dbg_tl) return;
+        cudaEvent_t ev;
+        cudaEventCreate(&ev);
+        cudaEventRecord(ev, st);
+        tl.emplace_back(label, ev);
+    };
+    mark("init");
     while (k < n_panels) {
         const int64_t kb = k * b, m = n - kb;
         double* const Wq = Wb + (size_t)par * 2 * b * ld;
         double* const Lq = Lb + (size_t)par * std::max<int64_t>(n, 1) * 2 * b;
         if (pairs && k + 1 < n_panels) {
             e = run_kp(kb, gp0, Wq);
+            mark("kp1");
             if (e == cudaSuccess) e = k2_gather_fix(ws, ld, (int32_t)(kb + b), (int32_t)b, 64, gp0, Lq, abort, st);
+            mark("r1_gather");
             if (e == cudaSuccess)
                 e = k2_gemm(ws, ld, (int32_t)(kb + b), (int32_t)b, (int32_t)(m - b), 64, Lq, 64, Wq, ld, wit, abort, st);
+            mark("r1_gemm");
             if (e == cudaSuccess) e = run_kp(kb + b, gp1, Wq + b * ld);
+            mark("kp2");
             if (e == cudaSuccess) e = k2_pair_prep(gp0, gp1, (int32_t)m, Wq, ld, Wp, gpair, abort, st);
+            mark("pair_prep");
             if (e == cudaSuccess) e = join_side();  // trailing rows final for the previous pair
+            mark("join");
             const int32_t nr = (int32_t)(n - kb - 2 * b);
-            if (e == cudaSuccess) e = k2_gather_fix(ws, ld, (int32_t)(kb + 2 * b), nr, 128, gpair, Lq, abort, st);
-            if (e == cudaSuccess)  // NL[:, 64:128] += NL[:, 0:64] * (-Wp)   (NL = -L; no witness: scratch)
-                e = k2_gemm(Lq + b, 2 * b, 0, nr, (int32_t)b, 64, Lq, 2 * b, Wp, b, nullptr, abort, st);
             // rows the next unit factors: a pair (128), a last single panel (64), or the tail (all)
             const int64_t k2 = k + 2;
             int64_t ahead = (k2 + 1 < n_panels) ? 2 * b : (k2 < n_panels ? b : nr);
@@ -901,20 +920,30 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
             } else {
                 ahead = nr;
             }
-            if (e == cudaSuccess && ahead < nr) {  // side stream: from here on L and W of this pair are final
-                e = cudaEventRecord(B->ev_a, st);
-                if (e == cudaSuccess) e = cudaStreamWaitEvent(side, B->ev_a, 0);
-            }
-            if (e == cudaSuccess)
-                e = k2_gemm(ws, ld, (int32_t)(kb + 2 * b), (int32_t)ahead, (int32_t)(m - 2 * b), 128, Lq, 2 * b, Wq, ld,
-                            wit, abort, st);
+            // gather + L correction + trailing update of `rows` rows starting at row offset r0
+            // (relative to the pair's trailing block) on stream `ss`
+            auto trailing = [&](int64_t r0, int64_t rows, cudaStream_t ss, int sm_budget) -> cudaError_t {
+                double* const Lr = Lq + r0 * 2 * b;
+                cudaError_t ee = k2_gather_fix(ws, ld, (int32_t)(kb + 2 * b + r0), (int32_t)rows, 128, gpair, Lr, abort, ss);
+                if (ss == st) mark("gather");
+                if (ee == cudaSuccess)  // NL[:, 64:128] += NL[:, 0:64] * (-Wp)   (NL = -L; no witness: scratch)
+                    ee = k2_gemm(Lr + b, 2 * b, 0, (int32_t)rows, (int32_t)b, 64, Lr, 2 * b, Wp, b, nullptr, abort, ss);
+                if (ss == st) mark("lcorr");
+                if (ee == cudaSuccess)
+                    ee = k2_gemm(ws, ld, (int32_t)(kb + 2 * b + r0), (int32_t)rows, (int32_t)(m - 2 * b), 128, Lr, 2 * b,
+                                 Wq, ld, wit, abort, ss, sm_budget);
+                if (ss == st) mark("trailing");
+                return ee;
+            };
+            // side stream: W, Wp and the gather descriptor are final once pair prep is done
+            if (e == cudaSuccess && ahead < nr) e = cudaEventRecord(B->ev_a, st);
+            if (e == cudaSuccess) e = trailing(0, ahead, st, 0);  // the critical rows first
             if (e == cudaSuccess && ahead < nr) {
-                if (e == cudaSuccess)
-                    e = k2_gemm(ws, ld, (int32_t)(kb + 2 * b + ahead), (int32_t)(nr - ahead), (int32_t)(m - 2 * b), 128,
-                                Lq + ahead * 2 * b, 2 * b, Wq, ld, wit, abort, side, (int)budget);
+                e = cudaStreamWaitEvent(side, B->ev_a, 0);
+                if (e == cudaSuccess) e = trailing(ahead, nr - ahead, side, (int)budget);
                 if (e == cudaSuccess) e = cudaEventRecord(B->ev_b, side);
                 side_pending = (e == cudaSuccess);
-                ++n_launch;
+                n_launch += 3;
             }
             n_launch += 8;  // 2 panels, gather, update of panel k+1, pair prep, gather, L correction, trailing
             k += 2;
@@ -938,6 +967,7 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
     }
     e = join_side();
     if (e != cudaSuccess) return fail(MCND_ECUDA, "K2 stream join: %s", cudaGetErrorString(e));
+    mark("final_join");
     // 3. unblocked tail (publishes the final 1x1)
     p.in_place = 1; p.wit_in = wit; p.row_pstep = d_iota;
     p.ncol0 = (int32_t)mt; p.n_steps = (int32_t)(mt - 1); p.seq = d_iota + kb_end; p.pstep_offset = (int32_t)kb_end;
@@ -946,6 +976,22 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
     if (e != cudaSuccess) return fail(MCND_ECUDA, "K2 tail launch: %s", cudaGetErrorString(e));
     CUDA_TRY(cudaEventRecord(B->ev1, st));
     out->launches = n_launch + 1;
+    if (dbg_tl) {
+        mark("tail");
+        cudaStreamSynchronize(st);
+        std::map<std::string, std::pair<double, int>> acc;
+        for (size_t i = 1; i < tl.size(); ++i) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, tl[i - 1].second, tl[i].second);
+            auto& a = acc[tl[i].first];
+            a.first += ms;
+            a.second += 1;
+        }
+        for (auto& kv : acc)
+            std::fprintf(stderr, "mcnd timeline %-10s %8.3f ms  (%d x %.1f us)\n", kv.first.c_str(), kv.second.first,
+                         kv.second.second, 1e3 * kv.second.first / kv.second.second);
+        for (auto& t : tl) cudaEventDestroy(t.second);
+    }
 
     PivRec* h_rec = (PivRec*)B->hpin;
     K1Err* h_err = (K1Err*)((char*)B->hpin + align_up((size_t)n * sizeof(PivRec), 64));
@@ -1062,6 +1108,9 @@ int mcnd_mc_parallel(const double* h_a, int64_t n, int64_t lda, int32_t p, uint3
     return parallel_dev(d_a, n, n, p, flags, (cudaStream_t)stream, out, stats, payload_entries, row_updates,
                         owners_out);
 }
+
+/* debug (not part of the ABI header): panel-launch spans of the calls since the last read */
+int mcnd_debug_kp_spans(unsigned long long* out, int max_spans) { return mcnd::kp_debug_spans(out, max_spans); }
 
 int mcnd_logdet_blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, void* stream,
                             mcnd_logdet* out, double* pivots_out, int32_t* cols_out) {

@@ -117,6 +117,8 @@ cudaError_t kp_launch(const KPParams& p, cudaStream_t s);
 size_t kp_smem_bytes(int cw, bool cluster);
 // clusters of G CTAs (chunk width cw) that can be co-resident; 0 if the shape cannot launch
 int kp_cluster_fits(int G, int cw);
+// debug: (entry, exit) globaltimer of the panel launches since the last call; returns the count
+int kp_debug_spans(unsigned long long* out, int max_spans);
 
 // All launches are asynchronous on `s`; `abort` (device) short-circuits every
 // kernel once a panel pivot failed the witness test.

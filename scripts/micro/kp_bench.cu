@@ -73,6 +73,12 @@ int main(int argc, char** argv) {
     printf("per step (cycles):");
     for (int k = 0; k < 7; ++k) printf(" %s %.0f", k == 6 ? "total" : nm[k], acc[k] / 61);
     printf("\n");
+    {
+        double p8 = 0, p9 = 0, p10 = 0, p1 = 0;
+        for (int s = 1; s < 62; ++s) { p8 += (double)(tr[s][8] - tr[s][0]); p9 += (double)(tr[s][9] - tr[s][8]);
+            p10 += (double)(tr[s][10] - tr[s][9]); p1 += (double)(tr[s][1] - tr[s][10]); }
+        printf("  A detail: poll %.0f  reduce %.0f  fetch %.0f  sync %.0f\n", p8 / 61, p9 / 61, p10 / 61, p1 / 61);
+    }
     printf("  prologue %llu cycles, loop %llu, W %llu\n", tr[0][9] - tr[0][8], tr[0][10] - tr[0][9], tr[0][11] - tr[0][10]);
 #endif
     return 0;

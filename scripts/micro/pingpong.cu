@@ -7,7 +7,7 @@ __device__ __forceinline__ void st16(double2* p, double2 v) {
 }
 __device__ __forceinline__ double2 ld16(const double2* p) {
     double2 v;
-    asm volatile("ld.relaxed.gpu.global.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p) : "memory");
+    asm volatile("ld.global.cg.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p) : "memory");
     return v;
 }
 __global__ void pp_global(double2* buf, int iters, long long* out, int far) {
