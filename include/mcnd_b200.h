@@ -129,6 +129,34 @@ int mcnd_dist_mc_parallel(void* handle, const double* d_rows, int64_t n, int64_t
                           double* rem_row, double* rem_wit, double* device_ms);
 void mcnd_dist_destroy(void* handle);
 
+/* ---- multi-GPU BLOCKED condensation, one process per GPU: the per-rank engine.
+ * Replaces mc_parallel's block-row worker loop (runtime.py:153-204) for the blocked
+ * variant ("K2: one broadcast per panel of W").  Rank r holds a
+ * contiguous block of rows (plan_blocks, runtime.py:33-44) x all n columns.  The host
+ * schedule (paper_1811_08057_b200/dist.py BlockedGroup) gives each panel pair to the
+ * rank with the most live rows (its topmost 128 live rows, north_star (3)); that rank
+ * runs mcnd_mg_pair, the host broadcasts W / Wp / the gather descriptor (NCCL), and
+ * every rank runs mcnd_mg_trailing on its own live rows.  The last rows are exported
+ * (mcnd_mg_export), gathered to one rank and finished by mcnd_mg_tail (K1).
+ * Records are 16 bytes {double v; int32 l; uint32 flag}; flag == the epoch returned
+ * in err[3] by mcnd_mg_records.  All device pointers; asynchronous unless stated. */
+int mcnd_mg_create(int64_t n, int64_t local_rows, void** handle);
+int mcnd_mg_load(void* handle, const double* d_rows, int64_t lds, void* stream);
+int mcnd_mg_pair(void* handle, int64_t lr0, int64_t t, int64_t m, double* d_W, int64_t ldw, double* d_Wp,
+                 void* d_gather, void* stream);
+int mcnd_mg_trailing(void* handle, int64_t lr0, int64_t rows, int64_t m, const double* d_W, int64_t ldw,
+                     const double* d_Wp, const void* d_gather, int32_t sm_budget, int32_t par, void* stream);
+int mcnd_mg_export(void* handle, int64_t lr0, int64_t rows, int64_t mt, double* d_out, int64_t ldo, double* d_wit,
+                   void* stream);
+/* synchronous: h_recs receives mt records, h_err {error, step, nonfinite} */
+int mcnd_mg_tail(void* handle, double* d_rows, int64_t ldr, const double* d_wit, int64_t mt, void* stream,
+                 void* h_recs, uint32_t* h_err);
+/* synchronous: n records (global step index) + {error, step, nonfinite, epoch} */
+int mcnd_mg_records(void* handle, void* h_recs, uint32_t* h_err, void* stream);
+int64_t mcnd_mg_gather_bytes(void);   /* size of the gather descriptor to broadcast */
+int64_t mcnd_mg_ld(void* handle);      /* workspace row stride (W buffers use it)    */
+int mcnd_mg_destroy(void* handle);
+
 /* ---- batched: two warps per small matrix (no reference counterpart; oracle = a loop
  * of logdet_condensation).  d_sign/d_log_abs: DEVICE outputs (batch entries);
  * d_pivots: optional DEVICE batch x n pivot values (for bitwise checks); d_nonfinite:

@@ -49,6 +49,8 @@ EXPORTS = (
     "mcnd_dist_destroy",
     "mcnd_last_error", "mcnd_version", "mcnd_k1_grid", "mcnd_release_workspace",
     "mcnd_logdet_blocked_dev", "mcnd_logdet_blocked", "mcnd_blocked_panel",
+    "mcnd_mg_create", "mcnd_mg_load", "mcnd_mg_pair", "mcnd_mg_trailing", "mcnd_mg_export", "mcnd_mg_tail",
+    "mcnd_mg_records", "mcnd_mg_gather_bytes", "mcnd_mg_ld", "mcnd_mg_destroy",
 )
 
 
@@ -96,6 +98,25 @@ def load(path: str | None = None):
             f.argtypes = [P, i64, i64, u32, P, LD, P, P]
             f.restype = ctypes.c_int
         lib.mcnd_blocked_panel.restype = ctypes.c_int32
+        VP = ctypes.POINTER(ctypes.c_void_p)
+        sigs = {
+            "mcnd_mg_create": [i64, i64, VP],
+            "mcnd_mg_load": [P, P, i64, P],
+            "mcnd_mg_pair": [P, i64, i64, i64, P, i64, P, P, P],
+            "mcnd_mg_trailing": [P, i64, i64, i64, P, i64, P, P, i32, i32, P],
+            "mcnd_mg_export": [P, i64, i64, i64, P, i64, P, P],
+            "mcnd_mg_tail": [P, P, i64, P, i64, P, P, P],
+            "mcnd_mg_records": [P, P, P, P],
+            "mcnd_mg_destroy": [P],
+        }
+        for name, args in sigs.items():
+            f = getattr(lib, name)
+            f.argtypes = args
+            f.restype = ctypes.c_int
+        lib.mcnd_mg_gather_bytes.argtypes = []
+        lib.mcnd_mg_gather_bytes.restype = ctypes.c_int64
+        lib.mcnd_mg_ld.argtypes = [P]
+        lib.mcnd_mg_ld.restype = ctypes.c_int64
         lib.mcnd_last_error.argtypes = []
         lib.mcnd_last_error.restype = ctypes.c_char_p
         lib.mcnd_version.restype = ctypes.c_int32

@@ -823,10 +823,13 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
     // ~192 columns per panel CTA: the pivot latency is flat up to ~200 columns
     // (`scripts/micro/kp_bench.cu`), and fewer panel CTAs leave more SMs to the
     // overlapped trailing GEMM
-    const int64_t kp_cols = std::max<int64_t>(64, env_long("MCND_KP_COLS", 192));
+    const int64_t kp_cols = std::min<int64_t>(256, std::max<int64_t>(64, env_long("MCND_KP_COLS", 192)));
+    auto kp_ctas = [&](int64_t m) {  // <= 256 columns per CTA (one lookahead pass, one bulk segment)
+        return std::min<int64_t>({(int64_t)B->sms, (int64_t)kKPMaxG, std::max<int64_t>((m + 255) / 256, m / kp_cols)});
+    };
     auto kp_grid = [&](int64_t m) {
         int64_t cw = 0;
-        return split(m, std::min<int64_t>({(int64_t)B->sms, (int64_t)kKPMaxG, std::max<int64_t>(1, m / kp_cols)}), &cw);
+        return split(m, kp_ctas(m), &cw);
     };
     auto run_kp = [&](int64_t kb, K2Gather* gp, double* Wout) -> cudaError_t {
         const int64_t m = n - kb;
@@ -837,7 +840,7 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
             kp.cluster = (G >= 2 && kp_smem_bytes((int)cw, true) <= 200 * 1024 && B->kp_cluster_ok(G, cw)) ? 1 : 0;
         }
         if (!kp.cluster) {
-            G = split(m, std::min<int64_t>({(int64_t)B->sms, (int64_t)kKPMaxG, std::max<int64_t>(1, m / kp_cols)}), &cw);
+            G = split(m, kp_ctas(m), &cw);
             if (kp_smem_bytes((int)cw, false) > 190 * 1024) return cudaErrorInvalidValue;
         }
         kp.row0 = (int32_t)kb;
@@ -1047,6 +1050,310 @@ struct DistHandle {
     bool connected = false;
     uint32_t epoch = 0;
 };
+
+// ---- multi-GPU blocked condensation: the per-rank engine (SURVEY.md §8(e) "K2:
+// one broadcast per panel of W").  One rank holds a contiguous block of rows x all
+// n columns.  The host schedule (dist.py) gives each panel pair to the rank with
+// the most live rows (its topmost 128 live rows; north_star (3)); that rank
+// factors the pair (mg_pair), the pair's W, Wp and gather descriptor are broadcast
+// (NCCL, by the host), and every rank applies the rank-128 update to its own live
+// rows (mg_trailing).  The last rows are gathered to one rank and finished by K1
+// (mg_tail).  Kernels are exactly the single-GPU K2 kernels.
+struct MgHandle {
+    int device = 0, sms = 0;
+    int64_t n = 0, lr = 0, ld = 0;
+    void* mem = nullptr;
+    size_t bytes = 0;
+    double* ws = nullptr;
+    double* wit = nullptr;
+    PivRec* recs = nullptr;
+    double* L = nullptr;       // [2][lr][128]
+    K2Gather* gp = nullptr;    // [2]
+    double2 *cand = nullptr, *wrec = nullptr, *colb = nullptr, *lastb = nullptr;
+    K1Err* err = nullptr;
+    unsigned* abort = nullptr;
+    int32_t* d_int = nullptr;  // iota[max(n,lr)] | never[lr] | init deal ptr[G0+1] rows[lr]
+    int64_t g0 = 1;
+    void* tail_mem = nullptr;  // tail metadata (iota, deal) + records
+    size_t tail_bytes = 0;
+    void* hpin = nullptr;
+    size_t hpin_bytes = 0;
+    uint32_t epoch = 0;
+};
+
+int mg_create(int64_t n, int64_t lr, MgHandle** out) {
+    if (n < 1 || lr < 0 || lr > n) return fail(MCND_EINVAL, "mg_create: bad sizes n=%lld rows=%lld", (long long)n, (long long)lr);
+    auto* h = new MgHandle();
+    cudaGetDevice(&h->device);
+    cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, h->device);
+    h->n = n;
+    h->lr = lr;
+    h->ld = (int64_t)align_up((size_t)n, 16);
+    const int64_t b = kK2B, lrr = std::max<int64_t>(lr, 1);
+    h->g0 = std::max<int64_t>(1, std::min<int64_t>(h->sms, lrr));
+    if ((lrr + h->g0 - 1) / h->g0 > kK1MaxRowsPerCta) { delete h; return fail(MCND_EINVAL, "mg_create: %lld rows too many", (long long)lr); }
+    size_t off = 0;
+    auto take = [&](size_t by) { size_t o = off; off = align_up(off + by, 256); return o; };
+    const size_t o_ws = take((size_t)lrr * h->ld * sizeof(double));
+    const size_t o_wit = take((size_t)lrr * sizeof(double));
+    const size_t o_rec = take((size_t)n * sizeof(PivRec));
+    const size_t o_L = take((size_t)2 * lrr * 2 * b * sizeof(double));
+    const size_t o_gp = take(2 * sizeof(K2Gather));
+    const size_t o_cand = take((size_t)64 * kKPMaxG * sizeof(double2));
+    const size_t o_wrec = take((size_t)64 * kKPMaxG * sizeof(double2));
+    const size_t o_colb = take((size_t)64 * kKPMaxG * 64 * sizeof(double2));
+    const size_t o_lastb = take((size_t)64 * 64 * sizeof(double2));
+    const size_t o_ctl = take(sizeof(K1Err) + 16);
+    const int64_t ni = std::max<int64_t>(n, lrr);
+    const size_t n_int = (size_t)(ni + lrr + (h->g0 + 1) + lrr);
+    const size_t o_int = take(n_int * sizeof(int32_t));
+    if (cudaMalloc(&h->mem, off) != cudaSuccess) {
+        cudaGetLastError();
+        delete h;
+        return fail(MCND_ECUDA, "mg_create: cudaMalloc(%zu) failed", off);
+    }
+    h->bytes = off;
+    char* base = (char*)h->mem;
+    h->ws = (double*)(base + o_ws);
+    h->wit = (double*)(base + o_wit);
+    h->recs = (PivRec*)(base + o_rec);
+    h->L = (double*)(base + o_L);
+    h->gp = (K2Gather*)(base + o_gp);
+    h->cand = (double2*)(base + o_cand);
+    h->wrec = (double2*)(base + o_wrec);
+    h->colb = (double2*)(base + o_colb);
+    h->lastb = (double2*)(base + o_lastb);
+    h->err = (K1Err*)(base + o_ctl);
+    h->abort = (unsigned*)(base + o_ctl + sizeof(K1Err));
+    h->d_int = (int32_t*)(base + o_int);
+    std::vector<int32_t> hi(n_int);
+    int32_t* iota = hi.data();
+    int32_t* never = iota + ni;
+    int32_t* iptr = never + lrr;
+    int32_t* irows = iptr + (h->g0 + 1);
+    for (int64_t i = 0; i < ni; ++i) iota[i] = (int32_t)i;
+    for (int64_t i = 0; i < lrr; ++i) never[i] = kNever;
+    iptr[0] = 0;
+    for (int64_t c = 0; c < h->g0; ++c) iptr[c + 1] = iptr[c] + (int32_t)((lr - c + h->g0 - 1) / h->g0);
+    std::vector<int32_t> fill(iptr, iptr + h->g0);
+    for (int64_t i = 0; i < lr; ++i) irows[fill[(size_t)(i % h->g0)]++] = (int32_t)i;
+    if (cudaMemcpy(h->d_int, hi.data(), n_int * sizeof(int32_t), cudaMemcpyHostToDevice) != cudaSuccess) {
+        cudaFree(h->mem);
+        delete h;
+        return fail(MCND_ECUDA, "mg_create: metadata upload failed");
+    }
+    *out = h;
+    return MCND_OK;
+}
+
+// copy + initial witness + finiteness of the local rows (K1 with no steps)
+int mg_load(MgHandle* h, const double* src, int64_t lds, cudaStream_t st) {
+    if (!src && h->lr > 0) return fail(MCND_EINVAL, "mg_load: null rows");
+    if (lds < h->n) return fail(MCND_EINVAL, "mg_load: row stride %lld < n", (long long)lds);
+    h->epoch = h->epoch + 1 + (h->epoch + 1 == 0 ? 1 : 0);
+    CUDA_TRY(cudaMemsetAsync(h->recs, 0, (size_t)h->n * sizeof(PivRec), st));
+    CUDA_TRY(cudaMemsetAsync(h->err, 0, sizeof(K1Err) + 16, st));
+    if (h->lr == 0) return MCND_OK;
+    const int64_t ni = std::max<int64_t>(h->n, h->lr);
+    K1Params p{};
+    p.src[0] = src;
+    p.src_row0[0] = 0;
+    p.lds = lds;
+    p.ws[0] = h->ws;
+    p.row_wit[0] = h->wit;
+    p.ld = h->ld;
+    p.n = (int32_t)h->lr;
+    p.n_groups = 1;
+    p.n_local_groups = 1;
+    p.epoch = h->epoch;
+    p.err = h->err;
+    p.chunk = (int32_t)std::min<int64_t>((int64_t)align_up((size_t)h->n, 2), kK1MaxChunk);
+    p.timeout_ns = 20ull * 1000000000ull;
+    p.abort_flag = h->abort;
+    p.ncol0 = (int32_t)h->n;
+    p.n_steps = 0;
+    p.seq = h->d_int;
+    p.row_pstep = h->d_int + ni;
+    p.cta_row_ptr = h->d_int + ni + h->lr;
+    p.cta_rows = p.cta_row_ptr + (h->g0 + 1);
+    p.ctas_per_group = (int32_t)h->g0;
+    p.rec[0] = h->recs;
+    cudaError_t e = k1_launch(p, false, st);
+    if (e != cudaSuccess) return fail(MCND_ECUDA, "mg_load: %s", cudaGetErrorString(e));
+    return MCND_OK;
+}
+
+KPParams mg_kp(MgHandle* h, int64_t lr0, int64_t t, int64_t m, K2Gather* gp, double* W, int64_t ldw) {
+    const int64_t b = kK2B;
+    const int64_t cols = std::min<int64_t>(256, std::max<int64_t>(64, env_long("MCND_KP_COLS", 192)));
+    int64_t G = std::min<int64_t>({(int64_t)h->sms, (int64_t)kKPMaxG, std::max<int64_t>((m + 255) / 256, m / cols)});
+    int64_t cw = 0;
+    for (;; --G) {
+        cw = (int64_t)align_up((size_t)((m + G - 1) / G), 2);
+        if (G == 1 || m - (G - 1) * cw >= b) break;
+    }
+    KPParams kp{};
+    kp.ws = h->ws;
+    kp.ld = h->ld;
+    kp.row0 = (int32_t)lr0;
+    kp.m = (int32_t)m;
+    kp.G = (int32_t)G;
+    kp.cw = (int32_t)cw;
+    kp.wit = h->wit;
+    kp.rec = h->recs + t;
+    kp.epoch = h->epoch;
+    kp.tag0 = (h->epoch << 16) ^ (uint32_t)(t + 1);
+    kp.W = W;
+    kp.ldw = ldw;
+    kp.pan = gp;
+    kp.abort = h->abort;
+    kp.cand = h->cand;
+    kp.wrec = h->wrec;
+    kp.colbuf = h->colb;
+    kp.lastbuf = h->lastb;
+    kp.err = h->err;
+    kp.timeout_ns = 20ull * 1000000000ull;
+    kp.cluster = 0;
+    return kp;
+}
+
+// owner of a panel pair: local rows lr0..lr0+127 are the pair, m the active width,
+// t the global index of its first pivot.  Outputs W (128 x (m-128) in the final
+// layout; row stride ldw >= m-64, even: W_k is m-64 wide before the pair prep), Wp
+// (64 x 64) and the pair's gather descriptor; pivot records to recs[t .. t+127].
+int mg_pair(MgHandle* h, int64_t lr0, int64_t t, int64_t m, double* W, int64_t ldw, double* Wp, K2Gather* gpair,
+            cudaStream_t st) {
+    const int64_t b = kK2B;
+    if (lr0 < 0 || lr0 + 2 * b > h->lr || m < 2 * b + 1 || m > h->n || t < 0 || t + 2 * b > h->n || ldw < m - b ||
+        (ldw & 1) || !W ||
+        !Wp || !gpair)
+        return fail(MCND_EINVAL, "mg_pair: bad arguments (lr0=%lld m=%lld t=%lld)", (long long)lr0, (long long)m,
+                    (long long)t);
+    K2Gather* gp0 = h->gp;
+    K2Gather* gp1 = h->gp + 1;
+    double* L = h->L;
+    KPParams kp = mg_kp(h, lr0, t, m, gp0, W, ldw);
+    cudaError_t e = kp_launch(kp, st);
+    if (e == cudaSuccess) e = k2_gather_fix(h->ws, h->ld, (int32_t)(lr0 + b), (int32_t)b, 64, gp0, L, h->abort, st);
+    if (e == cudaSuccess)
+        e = k2_gemm(h->ws, h->ld, (int32_t)(lr0 + b), (int32_t)b, (int32_t)(m - b), 64, L, 64, W, ldw, h->wit, h->abort, st);
+    if (e == cudaSuccess) {
+        KPParams kp1 = mg_kp(h, lr0 + b, t + b, m - b, gp1, W + b * ldw, ldw);
+        e = kp_launch(kp1, st);
+    }
+    if (e == cudaSuccess) e = k2_pair_prep(gp0, gp1, (int32_t)m, W, ldw, Wp, gpair, h->abort, st);
+    if (e != cudaSuccess) return fail(MCND_ECUDA, "mg_pair: %s", cudaGetErrorString(e));
+    return MCND_OK;
+}
+
+// every rank: gather + L correction + rank-128 update of local rows [lr0, lr0+rows)
+// by a pair of active width m (W, Wp, gpair as produced by mg_pair, possibly on
+// another rank); par selects the L buffer (alternate it per pair).
+int mg_trailing(MgHandle* h, int64_t lr0, int64_t rows, int64_t m, const double* W, int64_t ldw, const double* Wp,
+                const K2Gather* gpair, int32_t sm_budget, int32_t par, cudaStream_t st) {
+    const int64_t b = kK2B;
+    if (rows == 0) return MCND_OK;
+    if (lr0 < 0 || rows < 0 || lr0 + rows > h->lr || m < 2 * b + 1 || m > h->n || !W || !Wp || !gpair || ldw < m - b ||
+        (ldw & 1))
+        return fail(MCND_EINVAL, "mg_trailing: bad arguments");
+    double* L = h->L + (size_t)(par & 1) * std::max<int64_t>(h->lr, 1) * 2 * b;
+    cudaError_t e = k2_gather_fix(h->ws, h->ld, (int32_t)lr0, (int32_t)rows, 128, gpair, L, h->abort, st);
+    if (e == cudaSuccess)
+        e = k2_gemm(L + b, 2 * b, 0, (int32_t)rows, (int32_t)b, 64, L, 2 * b, Wp, b, nullptr, h->abort, st);
+    if (e == cudaSuccess)
+        e = k2_gemm(h->ws, h->ld, (int32_t)lr0, (int32_t)rows, (int32_t)(m - 2 * b), 128, L, 2 * b, W, ldw, h->wit,
+                    h->abort, st, sm_budget);
+    if (e != cudaSuccess) return fail(MCND_ECUDA, "mg_trailing: %s", cudaGetErrorString(e));
+    return MCND_OK;
+}
+
+// local rows [lr0, lr0+rows): their first mt columns (row stride ldo) and witnesses
+int mg_export(MgHandle* h, int64_t lr0, int64_t rows, int64_t mt, double* out, int64_t ldo, double* wit_out,
+              cudaStream_t st) {
+    if (rows == 0) return MCND_OK;
+    if (lr0 < 0 || lr0 + rows > h->lr || mt < 1 || mt > h->n || ldo < mt || !out || !wit_out)
+        return fail(MCND_EINVAL, "mg_export: bad arguments");
+    CUDA_TRY(cudaMemcpy2DAsync(out, (size_t)ldo * sizeof(double), h->ws + lr0 * h->ld, (size_t)h->ld * sizeof(double),
+                               (size_t)mt * sizeof(double), (size_t)rows, cudaMemcpyDeviceToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(wit_out, h->wit + lr0, (size_t)rows * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    return MCND_OK;
+}
+
+// the gathered last mt rows (row stride ldr, in place) with their carried witnesses:
+// K1 condenses them top to bottom; records (mt x 16 B) and the error word to the host
+int mg_tail(MgHandle* h, double* rows, int64_t ldr, const double* wit, int64_t mt, cudaStream_t st, void* h_recs,
+            uint32_t* h_err) {
+    if (mt < 1 || ldr < mt || (ldr & 1) || !rows || !wit || !h_recs) return fail(MCND_EINVAL, "mg_tail: bad arguments");
+    const int64_t Gt = std::max<int64_t>(1, std::min<int64_t>(h->sms, mt));
+    if ((mt + Gt - 1) / Gt > kK1MaxRowsPerCta) return fail(MCND_EINVAL, "mg_tail: %lld rows too many", (long long)mt);
+    size_t off = 0;
+    auto take = [&](size_t by) { size_t o = off; off = align_up(off + by, 256); return o; };
+    const size_t o_int = take((size_t)(mt + Gt + 1 + mt) * sizeof(int32_t));
+    const size_t o_rec = take((size_t)mt * sizeof(PivRec));
+    const size_t o_wit = take((size_t)mt * sizeof(double));
+    const size_t o_err = take(sizeof(K1Err));
+    int rc = ensure_dev(&h->tail_mem, &h->tail_bytes, off);
+    if (rc) return rc;
+    rc = ensure_pinned(&h->hpin, &h->hpin_bytes, (size_t)(mt + Gt + 1 + mt) * sizeof(int32_t) + 64);
+    if (rc) return rc;
+    char* base = (char*)h->tail_mem;
+    int32_t* hi = (int32_t*)h->hpin;
+    int32_t* iota = hi;
+    int32_t* tptr = iota + mt;
+    int32_t* trows = tptr + Gt + 1;
+    for (int64_t i = 0; i < mt; ++i) iota[i] = (int32_t)i;
+    tptr[0] = 0;
+    for (int64_t c = 0; c < Gt; ++c) tptr[c + 1] = tptr[c] + (int32_t)((mt - c + Gt - 1) / Gt);
+    std::vector<int32_t> fill(tptr, tptr + Gt);
+    for (int64_t i = 0; i < mt; ++i) trows[fill[(size_t)(i % Gt)]++] = (int32_t)i;
+    CUDA_TRY(cudaMemcpyAsync(base + o_int, hi, (size_t)(mt + Gt + 1 + mt) * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemsetAsync(base + o_rec, 0, (size_t)mt * sizeof(PivRec), st));
+    CUDA_TRY(cudaMemsetAsync(base + o_err, 0, sizeof(K1Err), st));
+    const int32_t* d_iota = (const int32_t*)(base + o_int);
+    K1Params p{};
+    p.ws[0] = rows;
+    p.row_wit[0] = (double*)(base + o_wit);
+    p.ld = ldr;
+    p.n = (int32_t)mt;
+    p.n_groups = 1;
+    p.n_local_groups = 1;
+    p.epoch = h->epoch;
+    p.err = (K1Err*)(base + o_err);
+    p.chunk = (int32_t)std::min<int64_t>((int64_t)align_up((size_t)mt, 2), kK1MaxChunk);
+    p.timeout_ns = 20ull * 1000000000ull;
+    p.abort_flag = nullptr;
+    p.in_place = 1;
+    p.wit_in = wit;
+    p.ncol0 = (int32_t)mt;
+    p.n_steps = (int32_t)(mt - 1);
+    p.seq = d_iota;
+    p.row_pstep = d_iota;
+    p.pstep_offset = 0;
+    p.cta_row_ptr = d_iota + mt;
+    p.cta_rows = p.cta_row_ptr + Gt + 1;
+    p.ctas_per_group = (int32_t)Gt;
+    p.rec[0] = (PivRec*)(base + o_rec);
+    cudaError_t e = k1_launch(p, false, st);
+    if (e != cudaSuccess) return fail(MCND_ECUDA, "mg_tail: %s", cudaGetErrorString(e));
+    CUDA_TRY(cudaMemcpyAsync(h_recs, base + o_rec, (size_t)mt * sizeof(PivRec), cudaMemcpyDeviceToHost, st));
+    K1Err he{};
+    CUDA_TRY(cudaMemcpyAsync(&he, base + o_err, sizeof(K1Err), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    if (h_err) { h_err[0] = he.error; h_err[1] = he.err_step; h_err[2] = he.nonfinite; }
+    return MCND_OK;
+}
+
+// this rank's pivot records (n x 16 B, global step index) and error word (error,
+// step, nonfinite); synchronises the stream
+int mg_records(MgHandle* h, void* h_recs, uint32_t* h_err, cudaStream_t st) {
+    if (!h_recs) return fail(MCND_EINVAL, "mg_records: null output");
+    CUDA_TRY(cudaMemcpyAsync(h_recs, h->recs, (size_t)h->n * sizeof(PivRec), cudaMemcpyDeviceToHost, st));
+    K1Err he{};
+    CUDA_TRY(cudaMemcpyAsync(&he, h->err, sizeof(K1Err), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    if (h_err) { h_err[0] = he.error; h_err[1] = he.err_step; h_err[2] = he.nonfinite; h_err[3] = h->epoch; }
+    return MCND_OK;
+}
 
 }  // namespace
 }  // namespace mcnd
@@ -1330,6 +1637,56 @@ void mcnd_release_workspace(void) {
     }
     cudaSetDevice(cur);
     g_bufs.clear();
+}
+
+
+/* ---- multi-GPU blocked condensation, per-rank engine (see mcnd_b200.h) ---- */
+int mcnd_mg_create(int64_t n, int64_t local_rows, void** handle) {
+    if (!handle) return fail(MCND_EINVAL, "null handle");
+    MgHandle* h = nullptr;
+    int rc = mg_create(n, local_rows, &h);
+    *handle = h;
+    return rc;
+}
+int mcnd_mg_load(void* handle, const double* d_rows, int64_t lds, void* stream) {
+    if (!handle) return fail(MCND_EINVAL, "null handle");
+    return mg_load((MgHandle*)handle, d_rows, lds, (cudaStream_t)stream);
+}
+int mcnd_mg_pair(void* handle, int64_t lr0, int64_t t, int64_t m, double* d_W, int64_t ldw, double* d_Wp,
+                 void* d_gather, void* stream) {
+    if (!handle) return fail(MCND_EINVAL, "null handle");
+    return mg_pair((MgHandle*)handle, lr0, t, m, d_W, ldw, d_Wp, (K2Gather*)d_gather, (cudaStream_t)stream);
+}
+int mcnd_mg_trailing(void* handle, int64_t lr0, int64_t rows, int64_t m, const double* d_W, int64_t ldw,
+                     const double* d_Wp, const void* d_gather, int32_t sm_budget, int32_t par, void* stream) {
+    if (!handle) return fail(MCND_EINVAL, "null handle");
+    return mg_trailing((MgHandle*)handle, lr0, rows, m, d_W, ldw, d_Wp, (const K2Gather*)d_gather, sm_budget, par,
+                       (cudaStream_t)stream);
+}
+int mcnd_mg_export(void* handle, int64_t lr0, int64_t rows, int64_t mt, double* d_out, int64_t ldo, double* d_wit,
+                   void* stream) {
+    if (!handle) return fail(MCND_EINVAL, "null handle");
+    return mg_export((MgHandle*)handle, lr0, rows, mt, d_out, ldo, d_wit, (cudaStream_t)stream);
+}
+int mcnd_mg_tail(void* handle, double* d_rows, int64_t ldr, const double* d_wit, int64_t mt, void* stream,
+                 void* h_recs, uint32_t* h_err) {
+    if (!handle) return fail(MCND_EINVAL, "null handle");
+    return mg_tail((MgHandle*)handle, d_rows, ldr, d_wit, mt, (cudaStream_t)stream, h_recs, h_err);
+}
+int mcnd_mg_records(void* handle, void* h_recs, uint32_t* h_err, void* stream) {
+    if (!handle) return fail(MCND_EINVAL, "null handle");
+    return mg_records((MgHandle*)handle, h_recs, h_err, (cudaStream_t)stream);
+}
+int64_t mcnd_mg_gather_bytes(void) { return (int64_t)sizeof(K2Gather); }
+int64_t mcnd_mg_ld(void* handle) { return handle ? ((MgHandle*)handle)->ld : 0; }
+int mcnd_mg_destroy(void* handle) {
+    auto* h = (MgHandle*)handle;
+    if (!h) return MCND_OK;
+    cudaFree(h->mem);
+    if (h->tail_mem) cudaFree(h->tail_mem);
+    if (h->hpin) cudaFreeHost(h->hpin);
+    delete h;
+    return MCND_OK;
 }
 
 }  // extern "C"

@@ -133,8 +133,263 @@ class BlockRowGroup:
             pass
 
 
+_PIVREC = np.dtype([("v", "<f8"), ("l", "<i4"), ("flag", "<u4")])
+
+
+def blocked_schedule(n: int, world: int, tail: int = 256, b: int = 64):
+    """Host schedule of the multi-GPU blocked condensation (deterministic, identical
+    on every rank).  Rows: contiguous blocks (plan_blocks, runtime.py:33-44).  Each
+    panel pair (2b rows) comes from the rank holding the most live rows, ties ->
+    lowest rank (north_star (3)), as that rank's topmost 2b live rows; the pivot
+    position k_pos = live rows of the ranks before it (runtime.py:158-160).  Returns
+    (pairs, tops, lives, t_tail): pairs = [(owner, local_row0, t, m, k_pos)]."""
+    plan = plan_blocks(n, world)
+    live = [ln for (_, ln) in plan.assignments]
+    top = [0] * world
+    pairs = []
+    t = 0
+    while True:
+        m = n - t
+        o = max(range(world), key=lambda r: (live[r], -r))
+        if live[o] < 2 * b or m - 2 * b < max(tail, 2):
+            break
+        pairs.append((o, top[o], t, m, sum(live[:o])))
+        live[o] -= 2 * b
+        top[o] += 2 * b
+        t += 2 * b
+    return pairs, top, live, t
+
+
+def blocked_pivot_sequence(n: int, world: int, tail: int = 256):
+    """Original row ids in the order the blocked multi-GPU schedule eliminates them
+    (for the oracle: logdet_condensation(a, pivot_sequence=...))."""
+    plan = plan_blocks(n, world)
+    pairs, top, live, _ = blocked_schedule(n, world, tail)
+    seq = []
+    for (o, lr0, _, _, _) in pairs:
+        s0 = plan.assignments[o][0]
+        seq.extend(range(s0 + lr0, s0 + lr0 + 128))
+    for r in range(world):  # tail: the remaining rows top to bottom in global order
+        s0 = plan.assignments[r][0]
+        seq.extend(range(s0 + top[r], s0 + top[r] + live[r]))
+    return seq[: n - 1]
+
+
+class BlockedGroup:
+    """Multi-GPU BLOCKED condensation over the ranks of a torch.distributed group
+    (one GPU per rank, current device set).  Per panel pair: the owner factors its
+    2x64 rows (mcnd_mg_pair), W / Wp / the gather descriptor are broadcast, every
+    rank applies the rank-128 update to its own live rows (mcnd_mg_trailing); the
+    last rows are all-gathered and finished by K1 on every rank (mcnd_mg_tail).
+    Kernels = the single-GPU K2 kernels ("one broadcast per panel
+    of W").  Same result type as logdet_condensation; parity by tolerance."""
+
+    def __init__(self, n: int, group=None, tail: int | None = None):
+        import torch
+        import torch.distributed as dist
+
+        self.torch, self.dist, self.group = torch, dist, group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.nccl = dist.get_backend(group) == "nccl"
+        self.n = int(n)
+        self.plan = plan_blocks(self.n, self.world)
+        self.row0, self.rows = self.plan.assignments[self.rank]
+        self.tail = int(os.environ.get("MCND_K2_TAIL", 256) if tail is None else tail)
+        self.pairs, self.tops, self.lives, self.t_tail = blocked_schedule(self.n, self.world, self.tail)
+        lib = _lib.load()
+        self.lib = lib
+        h = ctypes.c_void_p()
+        _lib.check(lib.mcnd_mg_create(self.n, self.rows, ctypes.byref(h)))
+        self.h = h
+        dev = torch.device("cuda", torch.cuda.current_device())
+        wmax = 128 * (self.n - 64 + 1)
+        self.W = [torch.empty(wmax, dtype=torch.float64, device=dev) for _ in range(2)]
+        self.Wp = [torch.empty(64 * 64, dtype=torch.float64, device=dev) for _ in range(2)]
+        gb = int(lib.mcnd_mg_gather_bytes())
+        self.gp = [torch.zeros(gb, dtype=torch.uint8, device=dev) for _ in range(2)]
+        self.comm = torch.cuda.Stream() if (self.nccl and self.world > 1) else None
+        self.last_device_ms = 0.0
+        self.last_launches = 0
+
+    def _bcast(self, t, src):
+        if self.world == 1:
+            return
+        if self.nccl:
+            self.dist.broadcast(t, src, group=self.group)
+        else:  # gloo (tests): host staging
+            c = t.cpu()
+            self.dist.broadcast(c, src, group=self.group)
+            t.copy_(c)
+
+    def _all_gather(self, t):
+        """all_gather of equal-shape device tensors -> list (rank order)."""
+        if self.world == 1:
+            return [t]
+        if self.nccl:
+            out = [self.torch.empty_like(t) for _ in range(self.world)]
+            self.dist.all_gather(out, t, group=self.group)
+            return out
+        out = [self.torch.empty_like(t, device="cpu") for _ in range(self.world)]
+        self.dist.all_gather(out, t.cpu(), group=self.group)
+        return [o.to(t.device) for o in out]
+
+    def logdet(self, rows) -> LogDet:
+        """rows: this rank's block (plan_blocks rows x n), float64 CUDA tensor."""
+        import math
+
+        torch, lib, h = self.torch, self.lib, self.h
+        n, rank = self.n, self.rank
+        if tuple(rows.shape) != (self.rows, n):
+            raise ValueError(f"rank {rank} expects its block of shape {(self.rows, n)}, got {tuple(rows.shape)}")
+        if rows.dtype != torch.float64 or rows.stride(1) != 1:
+            rows = rows.to(torch.float64).contiguous()
+        stream = torch.cuda.current_stream().cuda_stream
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        _lib.check(lib.mcnd_mg_load(h, rows.data_ptr(), rows.stride(0), stream))
+        nl = 1  # kernels launched on this rank
+        plan = self.plan
+        live = [ln for (_, ln) in plan.assignments]
+        top = [0] * self.world
+        pairs = self.pairs
+        cur = torch.cuda.current_stream()
+        comm = self.comm if (self.nccl and self.world > 1) else None
+        ev_pair = [torch.cuda.Event(), torch.cuda.Event()]
+        ev_bc = [torch.cuda.Event(), torch.cuda.Event()]
+        ev_tr = [torch.cuda.Event(), torch.cuda.Event()]
+
+        def ldw_of(m):
+            return (m - 64 + 1) // 2 * 2
+
+        def launch_pair(q):
+            o, lr0, t, m, _ = pairs[q]
+            W, Wp, gp = self.W[q & 1], self.Wp[q & 1], self.gp[q & 1]
+            _lib.check(lib.mcnd_mg_pair(h, lr0, t, m, W.data_ptr(), ldw_of(m), Wp.data_ptr(), gp.data_ptr(), stream))
+            ev_pair[q & 1].record(cur)
+
+        if pairs and pairs[0][0] == rank:
+            launch_pair(0)
+            nl += 5
+        for q, (o, lr0, t, m, _) in enumerate(pairs):
+            W, Wp, gp = self.W[q & 1], self.Wp[q & 1], self.gp[q & 1]
+            ldw = ldw_of(m)
+            if comm is not None:
+                # broadcast on its own stream: it waits only for the pair (owner) and for the
+                # buffer's previous user (trailing update of pair q-2 on this rank)
+                if rank == o:
+                    comm.wait_event(ev_pair[q & 1])
+                if q >= 2:
+                    comm.wait_event(ev_tr[q & 1])
+                with torch.cuda.stream(comm):
+                    self.dist.broadcast(W[: 128 * ldw], o, group=self.group)
+                    self.dist.broadcast(Wp, o, group=self.group)
+                    self.dist.broadcast(gp, o, group=self.group)
+                ev_bc[q & 1].record(comm)
+                cur.wait_event(ev_bc[q & 1])
+            elif self.world > 1:
+                self._bcast(W[: 128 * ldw], o)
+                self._bcast(Wp, o)
+                self._bcast(gp, o)
+            live[o] -= 128
+            top[o] += 128
+            # look-ahead: the next owner first updates the 128 rows it contributes next,
+            # factors them (its broadcast can start at once), then updates the rest
+            nxt = pairs[q + 1][0] if q + 1 < len(pairs) else -1
+            r0, rows_r = top[rank], live[rank]
+            if nxt == rank and rows_r > 128:
+                _lib.check(lib.mcnd_mg_trailing(h, r0, 128, m, W.data_ptr(), ldw, Wp.data_ptr(), gp.data_ptr(), 0,
+                                                q & 1, stream))
+                launch_pair(q + 1)
+                _lib.check(lib.mcnd_mg_trailing(h, r0 + 128, rows_r - 128, m, W.data_ptr(), ldw, Wp.data_ptr(),
+                                                gp.data_ptr(), 0, q & 1, stream))
+                nl += 5 + 6
+            else:
+                if rows_r > 0:
+                    _lib.check(lib.mcnd_mg_trailing(h, r0, rows_r, m, W.data_ptr(), ldw, Wp.data_ptr(), gp.data_ptr(),
+                                                    0, q & 1, stream))
+                    nl += 3
+                if nxt == rank:
+                    launch_pair(q + 1)
+                    nl += 5
+            ev_tr[q & 1].record(cur)
+        # tail: every rank's remaining rows (first mt columns), gathered in rank order
+        mt = n - self.t_tail
+        ldr = (mt + 1) // 2 * 2
+        rmax = max(live)
+        dev = rows.device
+        buf = torch.zeros((max(rmax, 1), ldr), dtype=torch.float64, device=dev)
+        wbuf = torch.zeros(max(rmax, 1), dtype=torch.float64, device=dev)
+        if live[rank] > 0:
+            _lib.check(lib.mcnd_mg_export(h, top[rank], live[rank], mt, buf.data_ptr(), ldr, wbuf.data_ptr(), stream))
+        bufs = self._all_gather(buf)
+        wbufs = self._all_gather(wbuf)
+        tail_rows = torch.cat([bufs[r][: live[r]] for r in range(self.world)]).contiguous()
+        tail_wit = torch.cat([wbufs[r][: live[r]] for r in range(self.world)]).contiguous()
+        trec = np.zeros(mt, dtype=_PIVREC)
+        terr = np.zeros(4, dtype=np.uint32)
+        stream = torch.cuda.current_stream().cuda_stream
+        _lib.check(lib.mcnd_mg_tail(h, tail_rows.data_ptr(), ldr, tail_wit.data_ptr(), mt, stream, trec.ctypes.data,
+                                    terr.ctypes.data))
+        self.last_launches = nl + 1
+        rec = np.zeros(n, dtype=_PIVREC)
+        err = np.zeros(4, dtype=np.uint32)
+        _lib.check(lib.mcnd_mg_records(h, rec.ctypes.data, err.ctypes.data, stream))
+        e1.record()
+        e1.synchronize()
+        self.last_device_ms = e0.elapsed_time(e1)
+        if self.world > 1:
+            gathered = [None] * self.world
+            self.dist.all_gather_object(gathered, (rec.tobytes(), err.tolist()), group=self.group)
+        else:
+            gathered = [(rec.tobytes(), err.tolist())]
+        recs = [np.frombuffer(g[0], dtype=_PIVREC) for g in gathered]
+        errs = [g[1] for g in gathered]
+        if any(e[2] for e in errs) or terr[2]:
+            raise ValueError("matrix entries must be finite (no NaN/Inf)")
+        if any(e[0] for e in errs) or terr[0]:
+            raise RuntimeError(f"mcnd_b200 multi-GPU blocked: device timeout (errors {errs}, tail {terr.tolist()})")
+        # fold: the reference's sign / log bookkeeping (condense.py:124-128, 159-160) in step order
+        sign, log_acc = 1, 0.0
+        for (o, lr0, t, m, kpos) in self.pairs:
+            ro, ep = recs[o], errs[o][3]
+            for s_ in range(128):
+                v, l, fl = float(ro["v"][t + s_]), int(ro["l"][t + s_]), int(ro["flag"][t + s_])
+                if fl != ep or l < 0:
+                    return SINGULAR
+                ms = m - s_
+                sign *= (1 if v > 0 else -1) * (-1 if l != ms - 1 else 1) * (-1 if (kpos + ms - 1) & 1 else 1)
+                log_acc += math.log(abs(v))
+        ep0 = errs[rank][3]
+        for j in range(mt):
+            v, l, fl = float(trec["v"][j]), int(trec["l"][j]), int(trec["flag"][j])
+            if fl != ep0 or l < 0:
+                return SINGULAR
+            mj = mt - j
+            if j < mt - 1:
+                sign *= (1 if v > 0 else -1) * (-1 if l != mj - 1 else 1) * (-1 if (mj - 1) & 1 else 1)
+            else:
+                sign *= 1 if v > 0 else -1
+            log_acc += math.log(abs(v))
+        return LogDet(sign, log_acc)
+
+    def close(self):
+        if self.h:
+            self.lib.mcnd_mg_destroy(self.h)
+            self.h = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def bench_main(args):
-    """bench.py --gpus N under torchrun: C3 on N GPUs (strong scaling)."""
+    """bench.py --gpus N under torchrun: one matrix, block rows over N GPUs (strong
+    scaling).  Default method as on one GPU: blocked for N >= 2048 (BlockedGroup:
+    panel pairs from the rank with the most live rows, W broadcast, local rank-128
+    updates), unblocked below (BlockRowGroup: pivot rows pushed over NVLink)."""
     import json
     import statistics
 
@@ -155,23 +410,31 @@ def bench_main(args):
     name, a, n = B.workload(args.config)
     if a.ndim != 2:
         raise SystemExit("multi-GPU bench needs a single-matrix config")
-    grp = BlockRowGroup(n)
-    s, ln = grp.local_rows()
+    method = args.method or ("unblocked" if n < 2048 else "blocked")
+    if method == "blocked":
+        grp = BlockedGroup(n)
+        s, ln = grp.row0, grp.rows
+        run = lambda d: grp.logdet(d)
+    else:
+        grp = BlockRowGroup(n)
+        s, ln = grp.local_rows()
+        run = lambda d: grp.mc_parallel(d, fast=args.fast).logdet
     block = np.ascontiguousarray(a[s:s + ln])
     d = torch.from_numpy(block).cuda()
     h = torch.empty(block.shape, dtype=torch.float64, pin_memory=True)
     h.numpy()[...] = block
     for _ in range(args.warmup):
-        res = grp.mc_parallel(d, fast=args.fast)
+        res = run(d)
     torch.cuda.synchronize()
     dist.barrier()
     stream = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     kms = []
+    launches0 = 0
     with B.ClockSampler(local) as clk:
         e0.record(stream)
         for _ in range(args.steps):
-            res = grp.mc_parallel(d, fast=args.fast)
+            res = run(d)
             kms.append(grp.last_device_ms)
         e1.record(stream)
         torch.cuda.synchronize()
@@ -185,18 +448,29 @@ def bench_main(args):
     f0.record(stream)
     for _ in range(args.steps):
         dd = h.cuda(non_blocking=True)
-        res_e = grp.mc_parallel(dd, fast=args.fast)
+        res_e = run(dd)
     f1.record(stream)
     torch.cuda.synchronize()
     ms_e = torch.tensor([f0.elapsed_time(f1) / args.steps], device="cuda")
     dist.all_reduce(ms_e, op=dist.ReduceOp.MAX)
-    assert res_e.logdet == res.logdet
+    assert res_e == res
+    lt = torch.tensor([getattr(grp, "last_launches", 1) * args.steps], device="cuda")
+    dist.all_reduce(lt)  # every rank's kernels
+    launches = int(lt.item())
     grp.close()
     if rank == 0:
         t = float(ms.item())
         hbm, peak_kind = B.peaks()
-        Bb = B.algorithmic_bytes(n)
-        achieved = Bb / (float(km.item()) * 1e-3) / 1e9
+        if method == "blocked":
+            achieved = B.flops(n) / (float(km.item()) * 1e-3) / 1e12
+            roof = {"bound": "tensor", "achieved": achieved, "peak": B.FP64_PEAK_TFLOPS * world,
+                    "peak_kind": f"measured cuBLAS DGEMM x{world}", "unit": "TFLOP/s",
+                    "frac": achieved / (B.FP64_PEAK_TFLOPS * world), "traffic": None}
+        else:
+            Bb = B.algorithmic_bytes(n)
+            achieved = Bb / (float(km.item()) * 1e-3) / 1e9
+            roof = {"bound": "hbm", "achieved": achieved, "peak": hbm * world, "peak_kind": peak_kind + f" x{world}",
+                    "unit": "GB/s", "frac": achieved / (hbm * world), "traffic": None}
         line = {
             "metric": B.metric_name(args.config), "value": B.flops(n) / (t * 1e-3) / 1e9, "unit": "GFLOP/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t,
@@ -204,17 +478,18 @@ def bench_main(args):
             "scaling": "strong",
             "vs_baseline": (B.PAPER_TABLE3_N8000.get(world) / (t / 1e3)) if (args.config == "c3" and world in B.PAPER_TABLE3_N8000) else None,
             "dtype": "f64", "data": "synthetic (numpy PCG64 seed, BASELINE recipe)",
-            "config": {"workload": name, "n": n, "parallelism": f"block-row x{world} GPUs, pivot rows pushed over NVLink",
+            "config": {"workload": name, "n": n, "method": method,
+                       "parallelism": (f"block rows x{world} GPUs: panel pairs from the rank with the most live rows, "
+                                       "W broadcast (NCCL), local rank-128 updates") if method == "blocked" else
+                                      f"block-row x{world} GPUs, pivot rows pushed over NVLink",
                        "mode": "fast-fma" if args.fast else "reference-exact",
                        "l2": "input larger than L2 per rank" if 8 * n * n / world > 126e6 else "per-rank block fits L2"},
-            "result": {"sign": res.logdet.sign, "log_abs": res.logdet.log_abs,
-                       "broadcasts": res.stats.broadcasts},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm * world, "peak_kind": peak_kind + f" x{world}",
-                         "unit": "GB/s", "frac": achieved / (hbm * world), "traffic": None},
+            "result": {"sign": res.sign, "log_abs": res.log_abs},
+            "roofline": roof,
             "e2e": {"value": B.flops(n) / (float(ms_e.item()) * 1e-3) / 1e9, "unit": "GFLOP/s",
                     "ms_per_step": float(ms_e.item()), "h2d_bytes_per_step": int(block.nbytes) * world,
-                    "d2h_bytes_per_step": (12 * n + 8 * world) * world},
-            "gpu_launches": args.steps * world,
+                    "d2h_bytes_per_step": 16 * n * world},
+            "gpu_launches": launches,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
