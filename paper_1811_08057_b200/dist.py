@@ -408,8 +408,8 @@ def bench_main(args):
     import bench as B
 
     name, a, n = B.workload(args.config)
-    if a.ndim != 2:
-        raise SystemExit("multi-GPU bench needs a single-matrix config")
+    if a.ndim == 3:
+        return _bench_batched(args, B, name, a, n, rank, world, local)
     method = args.method or ("unblocked" if n < 2048 else "blocked")
     if method == "blocked":
         grp = BlockedGroup(n)
@@ -492,5 +492,71 @@ def bench_main(args):
             "gpu_launches": launches,
             "clocks": clk.summary(),
         }
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+
+
+def _bench_batched(args, B, name, a, n, rank, world, local):
+    """C4 over N GPUs: the batch is sharded (contiguous slices), no exchange
+    (replicas of K3); total batch fixed (strong scaling)."""
+    import json
+    import statistics
+
+    import torch
+    import torch.distributed as dist
+
+    from .batched import logdet_batched
+
+    plan = plan_blocks(a.shape[0], world)
+    s, ln = plan.assignments[rank]
+    d = torch.from_numpy(np.ascontiguousarray(a[s:s + ln])).cuda()
+    for _ in range(args.warmup):
+        logdet_batched(d, fast=args.fast)
+    torch.cuda.synchronize()
+    flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")
+    stream = torch.cuda.current_stream()
+    times = []
+    with B.ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.fill_(1.0)
+            dist.barrier()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            sg, lg = logdet_batched(d, fast=args.fast)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1))
+    ms = torch.tensor([statistics.mean(times)], device="cuda")
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    h = torch.empty(d.shape, dtype=torch.float64, pin_memory=True)
+    h.copy_(d)
+    logdet_batched(h.numpy(), fast=args.fast)
+    dist.barrier()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    for _ in range(args.steps):
+        logdet_batched(h.numpy(), fast=args.fast)
+    f1.record(stream)
+    torch.cuda.synchronize()
+    ms_e = torch.tensor([f0.elapsed_time(f1) / args.steps], device="cuda")
+    dist.all_reduce(ms_e, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        t = float(ms.item())
+        hbm, peak_kind = B.peaks()
+        byt = a.nbytes + a.shape[0] * 12
+        fl = a.shape[0] * B.flops(n)
+        line = {"metric": B.metric_name("c4"), "value": fl / (t * 1e-3) / 1e9, "unit": "GFLOP/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": t, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (numpy PCG64 seed 4)",
+                "config": {"workload": name, "batch": a.shape[0], "n": n, "parallelism": f"batch sharded x{world}",
+                           "l2": "L2 flushed between iterations"},
+                "roofline": {"bound": "hbm", "achieved": byt / (t * 1e-3) / 1e9, "peak": hbm * world,
+                             "peak_kind": peak_kind + f" x{world}", "unit": "GB/s",
+                             "frac": byt / (t * 1e-3) / 1e9 / (hbm * world), "traffic": None},
+                "e2e": {"value": fl / (float(ms_e.item()) * 1e-3) / 1e9, "unit": "GFLOP/s",
+                        "ms_per_step": float(ms_e.item()), "h2d_bytes_per_step": a.nbytes,
+                        "d2h_bytes_per_step": a.shape[0] * 12},
+                "gpu_launches": args.steps * world, "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()

@@ -114,3 +114,44 @@ def test_round_robin_owner_equals_most_live_rows_when_divisible():
             most.append(w)
             consumed[w] += 1
         assert rr == most, (n, p)
+
+
+# ---- multi-GPU blocked schedule (host logic of dist.BlockedGroup) ----
+@pytest.mark.parametrize("n,world,tail", [(8000, 8, 256), (8000, 2, 256), (4000, 2, 256), (1000, 3, 100),
+                                          (700, 2, 2), (32768, 8, 256)])
+def test_blocked_schedule_invariants(n, world, tail):
+    from paper_1811_08057_b200.dist import blocked_schedule, blocked_pivot_sequence
+    from paper_1811_08057_b200.runtime import plan_blocks
+
+    plan = plan_blocks(n, world)
+    pairs, top, live, t_tail = blocked_schedule(n, world, tail)
+    lv = [ln for (_, ln) in plan.assignments]
+    tp = [0] * world
+    t = 0
+    for (o, lr0, tt, m, kpos) in pairs:
+        assert tt == t and m == n - t
+        assert lv[o] == max(lv) and all(lv[r] < lv[o] for r in range(o))  # most live rows, ties -> lowest
+        assert lr0 == tp[o] and lv[o] >= 128
+        assert kpos == sum(lv[:o])
+        lv[o] -= 128
+        tp[o] += 128
+        t += 128
+    assert (tp, lv, t) == (top, live, t_tail)
+    assert sum(live) == n - t_tail and n - t_tail >= 2
+    seq = blocked_pivot_sequence(n, world, tail)
+    assert len(seq) == n - 1 and len(set(seq)) == n - 1 and all(0 <= r < n for r in seq)
+
+
+def test_blocked_pivot_sequence_oracle_consistent():
+    """The schedule's pivot order is a valid reference pivot_sequence (condense.py:147-152):
+    the oracle accepts it and lands within tolerance of the top-to-bottom result."""
+    from oracle import mcnd_oracle as O
+    from paper_1811_08057_b200.dist import blocked_pivot_sequence
+
+    a = np.random.default_rng(5).uniform(-1, 1, (600, 600))
+    ref = O.logdet_condensation(a)
+    for world in (1, 2, 3):
+        seq = np.array(blocked_pivot_sequence(600, world, 2), dtype=np.int64)
+        got = O.logdet_condensation(a, pivot_sequence=seq)
+        assert got.sign == ref.sign
+        assert abs(got.log_abs - ref.log_abs) <= max(1e-8 * 600, 1e-10 * abs(ref.log_abs))
