@@ -486,6 +486,13 @@ cudaError_t k2_gemm(double* ws, int64_t ld, int32_t rbase, int32_t M, int32_t N2
         cudaFuncSetAttribute(k2_gemm_ms_kernel<64, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * (int)smem_ms);
         cudaFuncSetAttribute(k2_gemm_ms_kernel<128, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * (int)smem_ms);
     }
+    if (sm_budget < 0) {  // one tile per CTA: SMs are released tile by tile (priority-scheduled overlap)
+        const size_t smem_ms = (size_t)MS_ST * MS_STAGE * sizeof(double);
+        const int grid_t = (int)std::min<int64_t>(tiles, 1 << 30);
+        if (K == 64) k2_gemm_ms_kernel<64, 1><<<grid_t, MS_THREADS, smem_ms, s>>>(ws, ld, rbase, M, N2, L, ldl, W, ldw, w, abort);
+        else k2_gemm_ms_kernel<128, 1><<<grid_t, MS_THREADS, smem_ms, s>>>(ws, ld, rbase, M, N2, L, ldl, W, ldw, w, abort);
+        return cudaGetLastError();
+    }
     if (sm_budget > 0) {  // fat CTAs on at most sm_budget SMs
         const size_t smem_ms = (size_t)MS_ST * MS_STAGE * sizeof(double);
         const int grid_f = (int)std::min<int64_t>((tiles + 1) / 2, sm_budget);

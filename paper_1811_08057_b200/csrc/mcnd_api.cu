@@ -64,8 +64,10 @@ struct Buffers {
     void* din = nullptr;   size_t din_bytes = 0;    // H2D staging for host-input calls
     void* hpin = nullptr;  size_t hpin_bytes = 0;   // pinned metadata / result staging
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-    cudaStream_t side = nullptr;                 // K2: trailing updates overlapped with the next panels
+    cudaStream_t side = nullptr;                 // K2: trailing updates overlapped with the next panels (lowest priority)
+    cudaStream_t crit = nullptr;                 // K2: the panel chain (highest priority)
     cudaEvent_t ev_a = nullptr, ev_b = nullptr;  // K2: stream joins
+    cudaEvent_t ev_in = nullptr, ev_out = nullptr;
     int sms = 0;
     uint32_t epoch = 0;
     std::map<std::pair<int64_t, int64_t>, bool> kp_cluster_cache;  // (G, cw) -> co-residency
@@ -86,9 +88,14 @@ int init_buffers(Buffers& b, int dev) {
     cudaDeviceGetAttribute(&b.sms, cudaDevAttrMultiProcessorCount, dev);
     if (cudaEventCreate(&b.ev0) != cudaSuccess || cudaEventCreate(&b.ev1) != cudaSuccess)
         return fail(MCND_ECUDA, "cudaEventCreate failed");
+    int prio_lo = 0, prio_hi = 0;
+    cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
     if (cudaEventCreateWithFlags(&b.ev_a, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&b.ev_b, cudaEventDisableTiming) != cudaSuccess ||
-        cudaStreamCreateWithFlags(&b.side, cudaStreamNonBlocking) != cudaSuccess)
+        cudaEventCreateWithFlags(&b.ev_in, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&b.ev_out, cudaEventDisableTiming) != cudaSuccess ||
+        cudaStreamCreateWithPriority(&b.side, cudaStreamNonBlocking, prio_lo) != cudaSuccess ||
+        cudaStreamCreateWithPriority(&b.crit, cudaStreamNonBlocking, prio_hi) != cudaSuccess)
         return fail(MCND_ECUDA, "cudaEventCreate/cudaStreamCreate failed");
     return MCND_OK;
 }
@@ -683,7 +690,7 @@ int stage_input(Buffers& B, const double* h_a, int64_t rows, int64_t n, int64_t 
 // panel, then the unblocked K1 finishes the last m_tail..m_tail+b-1 rows.  All
 // launches are asynchronous; a failed witness test raises a device abort flag
 // that turns every later launch into a no-op; one D2H at the end.
-int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaStream_t st, mcnd_logdet* out,
+int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaStream_t st_caller, mcnd_logdet* out,
                 double* pivots_out, int32_t* cols_out) {
     clear_out(out);
     int rc = check_shape(d_a, n, lda);
@@ -691,6 +698,15 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
     int code = MCND_OK;
     Buffers* B = buffers_for_current(&code);
     if (!B) return code;
+    // The panel chain runs on a highest-priority stream, the overlapped trailing
+    // updates on a lowest-priority one: SMs freed by the trailing GEMM's CTAs go to
+    // the next panel first.  Joined with the caller's stream at entry and exit.
+    const bool prio = env_long("MCND_K2_PRIO", 1) != 0;
+    cudaStream_t st = prio ? B->crit : st_caller;
+    if (st != st_caller) {
+        CUDA_TRY(cudaEventRecord(B->ev_in, st_caller));
+        CUDA_TRY(cudaStreamWaitEvent(st, B->ev_in, 0));
+    }
     const bool fast = (flags & MCND_FLAG_FAST) != 0;
     const int64_t b = kK2B;
     int64_t m_tail = env_long("MCND_K2_TAIL", 256);
@@ -912,7 +928,9 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
             const int64_t k2 = k + 2;
             int64_t ahead = (k2 + 1 < n_panels) ? 2 * b : (k2 < n_panels ? b : nr);
             int64_t budget = 0;
-            if (overlap && ahead < nr) {
+            if (overlap && ahead < nr && prio) {
+                // priority scheduling: the side GEMM takes whatever SMs the panels leave
+            } else if (overlap && ahead < nr) {
                 // worth it only if the side GEMM on the SMs the next panels leave free
                 // finishes within (next pair's panel work + the full-machine GEMM):
                 // ~20 TF/s DMMA on all SMs, ~0.55 ms of panel work per pair
@@ -943,7 +961,7 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
             if (e == cudaSuccess) e = trailing(0, ahead, st, 0);  // the critical rows first
             if (e == cudaSuccess && ahead < nr) {
                 e = cudaStreamWaitEvent(side, B->ev_a, 0);
-                if (e == cudaSuccess) e = trailing(ahead, nr - ahead, side, (int)budget);
+                if (e == cudaSuccess) e = trailing(ahead, nr - ahead, side, prio ? -1 : (int)budget);
                 if (e == cudaSuccess) e = cudaEventRecord(B->ev_b, side);
                 side_pending = (e == cudaSuccess);
                 n_launch += 3;
@@ -1002,6 +1020,10 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
     CUDA_TRY(cudaMemcpyAsync(h_err, err, sizeof(K1Err), cudaMemcpyDeviceToHost, st));
     e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return fail(MCND_ECUDA, "blocked condensation: %s", cudaGetErrorString(e));
+    if (st != st_caller) {  // the caller's later work is ordered after ours
+        CUDA_TRY(cudaEventRecord(B->ev_out, st));
+        CUDA_TRY(cudaStreamWaitEvent(st_caller, B->ev_out, 0));
+    }
     float ms = 0.f;
     cudaEventElapsedTime(&ms, B->ev0, B->ev1);
     out->device_ms = ms;
