@@ -57,6 +57,65 @@ __global__ void k2_gather_fix_kernel(double* __restrict__ ws, int64_t ld, int32_
         if (lane + 32 * k < nm) row[gp->moved_c[lane + 32 * k]] = v[k];
 }
 
+// Pair gather fused with the L correction: per trailing row (one warp),
+// NL = -A[r, P[0:128]] and the moved columns fixed as in k2_gather_fix_kernel<128>,
+// then NL[64:128] += NL[0:64] * Wp (Wp = -W_k[:, P_{k+1}], staged in shared memory)
+// as 64 sequential FMAs per output -- replacing the separate 64-wide GEMM launch.
+constexpr int kGLThreads = 256;
+__global__ void __launch_bounds__(kGLThreads) k2_gather_lcorr_kernel(double* __restrict__ ws, int64_t ld, int32_t rbase,
+                                                                     int32_t nrows, const K2Gather* __restrict__ gp,
+                                                                     double* __restrict__ L, const double* __restrict__ Wp,
+                                                                     const unsigned* __restrict__ abort) {
+    __shared__ double sWp[64 * 64];
+    if (*(volatile const unsigned*)abort) return;
+    for (int e = threadIdx.x; e < 64 * 64; e += kGLThreads) sWp[e] = Wp[e];
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int nm = gp->n_moved;
+    int pk[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) pk[k] = gp->P[lane + 32 * k];
+    const int mc0 = lane < nm ? gp->moved_c[lane] : 0, ms0 = lane < nm ? gp->moved_src[lane] : 0;
+    const int mc1 = lane + 32 < nm ? gp->moved_c[lane + 32] : 0, ms1 = lane + 32 < nm ? gp->moved_src[lane + 32] : 0;
+    const int mc2 = lane + 64 < nm ? gp->moved_c[lane + 64] : 0, ms2 = lane + 64 < nm ? gp->moved_src[lane + 64] : 0;
+    const int mc3 = lane + 96 < nm ? gp->moved_c[lane + 96] : 0, ms3 = lane + 96 < nm ? gp->moved_src[lane + 96] : 0;
+    for (int i = blockIdx.x * (kGLThreads / 32) + (threadIdx.x >> 5); i < nrows; i += gridDim.x * (kGLThreads / 32)) {
+        double* row = ws + (int64_t)(rbase + i) * ld;
+        double x[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) x[k] = row[pk[k]];
+        double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
+        if (lane < nm) v0 = row[ms0];
+        if (lane + 32 < nm) v1 = row[ms1];
+        if (lane + 64 < nm) v2 = row[ms2];
+        if (lane + 96 < nm) v3 = row[ms3];
+        __syncwarp();
+        if (lane < nm) row[mc0] = v0;
+        if (lane + 32 < nm) row[mc1] = v1;
+        if (lane + 64 < nm) row[mc2] = v2;
+        if (lane + 96 < nm) row[mc3] = v3;
+        const double n00 = -x[0], n01 = -x[1];
+        double n10 = -x[2], n11 = -x[3];
+#pragma unroll 8
+        for (int k = 0; k < 32; ++k) {
+            const double a = __shfl_sync(0xffffffffu, n00, k);
+            n10 = fma(a, sWp[k * 64 + lane], n10);
+            n11 = fma(a, sWp[k * 64 + lane + 32], n11);
+        }
+#pragma unroll 8
+        for (int k = 0; k < 32; ++k) {
+            const double a = __shfl_sync(0xffffffffu, n01, k);
+            n10 = fma(a, sWp[(k + 32) * 64 + lane], n10);
+            n11 = fma(a, sWp[(k + 32) * 64 + lane + 32], n11);
+        }
+        double* Lr = L + (int64_t)i * 128;
+        Lr[lane] = n00;
+        Lr[lane + 32] = n01;
+        Lr[lane + 64] = n10;
+        Lr[lane + 96] = n11;
+    }
+}
+
 __device__ __forceinline__ int pi_of(const K2Gather* g, int x) {
     for (int k = 0; k < g->n_moved; ++k)
         if (g->moved_c[k] == x) return g->moved_src[k];
@@ -444,6 +503,21 @@ cudaError_t k2_gather_fix(double* ws, int64_t ld, int32_t rbase, int32_t nrows, 
     if (K == 64) k2_gather_fix_kernel<64><<<grid, warps * 32, 0, s>>>(ws, ld, rbase, nrows, gp, L, abort);
     else if (K == 128) k2_gather_fix_kernel<128><<<grid, warps * 32, 0, s>>>(ws, ld, rbase, nrows, gp, L, abort);
     else return cudaErrorInvalidValue;
+    return cudaGetLastError();
+}
+
+cudaError_t k2_gather_lcorr(double* ws, int64_t ld, int32_t rbase, int32_t nrows, const K2Gather* gp, double* L,
+                            const double* Wp, const unsigned* abort, cudaStream_t s) {
+    if (nrows <= 0) return cudaSuccess;
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const int per = kGLThreads / 32;
+    const int grid = (int)std::min<int64_t>(((int64_t)nrows + per - 1) / per, 4 * (int64_t)sms);
+    k2_gather_lcorr_kernel<<<grid, kGLThreads, 0, s>>>(ws, ld, rbase, nrows, gp, L, Wp, abort);
     return cudaGetLastError();
 }
 

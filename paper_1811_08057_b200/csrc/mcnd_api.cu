@@ -882,6 +882,7 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
     // pair parity so the side GEMM can read pair q's while pair q+1 writes its own.
     const bool pairs = env_long("MCND_K2_PAIRS", 1) != 0;
     const bool overlap = pairs && env_long("MCND_K2_OVERLAP", 1) != 0;
+    const bool fuse_lc = env_long("MCND_K2_FUSE_LC", 1) != 0;
     const int64_t min_budget = env_long("MCND_K2_MIN_BUDGET", B->sms / 4);
     bool side_pending = false;
     cudaStream_t side = B->side;
@@ -945,11 +946,17 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
             // (relative to the pair's trailing block) on stream `ss`
             auto trailing = [&](int64_t r0, int64_t rows, cudaStream_t ss, int sm_budget) -> cudaError_t {
                 double* const Lr = Lq + r0 * 2 * b;
-                cudaError_t ee = k2_gather_fix(ws, ld, (int32_t)(kb + 2 * b + r0), (int32_t)rows, 128, gpair, Lr, abort, ss);
-                if (ss == st) mark("gather");
-                if (ee == cudaSuccess)  // NL[:, 64:128] += NL[:, 0:64] * (-Wp)   (NL = -L; no witness: scratch)
-                    ee = k2_gemm(Lr + b, 2 * b, 0, (int32_t)rows, (int32_t)b, 64, Lr, 2 * b, Wp, b, nullptr, abort, ss);
-                if (ss == st) mark("lcorr");
+                cudaError_t ee;
+                if (fuse_lc) {  // gather + NL[:, 64:128] += NL[:, 0:64] * (-Wp) in one pass
+                    ee = k2_gather_lcorr(ws, ld, (int32_t)(kb + 2 * b + r0), (int32_t)rows, gpair, Lr, Wp, abort, ss);
+                    if (ss == st) mark("gather_lcorr");
+                } else {
+                    ee = k2_gather_fix(ws, ld, (int32_t)(kb + 2 * b + r0), (int32_t)rows, 128, gpair, Lr, abort, ss);
+                    if (ss == st) mark("gather");
+                    if (ee == cudaSuccess)  // NL[:, 64:128] += NL[:, 0:64] * (-Wp)   (NL = -L; no witness: scratch)
+                        ee = k2_gemm(Lr + b, 2 * b, 0, (int32_t)rows, (int32_t)b, 64, Lr, 2 * b, Wp, b, nullptr, abort, ss);
+                    if (ss == st) mark("lcorr");
+                }
                 if (ee == cudaSuccess)
                     ee = k2_gemm(ws, ld, (int32_t)(kb + 2 * b + r0), (int32_t)rows, (int32_t)(m - 2 * b), 128, Lr, 2 * b,
                                  Wq, ld, wit, abort, ss, sm_budget);

@@ -125,6 +125,9 @@ int kp_debug_spans(unsigned long long* out, int max_spans);
 // Per trailing row: L[r, 0:K] = -A[r, P[0:K]] (negated), then A[r, c] = A[r, src] for the moved columns.
 cudaError_t k2_gather_fix(double* ws, int64_t ld, int32_t rbase, int32_t nrows, int32_t K, const K2Gather* gp,
                           double* L, const unsigned* abort, cudaStream_t s);
+// Pair gather (K = 128) fused with the L correction NL[:, 64:128] += NL[:, 0:64] * Wp.
+cudaError_t k2_gather_lcorr(double* ws, int64_t ld, int32_t rbase, int32_t nrows, const K2Gather* gp, double* L,
+                            const double* Wp, const unsigned* abort, cudaStream_t s);
 // Panel pair (two 64-row panels, one rank-128 trailing update): from the two panels'
 // descriptors build the composite gather descriptor, Wp[s][s'] = W0[s][P1[s']] and
 // permute W0's columns into the final layout of the pair (one CTA).
