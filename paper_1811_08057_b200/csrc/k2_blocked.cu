@@ -25,6 +25,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include "mcnd_internal.h"
+#include "k2_pair_prep.cuh"
 
 namespace mcnd {
 namespace {
@@ -116,16 +117,7 @@ __global__ void __launch_bounds__(kGLThreads) k2_gather_lcorr_kernel(double* __r
     }
 }
 
-__device__ __forceinline__ int pi_of(const K2Gather* g, int x) {
-    for (int k = 0; k < g->n_moved; ++k)
-        if (g->moved_c[k] == x) return g->moved_src[k];
-    return x;
-}
-
-// Single CTA (512 threads).  g0: panel k (layout width m), g1: panel k+1 (layout
-// width m-64).  Wc rows 0..63 = W_k (width m-64 layout), rows 64..127 = W_{k+1}.
-// Both descriptors are staged in shared memory first: the column-map compositions
-// (pi_of) then walk shared memory instead of chains of dependent global loads.
+// Single CTA (512 threads): the standalone pair prep (k2_pair_prep.cuh).
 constexpr int kPrepThreads = 512;
 __global__ void __launch_bounds__(kPrepThreads) k2_pair_prep_kernel(const K2Gather* __restrict__ g0,
                                                                     const K2Gather* __restrict__ g1, int32_t m,
@@ -133,61 +125,8 @@ __global__ void __launch_bounds__(kPrepThreads) k2_pair_prep_kernel(const K2Gath
                                                                     double* __restrict__ Wp, K2Gather* __restrict__ gpair,
                                                                     const unsigned* __restrict__ abort) {
     if (*(volatile const unsigned*)abort) return;
-    const int tid = threadIdx.x;
-    __shared__ K2Gather s0, s1;
-    __shared__ int s_cand[4 * kK2B];
-    __shared__ int s_nc, s_nm;
-    {
-        constexpr int kWords = (int)(sizeof(K2Gather) / sizeof(int32_t));
-        const int32_t* a0 = reinterpret_cast<const int32_t*>(g0);
-        const int32_t* a1 = reinterpret_cast<const int32_t*>(g1);
-        for (int i = tid; i < kWords; i += kPrepThreads) {
-            reinterpret_cast<int32_t*>(&s0)[i] = a0[i];
-            reinterpret_cast<int32_t*>(&s1)[i] = a1[i];
-        }
-        if (tid == 0) { s_nc = 0; s_nm = 0; }
-    }
-    __syncthreads();
-    // (a) Wp[s][s'] = W_k[s][P1[s']] (before W_k's columns are permuted)
-#pragma unroll 4
-    for (int e = tid; e < kK2B * kK2B; e += kPrepThreads) {
-        const int sr = e / kK2B, sp = e % kK2B;
-        Wp[sr * kK2B + sp] = -Wc[(int64_t)sr * ldw + s1.P[sp]];  // negated: (-L1) = (-X) + (-L0)(-Wp)
-    }
-    // (b) composite gather columns: panel k's pivots, then panel k+1's pivots mapped to width m
-    if (tid < kK2B) {
-        gpair->P[tid] = s0.P[tid];
-        gpair->P[kK2B + tid] = pi_of(&s0, s1.P[tid]);
-        gpair->l[tid] = s1.l[tid];
-    }
-    // candidate moved columns of the pair: targets of either panel inside the final width
-    const int wf = m - 2 * kK2B;
-    if (tid < s1.n_moved && s1.moved_c[tid] < wf) s_cand[atomicAdd(&s_nc, 1)] = s1.moved_c[tid];
-    if (tid < s0.n_moved && s0.moved_c[tid] < wf) s_cand[atomicAdd(&s_nc, 1)] = s0.moved_c[tid];
-    __syncthreads();
-    if (tid < s_nc) {
-        const int c = s_cand[tid];
-        bool first = true;
-        for (int k = 0; k < tid && first; ++k) first = s_cand[k] != c;
-        if (first) {
-            const int src = pi_of(&s0, pi_of(&s1, c));
-            if (src != c) {
-                const int k = atomicAdd(&s_nm, 1);
-                gpair->moved_c[k] = c;
-                gpair->moved_src[k] = src;
-            }
-        }
-    }
-    __syncthreads();
-    if (tid == 0) gpair->n_moved = s_nm;
-    // (c) W_k's columns into the pair's final layout: column c <- column pi_{k+1}(c)
-    //     (sources lie in the tail [m-128, m-64), never written)
-    const int nm1 = s1.n_moved;
-    for (int e = tid; e < kK2B * nm1; e += kPrepThreads) {
-        const int sr = e / nm1, k = e % nm1;
-        const int c = s1.moved_c[k];
-        if (c < wf) Wc[(int64_t)sr * ldw + c] = Wc[(int64_t)sr * ldw + s1.moved_src[k]];
-    }
+    __shared__ PairPrepSmem sm;
+    pair_prep_body<kPrepThreads>(g0, g1, m, Wc, ldw, Wp, gpair, sm, threadIdx.x);
 }
 
 // ---- DMMA GEMM: C[M x N2] (rows rbase.., in ws) += NL[M x K] * W[K x N2], K = 64 or 128, where

@@ -28,6 +28,7 @@
 #include <cstdint>
 #include <climits>
 #include "mcnd_internal.h"
+#include "k2_pair_prep.cuh"
 
 namespace mcnd {
 namespace {
@@ -169,6 +170,7 @@ __global__ void __launch_bounds__(kThreads, 1) kp_panel_kernel(const KPParams p)
     __shared__ int s_l[kB];
     __shared__ double s_cv, s_win_v, s_win_w;
     __shared__ int s_cpos, s_win_l, s_win_g, s_stop;
+    __shared__ PairPrepSmem s_pp;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g = blockIdx.x, G = p.G, cw = p.cw, m = p.m;
@@ -602,6 +604,10 @@ __global__ void __launch_bounds__(kThreads, 1) kp_panel_kernel(const KPParams p)
                 p.pan->moved_src[k] = q;
             }
         }
+    }
+    if (p.pp_g0 && g == 0) {  // pair prep right here: this CTA's descriptor is final
+        __syncthreads();
+        pair_prep_body<kThreads>(p.pp_g0, p.pan, p.pp_m, p.pp_W, p.pp_ldw, p.pp_Wp, p.pp_gpair, s_pp, tid);
     }
     }
     KP_MARK(0, 11);

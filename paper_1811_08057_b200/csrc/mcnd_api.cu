@@ -883,6 +883,7 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
     const bool pairs = env_long("MCND_K2_PAIRS", 1) != 0;
     const bool overlap = pairs && env_long("MCND_K2_OVERLAP", 1) != 0;
     const bool fuse_lc = env_long("MCND_K2_FUSE_LC", 1) != 0;
+    const bool fuse_pp = env_long("MCND_K2_FUSE_PP", 1) != 0;
     const int64_t min_budget = env_long("MCND_K2_MIN_BUDGET", B->sms / 4);
     bool side_pending = false;
     cudaStream_t side = B->side;
@@ -918,10 +919,14 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
             if (e == cudaSuccess)
                 e = k2_gemm(ws, ld, (int32_t)(kb + b), (int32_t)b, (int32_t)(m - b), 64, Lq, 64, Wq, ld, wit, abort, st);
             mark("r1_gemm");
+            if (fuse_pp) {  // the second panel kernel runs the pair prep in its CTA 0
+                kp.pp_g0 = gp0; kp.pp_W = Wq; kp.pp_ldw = ld; kp.pp_Wp = Wp; kp.pp_gpair = gpair; kp.pp_m = (int32_t)m;
+            }
             if (e == cudaSuccess) e = run_kp(kb + b, gp1, Wq + b * ld);
+            kp.pp_g0 = nullptr;
             mark("kp2");
-            if (e == cudaSuccess) e = k2_pair_prep(gp0, gp1, (int32_t)m, Wq, ld, Wp, gpair, abort, st);
-            mark("pair_prep");
+            if (e == cudaSuccess && !fuse_pp) e = k2_pair_prep(gp0, gp1, (int32_t)m, Wq, ld, Wp, gpair, abort, st);
+            if (!fuse_pp) mark("pair_prep");
             if (e == cudaSuccess) e = join_side();  // trailing rows final for the previous pair
             mark("join");
             const int32_t nr = (int32_t)(n - kb - 2 * b);
@@ -973,7 +978,7 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
                 side_pending = (e == cudaSuccess);
                 n_launch += 3;
             }
-            n_launch += 8;  // 2 panels, gather, update of panel k+1, pair prep, gather, L correction, trailing
+            n_launch += (fuse_pp ? 7 : 8) - (fuse_lc ? 1 : 0);  // 2 panels, gather, update, [prep], gather, [L corr], trailing
             k += 2;
             par ^= 1;
         } else {
@@ -1268,9 +1273,9 @@ int mg_pair(MgHandle* h, int64_t lr0, int64_t t, int64_t m, double* W, int64_t l
         e = k2_gemm(h->ws, h->ld, (int32_t)(lr0 + b), (int32_t)b, (int32_t)(m - b), 64, L, 64, W, ldw, h->wit, h->abort, st);
     if (e == cudaSuccess) {
         KPParams kp1 = mg_kp(h, lr0 + b, t + b, m - b, gp1, W + b * ldw, ldw);
-        e = kp_launch(kp1, st);
+        kp1.pp_g0 = gp0; kp1.pp_W = W; kp1.pp_ldw = ldw; kp1.pp_Wp = Wp; kp1.pp_gpair = gpair; kp1.pp_m = (int32_t)m;
+        e = kp_launch(kp1, st);  // + the pair prep in its CTA 0
     }
-    if (e == cudaSuccess) e = k2_pair_prep(gp0, gp1, (int32_t)m, W, ldw, Wp, gpair, h->abort, st);
     if (e != cudaSuccess) return fail(MCND_ECUDA, "mg_pair: %s", cudaGetErrorString(e));
     return MCND_OK;
 }

@@ -110,6 +110,13 @@ struct KPParams {
     K1Err* err;
     unsigned long long timeout_ns;
     int32_t cluster;          // 1: one thread-block cluster, records pushed over DSMEM (G <= kKPClusterMax)
+    // second panel of a pair: CTA 0 also runs the pair prep (k2_pair_prep.cuh) at the end
+    const K2Gather* pp_g0;    // the pair's first descriptor (nullptr: no pair prep)
+    double* pp_W;             // W of the pair (rows 0..63 = W_k), row stride pp_ldw
+    int64_t pp_ldw;
+    double* pp_Wp;
+    K2Gather* pp_gpair;
+    int32_t pp_m;             // active width at the first panel of the pair
 };
 constexpr int kKPMaxG = 160;
 constexpr int kKPClusterMax = 16;

@@ -270,7 +270,7 @@ class BlockedGroup:
 
         if pairs and pairs[0][0] == rank:
             launch_pair(0)
-            nl += 5
+            nl += 4
         for q, (o, lr0, t, m, _) in enumerate(pairs):
             W, Wp, gp = self.W[q & 1], self.Wp[q & 1], self.gp[q & 1]
             ldw = ldw_of(m)
@@ -303,7 +303,7 @@ class BlockedGroup:
                 launch_pair(q + 1)
                 _lib.check(lib.mcnd_mg_trailing(h, r0 + 128, rows_r - 128, m, W.data_ptr(), ldw, Wp.data_ptr(),
                                                 gp.data_ptr(), 0, q & 1, stream))
-                nl += 5 + 6
+                nl += 4 + 6
             else:
                 if rows_r > 0:
                     _lib.check(lib.mcnd_mg_trailing(h, r0, rows_r, m, W.data_ptr(), ldw, Wp.data_ptr(), gp.data_ptr(),
@@ -311,7 +311,7 @@ class BlockedGroup:
                     nl += 3
                 if nxt == rank:
                     launch_pair(q + 1)
-                    nl += 5
+                    nl += 4
             ev_tr[q & 1].record(cur)
         # tail: every rank's remaining rows (first mt columns), gathered in rank order
         mt = n - self.t_tail
