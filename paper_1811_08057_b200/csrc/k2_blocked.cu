@@ -30,7 +30,6 @@
 namespace mcnd {
 namespace {
 
-constexpr int kB = kK2B;
 
 // One warp per trailing row: L[r, 0:K] = A[r, P], then the moved columns.
 template <int K>
