@@ -157,7 +157,8 @@ __device__ unsigned long long g_kp_trace[64][12];
 #define KP_MARK(s, k) do { } while (0)
 #endif
 
-template <bool kCl>
+// KPER: candidate records per lane of the reducing warp (G <= 32 * KPER)
+template <bool kCl, int KPER>
 __global__ void __launch_bounds__(kThreads, 1) kp_panel_kernel(const KPParams p) {
     extern __shared__ __align__(16) double S[];  // [kB][cw]
     __shared__ double sTi[kB][kB + 1];  // T^{-1}, built one column per step
@@ -276,7 +277,7 @@ __global__ void __launch_bounds__(kThreads, 1) kp_panel_kernel(const KPParams p)
         KP_MARK(s, 0);
         // ---- A. reduce the G proposals for pivot s: warp 0 polls all tagged records
         if (warp == 0) {
-            constexpr int kPer = kKPMaxG / 32;
+            constexpr int kPer = KPER;
             double2 c[kPer], w[kPer];
             unsigned need = 0;  // bit k: record lane + 32k still missing
 #pragma unroll
@@ -635,8 +636,8 @@ size_t kp_smem_bytes(int cw, bool cluster) {
 int kp_cluster_fits(int G, int cw) {
     if (G < 1 || G > kClMax) return 0;
     const size_t smem = kp_smem_bytes(cw, true);
-    if (cudaFuncSetAttribute(kp_panel_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
-        cudaFuncSetAttribute(kp_panel_kernel<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+    if (cudaFuncSetAttribute(kp_panel_kernel<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
+        cudaFuncSetAttribute(kp_panel_kernel<true, 1>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
         cudaGetLastError();
         return 0;
     }
@@ -652,7 +653,7 @@ int kp_cluster_fits(int G, int cw) {
     cfg.attrs = at;
     cfg.numAttrs = 1;
     int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, kp_panel_kernel<true>, &cfg) != cudaSuccess) {
+    if (cudaOccupancyMaxActiveClusters(&n, kp_panel_kernel<true, 1>, &cfg) != cudaSuccess) {
         cudaGetLastError();
         return 0;
     }
@@ -664,8 +665,8 @@ cudaError_t kp_launch(const KPParams& p, cudaStream_t s) {
     const size_t smem = kp_smem_bytes(p.cw, cl);
     KPParams pc = p;
     if (cl) {
-        cudaError_t e = cudaFuncSetAttribute(kp_panel_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e == cudaSuccess) e = cudaFuncSetAttribute(kp_panel_kernel<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        cudaError_t e = cudaFuncSetAttribute(kp_panel_kernel<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(kp_panel_kernel<true, 1>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         if (e != cudaSuccess) return e;
         cudaLaunchConfig_t cfg = {};
         cudaLaunchAttribute at[1];
@@ -679,12 +680,16 @@ cudaError_t kp_launch(const KPParams& p, cudaStream_t s) {
         cfg.stream = s;
         cfg.attrs = at;
         cfg.numAttrs = 1;
-        return cudaLaunchKernelEx(&cfg, kp_panel_kernel<true>, pc);
+        return cudaLaunchKernelEx(&cfg, kp_panel_kernel<true, 1>, pc);
     }
-    cudaError_t e = cudaFuncSetAttribute(kp_panel_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const void* fn = p.G <= 32   ? (const void*)kp_panel_kernel<false, 1>
+                     : p.G <= 64 ? (const void*)kp_panel_kernel<false, 2>
+                     : p.G <= 96 ? (const void*)kp_panel_kernel<false, 3>
+                                 : (const void*)kp_panel_kernel<false, kKPMaxG / 32>;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     void* args[] = {&pc};
-    return cudaLaunchCooperativeKernel((const void*)kp_panel_kernel<false>, dim3(p.G), dim3(kThreads), args, smem, s);
+    return cudaLaunchCooperativeKernel(fn, dim3(p.G), dim3(kThreads), args, smem, s);
 }
 
 }  // namespace mcnd
