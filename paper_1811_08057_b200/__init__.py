@@ -11,6 +11,7 @@ Everything below the Python surface is sm_100a CUDA behind a C ABI
 
 from .batched import logdet_batched
 from .condense import SINGULAR, SINGULAR_RTOL, LogDet, SingularRowError, logdet_blocked, logdet_condensation
+from .io import FormatError, read_matrix, read_matrix_device, write_matrix
 from .matrix import GENERATOR_KINDS, MatrixSpec, as_matrix, generate, require_square
 from .registry import ALGORITHMS, run_algorithm
 from .runtime import CommStats, RunResult, WorkerPlan, mc_parallel, plan_blocks
@@ -35,4 +36,8 @@ __all__ = [
     "as_matrix",
     "generate",
     "require_square",
+    "FormatError",
+    "read_matrix",
+    "read_matrix_device",
+    "write_matrix",
 ]
