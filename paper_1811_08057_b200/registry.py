@@ -10,7 +10,9 @@ a pointer back to the reference package.
 
 from __future__ import annotations
 
+import csv
 import time
+from dataclasses import dataclass
 
 from .condense import logdet_blocked, logdet_condensation
 from .runtime import CommStats, RunResult, mc_parallel
@@ -34,3 +36,74 @@ def run_algorithm(algorithm: str, a, p: int, *, fast: bool = False) -> RunResult
     if algorithm in REFERENCE_ONLY:
         raise ValueError(f"algorithm {algorithm!r} is not on the GPU condensation path; use mcnd for it")
     raise ValueError(f"unknown algorithm {algorithm!r}")
+
+
+# ---- benchmark records in the reference's CSV format ----
+# mcnd/bench.py:26-43: BenchRecord / CSV_HEADER; a GPU sweep written with
+# write_records() is read back by mcnd.bench.read_records, so the reference's
+# format_report (speedup T_s / T_p, bench.py:178-195) covers GPU runs unchanged.
+CSV_HEADER = ["algorithm", "n", "p", "run", "total_s", "scatter_s", "comm_s", "sign", "logabs"]
+GPU_ALGORITHMS = {"mc-gpu": "mc-serial", "mc-gpu-parallel": "mc-parallel", "mc-gpu-blocked": "mc-blocked"}
+
+
+@dataclass(frozen=True)
+class BenchRecord:
+    algorithm: str
+    n: int
+    p: int
+    run_index: int
+    total_seconds: float
+    scatter_seconds: float
+    comm_seconds: float
+    sign: int
+    log_abs: float
+
+
+def run_bench(sizes, workers, repeats: int = 5, kind: str = "uniform-random", seed: int = 0,
+              algorithms=tuple(GPU_ALGORITHMS)) -> list:
+    """The reference's sweep protocol (bench.py:68-108) on the GPU path: one record
+    per (algorithm, n, p, run).  The matrix is made resident on the device once per
+    (n, p) (its copy time = scatter_s, excluded from total_s as in the reference,
+    bench.py:3-4); total_s = wall time of the (synchronous) call: device work + host
+    fold; comm_s = 0 (the exchange is fused into the kernels).  Serial algorithms run only
+    at p = 1."""
+    import torch
+
+    from .matrix import MatrixSpec, generate
+
+    if repeats < 1:
+        raise ValueError("repeats must be >= 1")
+    records = []
+    for n in sizes:
+        a = generate(MatrixSpec(size=n, kind=kind, seed=seed))
+        for p in workers:
+            if p > n:
+                continue
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            d = torch.from_numpy(a).cuda()
+            e1.record()
+            e1.synchronize()
+            scatter = e0.elapsed_time(e1) / 1e3
+            for run in range(repeats):
+                for alg in algorithms:
+                    base = GPU_ALGORITHMS[alg]
+                    if base != "mc-parallel" and p != 1:
+                        continue
+                    torch.cuda.synchronize()
+                    t0 = time.perf_counter()
+                    res = run_algorithm(base, d, p)
+                    total = time.perf_counter() - t0
+                    records.append(BenchRecord(alg, n, p, run, total, scatter, 0.0, res.logdet.sign,
+                                               res.logdet.log_abs))
+    return records
+
+
+def write_records(records, path) -> None:
+    """CSV exactly as mcnd.bench.write_records (bench.py:111-128)."""
+    with open(path, "w", newline="") as f:
+        w = csv.writer(f)
+        w.writerow(CSV_HEADER)
+        for r in records:
+            w.writerow([r.algorithm, r.n, r.p, r.run_index, repr(r.total_seconds), repr(r.scatter_seconds),
+                        repr(r.comm_seconds), r.sign, repr(r.log_abs)])
