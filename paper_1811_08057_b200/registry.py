@@ -43,7 +43,21 @@ def run_algorithm(algorithm: str, a, p: int, *, fast: bool = False) -> RunResult
 # write_records() is read back by mcnd.bench.read_records, so the reference's
 # format_report (speedup T_s / T_p, bench.py:178-195) covers GPU runs unchanged.
 CSV_HEADER = ["algorithm", "n", "p", "run", "total_s", "scatter_s", "comm_s", "sign", "logabs"]
-GPU_ALGORITHMS = {"mc-gpu": "mc-serial", "mc-gpu-parallel": "mc-parallel", "mc-gpu-blocked": "mc-blocked"}
+GPU_ALGORITHMS = {"mc-gpu": "mc-serial", "mc-gpu-parallel": "mc-parallel", "mc-gpu-blocked": "mc-blocked",
+                  "ge-gpu": "ge-cusolver"}
+
+
+def _ge_cusolver(d):
+    """The paper's Gaussian-elimination comparison point on the GPU (SURVEY.md §8(f)
+    rank 3): cuSOLVER LU via torch.linalg.slogdet -- a library baseline, not this
+    package's path."""
+    import torch
+
+    from .condense import SINGULAR, LogDet
+
+    sign, la = torch.linalg.slogdet(d)
+    sg = int(sign.item())
+    return SINGULAR if sg == 0 else LogDet(sg, float(la.item()))
 
 
 @dataclass(frozen=True)
@@ -92,10 +106,12 @@ def run_bench(sizes, workers, repeats: int = 5, kind: str = "uniform-random", se
                         continue
                     torch.cuda.synchronize()
                     t0 = time.perf_counter()
-                    res = run_algorithm(base, d, p)
+                    if base == "ge-cusolver":
+                        ld = _ge_cusolver(d)
+                    else:
+                        ld = run_algorithm(base, d, p).logdet
                     total = time.perf_counter() - t0
-                    records.append(BenchRecord(alg, n, p, run, total, scatter, 0.0, res.logdet.sign,
-                                               res.logdet.log_abs))
+                    records.append(BenchRecord(alg, n, p, run, total, scatter, 0.0, ld.sign, ld.log_abs))
     return records
 
 
