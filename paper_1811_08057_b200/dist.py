@@ -208,7 +208,9 @@ class BlockedGroup:
         self.Wp = [torch.empty(64 * 64, dtype=torch.float64, device=dev) for _ in range(2)]
         gb = int(lib.mcnd_mg_gather_bytes())
         self.gp = [torch.zeros(gb, dtype=torch.uint8, device=dev) for _ in range(2)]
-        self.comm = torch.cuda.Stream() if (self.nccl and self.world > 1) else None
+        # MCND_MG_FORCE_COMM=1: run the broadcast/comm-stream path even with one rank (test hook)
+        self.force_comm = os.environ.get("MCND_MG_FORCE_COMM", "0") == "1"
+        self.comm = torch.cuda.Stream() if (self.nccl and (self.world > 1 or self.force_comm)) else None
         self.last_device_ms = 0.0
         self.last_launches = 0
 
@@ -254,7 +256,7 @@ class BlockedGroup:
         top = [0] * self.world
         pairs = self.pairs
         cur = torch.cuda.current_stream()
-        comm = self.comm if (self.nccl and self.world > 1) else None
+        comm = self.comm
         ev_pair = [torch.cuda.Event(), torch.cuda.Event()]
         ev_bc = [torch.cuda.Event(), torch.cuda.Event()]
         ev_tr = [torch.cuda.Event(), torch.cuda.Event()]
