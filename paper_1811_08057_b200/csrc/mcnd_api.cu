@@ -1290,10 +1290,9 @@ int mg_trailing(MgHandle* h, int64_t lr0, int64_t rows, int64_t m, const double*
     if (lr0 < 0 || rows < 0 || lr0 + rows > h->lr || m < 2 * b + 1 || m > h->n || !W || !Wp || !gpair || ldw < m - b ||
         (ldw & 1))
         return fail(MCND_EINVAL, "mg_trailing: bad arguments");
-    double* L = h->L + (size_t)(par & 1) * std::max<int64_t>(h->lr, 1) * 2 * b;
-    cudaError_t e = k2_gather_fix(h->ws, h->ld, (int32_t)lr0, (int32_t)rows, 128, gpair, L, h->abort, st);
-    if (e == cudaSuccess)
-        e = k2_gemm(L + b, 2 * b, 0, (int32_t)rows, (int32_t)b, 64, L, 2 * b, Wp, b, nullptr, h->abort, st);
+    // L rows are indexed by local row: concurrent calls on disjoint rows never collide
+    double* L = h->L + (size_t)(par & 1) * std::max<int64_t>(h->lr, 1) * 2 * b + (size_t)lr0 * 2 * b;
+    cudaError_t e = k2_gather_lcorr(h->ws, h->ld, (int32_t)lr0, (int32_t)rows, gpair, L, Wp, h->abort, st);
     if (e == cudaSuccess)
         e = k2_gemm(h->ws, h->ld, (int32_t)lr0, (int32_t)rows, (int32_t)(m - 2 * b), 128, L, 2 * b, W, ldw, h->wit,
                     h->abort, st, sm_budget);

@@ -211,6 +211,9 @@ class BlockedGroup:
         # MCND_MG_FORCE_COMM=1: run the broadcast/comm-stream path even with one rank (test hook)
         self.force_comm = os.environ.get("MCND_MG_FORCE_COMM", "0") == "1"
         self.comm = torch.cuda.Stream() if (self.nccl and (self.world > 1 or self.force_comm)) else None
+        # the panel chain on a high-priority stream, overlapped trailing updates on a low one
+        self.crit = torch.cuda.Stream(priority=-1)
+        self.side = self.crit if os.environ.get("MCND_MG_SERIAL", "0") == "1" else torch.cuda.Stream(priority=0)
         self.last_device_ms = 0.0
         self.last_launches = 0
 
@@ -246,20 +249,26 @@ class BlockedGroup:
             raise ValueError(f"rank {rank} expects its block of shape {(self.rows, n)}, got {tuple(rows.shape)}")
         if rows.dtype != torch.float64 or rows.stride(1) != 1:
             rows = rows.to(torch.float64).contiguous()
-        stream = torch.cuda.current_stream().cuda_stream
+        cur = torch.cuda.current_stream()
+        crit, side = self.crit, self.side
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        _lib.check(lib.mcnd_mg_load(h, rows.data_ptr(), rows.stride(0), stream))
+        e0.record(cur)
+        crit.wait_stream(cur)
+        side.wait_stream(cur)
+        hc, hs = crit.cuda_stream, side.cuda_stream
+        _lib.check(lib.mcnd_mg_load(h, rows.data_ptr(), rows.stride(0), hc))
         nl = 1  # kernels launched on this rank
         plan = self.plan
         live = [ln for (_, ln) in plan.assignments]
         top = [0] * self.world
         pairs = self.pairs
-        cur = torch.cuda.current_stream()
         comm = self.comm
         ev_pair = [torch.cuda.Event(), torch.cuda.Event()]
         ev_bc = [torch.cuda.Event(), torch.cuda.Event()]
-        ev_tr = [torch.cuda.Event(), torch.cuda.Event()]
+        ev_trc = [torch.cuda.Event(), torch.cuda.Event()]  # crit / side users of W[q & 1] done
+        ev_trs = [torch.cuda.Event(), torch.cuda.Event()]
+        ev_side = torch.cuda.Event()
+        side_pending = False
 
         def ldw_of(m):
             return (m - 64 + 1) // 2 * 2
@@ -267,8 +276,12 @@ class BlockedGroup:
         def launch_pair(q):
             o, lr0, t, m, _ = pairs[q]
             W, Wp, gp = self.W[q & 1], self.Wp[q & 1], self.gp[q & 1]
-            _lib.check(lib.mcnd_mg_pair(h, lr0, t, m, W.data_ptr(), ldw_of(m), Wp.data_ptr(), gp.data_ptr(), stream))
-            ev_pair[q & 1].record(cur)
+            _lib.check(lib.mcnd_mg_pair(h, lr0, t, m, W.data_ptr(), ldw_of(m), Wp.data_ptr(), gp.data_ptr(), hc))
+            ev_pair[q & 1].record(crit)
+
+        def trailing(r0, nrows, m, W, ldw, Wp, gp, q, on_side):
+            _lib.check(lib.mcnd_mg_trailing(h, r0, nrows, m, W.data_ptr(), ldw, Wp.data_ptr(), gp.data_ptr(),
+                                            -1 if on_side else 0, q & 1, hs if on_side else hc))
 
         if pairs and pairs[0][0] == rank:
             launch_pair(0)
@@ -278,43 +291,60 @@ class BlockedGroup:
             ldw = ldw_of(m)
             if comm is not None:
                 # broadcast on its own stream: it waits only for the pair (owner) and for the
-                # buffer's previous user (trailing update of pair q-2 on this rank)
+                # buffer's previous users (pair q-2's updates on this rank)
                 if rank == o:
                     comm.wait_event(ev_pair[q & 1])
                 if q >= 2:
-                    comm.wait_event(ev_tr[q & 1])
+                    comm.wait_event(ev_trc[q & 1])
+                    comm.wait_event(ev_trs[q & 1])
                 with torch.cuda.stream(comm):
                     self.dist.broadcast(W[: 128 * ldw], o, group=self.group)
                     self.dist.broadcast(Wp, o, group=self.group)
                     self.dist.broadcast(gp, o, group=self.group)
                 ev_bc[q & 1].record(comm)
-                cur.wait_event(ev_bc[q & 1])
-            elif self.world > 1:
+                crit.wait_event(ev_bc[q & 1])
+                side.wait_event(ev_bc[q & 1])
+            elif self.world == 1:
+                side.wait_event(ev_pair[q & 1])  # the side update reads the pair's W, Wp, descriptor
+            else:  # gloo (tests): synchronous host-staged broadcasts
+                crit.synchronize()
+                side.synchronize()
                 self._bcast(W[: 128 * ldw], o)
                 self._bcast(Wp, o)
                 self._bcast(gp, o)
+                crit.wait_stream(cur)  # the host-staged copies landed on the caller's stream
+                side.wait_stream(cur)
             live[o] -= 128
             top[o] += 128
-            # look-ahead: the next owner first updates the 128 rows it contributes next,
-            # factors them (its broadcast can start at once), then updates the rest
+            # look-ahead: the next owner updates the 128 rows it contributes next on the
+            # high-priority stream, factors them at once (its broadcast can start), and
+            # updates the rest on the low-priority stream meanwhile (single-GPU schedule)
             nxt = pairs[q + 1][0] if q + 1 < len(pairs) else -1
             r0, rows_r = top[rank], live[rank]
+            if side_pending:  # rows about to be touched on crit were last updated on side
+                crit.wait_event(ev_side)
+                side_pending = False
             if nxt == rank and rows_r > 128:
-                _lib.check(lib.mcnd_mg_trailing(h, r0, 128, m, W.data_ptr(), ldw, Wp.data_ptr(), gp.data_ptr(), 0,
-                                                q & 1, stream))
+                trailing(r0, 128, m, W, ldw, Wp, gp, q, False)
                 launch_pair(q + 1)
-                _lib.check(lib.mcnd_mg_trailing(h, r0 + 128, rows_r - 128, m, W.data_ptr(), ldw, Wp.data_ptr(),
-                                                gp.data_ptr(), 0, q & 1, stream))
-                nl += 4 + 6
+                if q >= 1:
+                    side.wait_event(ev_trc[(q - 1) & 1])  # its rows' previous update (crit)
+                trailing(r0 + 128, rows_r - 128, m, W, ldw, Wp, gp, q, True)
+                ev_side.record(side)
+                side_pending = True
+                nl += 4 + 4
             else:
                 if rows_r > 0:
-                    _lib.check(lib.mcnd_mg_trailing(h, r0, rows_r, m, W.data_ptr(), ldw, Wp.data_ptr(), gp.data_ptr(),
-                                                    0, q & 1, stream))
-                    nl += 3
+                    trailing(r0, rows_r, m, W, ldw, Wp, gp, q, False)
+                    nl += 2
                 if nxt == rank:
                     launch_pair(q + 1)
                     nl += 4
-            ev_tr[q & 1].record(cur)
+            ev_trc[q & 1].record(crit)
+            ev_trs[q & 1].record(side)
+        crit.wait_stream(side)
+        cur.wait_stream(crit)
+        stream = cur.cuda_stream
         # tail: every rank's remaining rows (first mt columns), gathered in rank order
         mt = n - self.t_tail
         ldr = (mt + 1) // 2 * 2
@@ -421,10 +451,15 @@ def bench_main(args):
         grp = BlockRowGroup(n)
         s, ln = grp.local_rows()
         run = lambda d: grp.mc_parallel(d, fast=args.fast).logdet
-    block = np.ascontiguousarray(a[s:s + ln])
-    d = torch.from_numpy(block).cuda()
-    h = torch.empty(block.shape, dtype=torch.float64, pin_memory=True)
-    h.numpy()[...] = block
+    if isinstance(a, np.ndarray):
+        block = np.ascontiguousarray(a[s:s + ln])
+        d = torch.from_numpy(block).cuda()
+    else:  # device-generated workload (C5)
+        d = a[s:s + ln].contiguous()
+        block = None
+    h = torch.empty(tuple(d.shape), dtype=torch.float64, pin_memory=True)
+    h.copy_(d)
+    nbytes = h.numel() * 8
     for _ in range(args.warmup):
         res = run(d)
     torch.cuda.synchronize()
@@ -489,7 +524,7 @@ def bench_main(args):
             "result": {"sign": res.sign, "log_abs": res.log_abs},
             "roofline": roof,
             "e2e": {"value": B.flops(n) / (float(ms_e.item()) * 1e-3) / 1e9, "unit": "GFLOP/s",
-                    "ms_per_step": float(ms_e.item()), "h2d_bytes_per_step": int(block.nbytes) * world,
+                    "ms_per_step": float(ms_e.item()), "h2d_bytes_per_step": int(nbytes) * world,
                     "d2h_bytes_per_step": 16 * n * world},
             "gpu_launches": launches,
             "clocks": clk.summary(),
