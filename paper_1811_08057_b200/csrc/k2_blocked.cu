@@ -297,6 +297,9 @@ constexpr int MS_BK = 16, MS_ST = 4;          // K per stage, ring depth
 constexpr int MS_LDL = MS_BK + 4;             // 20 doubles: conflict-free A fragments
 constexpr int MS_STAGE = BM * MS_LDL + MS_BK * LDWS;
 constexpr int MS_THREADS = 256;               // 8 warps: 2 (M) x 4 (N), warp tile 32 x 32
+#ifndef MS_PREFETCH_C
+#define MS_PREFETCH_C 1
+#endif
 
 // SUB = 2: a "fat" CTA of two independent 256-thread sub-CTAs (own smem ring, own named
 // barrier) that fills a whole SM, so a grid of B fat CTAs occupies exactly B SMs and
@@ -351,6 +354,22 @@ __global__ void __launch_bounds__(MS_THREADS * SUB, 2 / SUB) k2_gemm_ms_kernel(d
         asm volatile("cp.async.commit_group;" ::: "memory");  // (possibly empty) group keeps the count
     };
 
+    // C tiles are pulled into L2 ahead of use (the first at entry, each next one
+    // mid-way through the current tile): the accumulator load then hits L2
+    auto prefetch_c = [&](int64_t t) {
+        if (MS_PREFETCH_C == 0) return;
+        const int row0 = (int)(t / ntn) * BM, col0 = (int)(t % ntn) * BN;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int r = row0 + wm * 32 + i * 8 + g;
+            if (r < M && q == 0) {
+                const double* crow = ws + (int64_t)(rbase + r) * ld + col0 + wn * 32;
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(crow));
+                if (col0 + wn * 32 + 16 < N2) asm volatile("prefetch.global.L2 [%0];" ::"l"(crow + 16));
+            }
+        }
+    };
+    prefetch_c(t_begin);
 #pragma unroll
     for (int j = 0; j < MS_ST - 1; ++j) load_stage(j);
     double rmx[4] = {0.0, 0.0, 0.0, 0.0};
@@ -368,9 +387,14 @@ __global__ void __launch_bounds__(MS_THREADS * SUB, 2 / SUB) k2_gemm_ms_kernel(d
                 for (int jj = 0; jj < NJ; ++jj) {
                     const int c = col0 + wn * 32 + jj * 8 + 2 * q;
                     if (r < M && c < N2) {
+#ifdef MS_NO_CLOAD  // microbenchmark knob: cost of the C-tile load
+                        acc[i][jj][0] = 0.0;
+                        acc[i][jj][1] = 0.0;
+#else
                         const double2 v = __ldcs(reinterpret_cast<const double2*>(crow + c));
                         acc[i][jj][0] = v.x;
                         acc[i][jj][1] = v.y;
+#endif
                     } else {
                         acc[i][jj][0] = 0.0;
                         acc[i][jj][1] = 0.0;
@@ -378,6 +402,7 @@ __global__ void __launch_bounds__(MS_THREADS * SUB, 2 / SUB) k2_gemm_ms_kernel(d
                 }
             }
         }
+        if (ks == KS / 2 && t + 1 < t_end) prefetch_c(t + 1);
         asm volatile("cp.async.wait_group %0;" ::"n"(MS_ST - 2) : "memory");
         sync();  // stage j landed; buffer (j-1) % MS_ST is free
         load_stage(j + MS_ST - 1);
@@ -514,7 +539,11 @@ cudaError_t k2_gemm(double* ws, int64_t ld, int32_t rbase, int32_t M, int32_t N2
     }
     if (ms_mode) {
         const size_t smem_ms = (size_t)MS_ST * MS_STAGE * sizeof(double);
-        const int grid_ms = (int)std::min<int64_t>(tiles, 2 * (int64_t)sms);
+        // one tile per CTA (measured faster than a persistent grid: CTAs of the next
+        // wave overlap the previous CTAs' epilogues); MCND_K2_GEMM_PERSIST=1 for the other
+        const char* pv = std::getenv("MCND_K2_GEMM_PERSIST");
+        const long persist = pv ? std::strtol(pv, nullptr, 10) : 0;
+        const int grid_ms = (int)(persist ? std::min<int64_t>(tiles, 2 * (int64_t)sms) : std::min<int64_t>(tiles, 1 << 30));
         if (K == 64) k2_gemm_ms_kernel<64, 1><<<grid_ms, MS_THREADS, smem_ms, s>>>(ws, ld, rbase, M, N2, L, ldl, W, ldw, w, abort);
         else k2_gemm_ms_kernel<128, 1><<<grid_ms, MS_THREADS, smem_ms, s>>>(ws, ld, rbase, M, N2, L, ldl, W, ldw, w, abort);
         return cudaGetLastError();
