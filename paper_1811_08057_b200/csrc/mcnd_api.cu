@@ -709,7 +709,7 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
     }
     const bool fast = (flags & MCND_FLAG_FAST) != 0;
     const int64_t b = kK2B;
-    int64_t m_tail = env_long("MCND_K2_TAIL", 256);
+    int64_t m_tail = env_long("MCND_K2_TAIL", 64);
     if (m_tail < 2) m_tail = 2;
     const int64_t n_panels = (n - m_tail >= b) ? (n - m_tail) / b : 0;
     const int64_t kb_end = n_panels * b;

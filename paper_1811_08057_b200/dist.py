@@ -136,7 +136,7 @@ class BlockRowGroup:
 _PIVREC = np.dtype([("v", "<f8"), ("l", "<i4"), ("flag", "<u4")])
 
 
-def blocked_schedule(n: int, world: int, tail: int = 256, b: int = 64):
+def blocked_schedule(n: int, world: int, tail: int = 64, b: int = 64):
     """Host schedule of the multi-GPU blocked condensation (deterministic, identical
     on every rank).  Rows: contiguous blocks (plan_blocks, runtime.py:33-44).  Each
     panel pair (2b rows) comes from the rank holding the most live rows, ties ->
@@ -160,7 +160,7 @@ def blocked_schedule(n: int, world: int, tail: int = 256, b: int = 64):
     return pairs, top, live, t
 
 
-def blocked_pivot_sequence(n: int, world: int, tail: int = 256):
+def blocked_pivot_sequence(n: int, world: int, tail: int = 64):
     """Original row ids in the order the blocked multi-GPU schedule eliminates them
     (for the oracle: logdet_condensation(a, pivot_sequence=...))."""
     plan = plan_blocks(n, world)
@@ -195,7 +195,7 @@ class BlockedGroup:
         self.n = int(n)
         self.plan = plan_blocks(self.n, self.world)
         self.row0, self.rows = self.plan.assignments[self.rank]
-        self.tail = int(os.environ.get("MCND_K2_TAIL", 256) if tail is None else tail)
+        self.tail = int(os.environ.get("MCND_K2_TAIL", 64) if tail is None else tail)
         self.pairs, self.tops, self.lives, self.t_tail = blocked_schedule(self.n, self.world, self.tail)
         lib = _lib.load()
         self.lib = lib
