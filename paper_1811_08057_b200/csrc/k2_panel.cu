@@ -236,6 +236,68 @@ __global__ void __launch_bounds__(kThreads, 1) kp_panel_kernel(const KPParams p)
     if (tid < kB) s_wit0[tid] = p.wit[p.row0 + tid];
     if (g == 0 && tid == 0) p.pan->n_moved = 0;
     __syncthreads();
+    if (p.r1_g0) {
+        // ---- the pair's first panel applied to these rows (replaces the gather + GEMM
+        //      launches): NL = -A[rows, P0] (staged in sTi's storage), the moved columns,
+        //      then S += NL * W0 with the GEMM's k order (bitwise the DMMA update)
+        const K2Gather* g0 = p.r1_g0;
+        for (int e = tid; e < kB * kB; e += kThreads) {
+            const int r = e >> 6, k = e & 63;
+            sTi[r][k] = -__ldcg(p.ws + (int64_t)(p.row0 + r) * p.ld + __ldg(&g0->P[k]));
+        }
+        const int nm = __ldg(&g0->n_moved);
+        for (int e = tid; e < kB * nm; e += kThreads) {
+            const int r = e / nm, j = e - r * nm;
+            const int c = __ldg(&g0->moved_c[j]);
+            if (c >= lo && c < lo + wc)
+                S[r * cw + (c - lo)] = __ldcg(p.ws + (int64_t)(p.row0 + r) * p.ld + __ldg(&g0->moved_src[j]));
+        }
+        __syncthreads();
+        const double* W0 = p.r1_W + lo;
+        for (int tb = warp; tb < kB / 4; tb += kThreads / 32) {
+            for (int c0 = 0; c0 < wc; c0 += 128) {
+                double acc[4][4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk) {
+                        const int c = c0 + lane + 32 * kk;
+                        acc[i][kk] = (c < wc) ? S[(4 * tb + i) * cw + c] : 0.0;
+                    }
+                for (int k0 = 0; k0 < kB; k0 += 8) {  // 32 W loads in flight per thread
+                    double w[8][4];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u)
+#pragma unroll
+                        for (int kk = 0; kk < 4; ++kk) {
+                            const int c = c0 + lane + 32 * kk;
+                            w[u][kk] = (c < wc) ? __ldg(W0 + (int64_t)(k0 + u) * p.r1_ldw + c) : 0.0;
+                        }
+#pragma unroll
+                    for (int u = 0; u < 8; ++u)
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+                            const double a = sTi[4 * tb + i][k0 + u];
+#pragma unroll
+                            for (int kk = 0; kk < 4; ++kk) acc[i][kk] = fma(a, w[u][kk], acc[i][kk]);
+                        }
+                }
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk) {
+                        const int c = c0 + lane + 32 * kk;
+                        if (c < wc) S[(4 * tb + i) * cw + c] = acc[i][kk];
+                    }
+            }
+        }
+        __syncthreads();
+        for (int e = tid; e < kB * (kB + 1); e += kThreads) {
+            const int t = e / (kB + 1), j = e - t * (kB + 1);
+            sTi[t][j] = (t == j) ? 1.0 : 0.0;
+        }
+        __syncthreads();
+    }
     {
         const int r = tid / kTPR, j = tid % kTPR;  // 64 rows x kTPR threads
         const unsigned hm = ((1u << kTPR) - 1u) << (lane & (32 - kTPR));

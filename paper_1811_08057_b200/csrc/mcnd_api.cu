@@ -884,6 +884,7 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
     const bool overlap = pairs && env_long("MCND_K2_OVERLAP", 1) != 0;
     const bool fuse_lc = env_long("MCND_K2_FUSE_LC", 1) != 0;
     const bool fuse_pp = env_long("MCND_K2_FUSE_PP", 1) != 0;
+    const bool fuse_r1 = env_long("MCND_K2_FUSE_R1", 1) != 0;
     const int64_t min_budget = env_long("MCND_K2_MIN_BUDGET", B->sms / 4);
     bool side_pending = false;
     cudaStream_t side = B->side;
@@ -914,16 +915,21 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
         if (pairs && k + 1 < n_panels) {
             e = run_kp(kb, gp0, Wq);
             mark("kp1");
-            if (e == cudaSuccess) e = k2_gather_fix(ws, ld, (int32_t)(kb + b), (int32_t)b, 64, gp0, Lq, abort, st);
-            mark("r1_gather");
-            if (e == cudaSuccess)
-                e = k2_gemm(ws, ld, (int32_t)(kb + b), (int32_t)b, (int32_t)(m - b), 64, Lq, 64, Wq, ld, wit, abort, st);
-            mark("r1_gemm");
+            if (!fuse_r1) {
+                if (e == cudaSuccess) e = k2_gather_fix(ws, ld, (int32_t)(kb + b), (int32_t)b, 64, gp0, Lq, abort, st);
+                mark("r1_gather");
+                if (e == cudaSuccess)
+                    e = k2_gemm(ws, ld, (int32_t)(kb + b), (int32_t)b, (int32_t)(m - b), 64, Lq, 64, Wq, ld, wit, abort, st);
+                mark("r1_gemm");
+            } else {  // the second panel kernel applies the first panel to its rows itself
+                kp.r1_g0 = gp0; kp.r1_W = Wq; kp.r1_ldw = ld;
+            }
             if (fuse_pp) {  // the second panel kernel runs the pair prep in its CTA 0
                 kp.pp_g0 = gp0; kp.pp_W = Wq; kp.pp_ldw = ld; kp.pp_Wp = Wp; kp.pp_gpair = gpair; kp.pp_m = (int32_t)m;
             }
             if (e == cudaSuccess) e = run_kp(kb + b, gp1, Wq + b * ld);
             kp.pp_g0 = nullptr;
+            kp.r1_g0 = nullptr;
             mark("kp2");
             if (e == cudaSuccess && !fuse_pp) e = k2_pair_prep(gp0, gp1, (int32_t)m, Wq, ld, Wp, gpair, abort, st);
             if (!fuse_pp) mark("pair_prep");
@@ -978,7 +984,7 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
                 side_pending = (e == cudaSuccess);
                 n_launch += 3;
             }
-            n_launch += (fuse_pp ? 7 : 8) - (fuse_lc ? 1 : 0);  // 2 panels, gather, update, [prep], gather, [L corr], trailing
+            n_launch += (fuse_pp ? 7 : 8) - (fuse_lc ? 1 : 0) - (fuse_r1 ? 2 : 0);  // 2 panels, [gather, update], [prep], gather, [L corr], trailing
             k += 2;
             par ^= 1;
         } else {
@@ -1268,11 +1274,10 @@ int mg_pair(MgHandle* h, int64_t lr0, int64_t t, int64_t m, double* W, int64_t l
     double* L = h->L;
     KPParams kp = mg_kp(h, lr0, t, m, gp0, W, ldw);
     cudaError_t e = kp_launch(kp, st);
-    if (e == cudaSuccess) e = k2_gather_fix(h->ws, h->ld, (int32_t)(lr0 + b), (int32_t)b, 64, gp0, L, h->abort, st);
-    if (e == cudaSuccess)
-        e = k2_gemm(h->ws, h->ld, (int32_t)(lr0 + b), (int32_t)b, (int32_t)(m - b), 64, L, 64, W, ldw, h->wit, h->abort, st);
+    (void)L;
     if (e == cudaSuccess) {
         KPParams kp1 = mg_kp(h, lr0 + b, t + b, m - b, gp1, W + b * ldw, ldw);
+        kp1.r1_g0 = gp0; kp1.r1_W = W; kp1.r1_ldw = ldw;  // + the first panel's update of these rows
         kp1.pp_g0 = gp0; kp1.pp_W = W; kp1.pp_ldw = ldw; kp1.pp_Wp = Wp; kp1.pp_gpair = gpair; kp1.pp_m = (int32_t)m;
         e = kp_launch(kp1, st);  // + the pair prep in its CTA 0
     }

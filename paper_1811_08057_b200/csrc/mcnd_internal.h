@@ -117,6 +117,12 @@ struct KPParams {
     double* pp_Wp;
     K2Gather* pp_gpair;
     int32_t pp_m;             // active width at the first panel of the pair
+    // second panel of a pair: the first panel's update of these 64 rows is applied in
+    // the prologue (gather of -A[rows, P0], moved columns, rank-64 FMA update) instead
+    // of by separate gather + GEMM launches
+    const K2Gather* r1_g0;    // the first panel's descriptor (nullptr: rows already updated)
+    const double* r1_W;       // its W (64 rows, row stride r1_ldw)
+    int64_t r1_ldw;
 };
 constexpr int kKPMaxG = 160;
 constexpr int kKPClusterMax = 16;

@@ -285,7 +285,7 @@ class BlockedGroup:
 
         if pairs and pairs[0][0] == rank:
             launch_pair(0)
-            nl += 4
+            nl += 2
         for q, (o, lr0, t, m, _) in enumerate(pairs):
             W, Wp, gp = self.W[q & 1], self.Wp[q & 1], self.gp[q & 1]
             ldw = ldw_of(m)
@@ -332,14 +332,14 @@ class BlockedGroup:
                 trailing(r0 + 128, rows_r - 128, m, W, ldw, Wp, gp, q, True)
                 ev_side.record(side)
                 side_pending = True
-                nl += 4 + 4
+                nl += 2 + 4
             else:
                 if rows_r > 0:
                     trailing(r0, rows_r, m, W, ldw, Wp, gp, q, False)
                     nl += 2
                 if nxt == rank:
                     launch_pair(q + 1)
-                    nl += 4
+                    nl += 2
             ev_trc[q & 1].record(crit)
             ev_trs[q & 1].record(side)
         crit.wait_stream(side)
