@@ -92,30 +92,38 @@ struct Smem {
 };
 
 // Whole-CTA reduction of (argmax value, column) and witness max.  Every thread
-// returns the CTA result.
+// returns the CTA result.  Exact: |x| compared as its 64-bit pattern (redux.sync
+// on the high then the low word), ties -> lowest column, as beats() orders them.
+__device__ __forceinline__ unsigned long long abs_bits(double x) {
+    return (unsigned long long)__double_as_longlong(x) & 0x7fffffffffffffffull;
+}
+__device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v) {
+    const unsigned hi = (unsigned)(v >> 32), lo = (unsigned)v;
+    const unsigned mh = __reduce_max_sync(kFull, hi);
+    const unsigned ml = __reduce_max_sync(kFull, hi == mh ? lo : 0u);
+    return ((unsigned long long)mh << 32) | ml;
+}
+__device__ __forceinline__ void warp_argmax(double& v, int& i, unsigned long long& w) {
+    const unsigned long long kb = abs_bits(v);
+    const unsigned long long mb = warp_max_u64(kb);
+    const unsigned wi = __reduce_min_sync(kFull, kb == mb ? (unsigned)i : 0xffffffffu);
+    const int src = __ffs(__ballot_sync(kFull, kb == mb && (unsigned)i == wi)) - 1;
+    v = __shfl_sync(kFull, v, src);
+    i = __shfl_sync(kFull, i, src);
+    w = warp_max_u64(w);
+}
 __device__ __forceinline__ void cta_reduce(Smem& sm, double& v, int& i, double& w) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-        double ov = __shfl_xor_sync(kFull, v, o);
-        int oi = __shfl_xor_sync(kFull, i, o);
-        double ow = __shfl_xor_sync(kFull, w, o);
-        if (beats(ov, oi, v, i)) { v = ov; i = oi; }
-        w = fmax(w, ow);
-    }
-    if (lane == 0) { sm.red_v[warp] = v; sm.red_i[warp] = i; sm.red_w[warp] = w; }
+    unsigned long long wb = abs_bits(w);
+    warp_argmax(v, i, wb);
+    if (lane == 0) { sm.red_v[warp] = v; sm.red_i[warp] = i; sm.red_w[warp] = __longlong_as_double((long long)wb); }
     __syncthreads();
     if (warp == 0) {
-        v = sm.red_v[lane]; i = sm.red_i[lane]; w = sm.red_w[lane];
-#pragma unroll
-        for (int o = 16; o; o >>= 1) {
-            double ov = __shfl_xor_sync(kFull, v, o);
-            int oi = __shfl_xor_sync(kFull, i, o);
-            double ow = __shfl_xor_sync(kFull, w, o);
-            if (beats(ov, oi, v, i)) { v = ov; i = oi; }
-            w = fmax(w, ow);
-        }
-        if (lane == 0) { sm.red_v[kWarps] = v; sm.red_i[kWarps] = i; sm.red_w[kWarps] = w; }
+        v = lane < kWarps ? sm.red_v[lane] : 0.0;
+        i = lane < kWarps ? sm.red_i[lane] : INT_MAX;
+        wb = lane < kWarps ? abs_bits(sm.red_w[lane]) : 0ull;
+        warp_argmax(v, i, wb);
+        if (lane == 0) { sm.red_v[kWarps] = v; sm.red_i[kWarps] = i; sm.red_w[kWarps] = __longlong_as_double((long long)wb); }
     }
     __syncthreads();
     v = sm.red_v[kWarps]; i = sm.red_i[kWarps]; w = sm.red_w[kWarps];
@@ -146,7 +154,9 @@ __device__ void publish(const K1Params& p, Smem& sm, int g, int row, int t, int 
             p.rec[h][t].v = v;
             p.rec[h][t].l = singular ? -1 : l;
         }
-        if (sys) __threadfence_system(); else __threadfence();
+        // single GPU: the gpu-scope release is cumulative over the CTA's row stores
+        // (ordered before it by the barrier), no separate fence needed
+        if (sys) __threadfence_system();
         for (int h = 0; h < p.n_groups; ++h) st_release_flag(&p.rec[h][t].flag, p.epoch, sys);
     }
 }
