@@ -61,6 +61,10 @@ __device__ __forceinline__ unsigned long long globaltimer() {
     return t;
 }
 
+#ifndef K1_POLL_SLEEP
+#define K1_POLL_SLEEP 32  // ns between flag polls
+#endif
+
 template <bool kFast>
 __device__ __forceinline__ double upd(double x, double mult, double p) {
     if (kFast) return fma(-mult, p, x);
@@ -261,7 +265,7 @@ __global__ void __launch_bounds__(kThreads, 1) k1_condense(const K1Params p) {
                     atomicExch(&p.err->err_step, (unsigned)s);
                     break;
                 }
-                __nanosleep(32);
+                if (K1_POLL_SLEEP) __nanosleep(K1_POLL_SLEEP);
             }
             sm.step_l = l;
         }
