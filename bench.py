@@ -304,6 +304,9 @@ def run_single(args):
                 "peak_kind": "measured here (cuBLAS DGEMM, FP64 DMMA)", "unit": "TFLOP/s",
                 "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic_from_profiles(args.config + "_blocked"),
                 "algorithmic_flops_per_launch": flops(n)}
+        chain = panel_chain(mc, d, args.fast)
+        if chain:
+            roof["panel_chain"] = chain
     else:
         B = algorithmic_bytes(n)
         achieved = B / (kms * 1e-3) / 1e9
@@ -358,6 +361,27 @@ def run_single(args):
     if not args.no_cpu_baseline and a is not None:
         line["cpu_baseline"] = cpu_baseline(a, args.cpu_seconds)
     print(json.dumps(line), flush=True)
+
+
+def panel_chain(mc, d, fast):
+    """In-kernel time of the panel kernels of one blocked call (device globaltimer
+    spans logged by the panel kernel's CTA 0): the latency-bound pivot chain that
+    bounds the blocked path at moderate N, as a share of the call."""
+    import ctypes
+
+    lib = mc._lib.load()
+    if not hasattr(lib, "mcnd_debug_kp_spans"):
+        return None
+    buf = np.zeros((4096, 2), dtype=np.uint64)
+    lib.mcnd_debug_kp_spans(ctypes.c_void_p(buf.ctypes.data), 4096)  # reset
+    r = mc.logdet_blocked(d, fast=fast, return_pivots=True)
+    k = lib.mcnd_debug_kp_spans(ctypes.c_void_p(buf.ctypes.data), 4096)
+    if k <= 0:
+        return None
+    sp = buf[:k].astype(np.int64)
+    kp_ms = float((sp[:, 1] - sp[:, 0]).sum()) / 1e6
+    return {"panels": int(k), "panel_kernel_ms": kp_ms, "call_ms": r[3], "share": kp_ms / r[3],
+            "pivots": int(k) * 64, "us_per_pivot": 1e3 * kp_ms / (int(k) * 64)}
 
 
 def check_parity(cfg, res, fast):
