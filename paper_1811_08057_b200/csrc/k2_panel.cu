@@ -331,6 +331,12 @@ __global__ void __launch_bounds__(kThreads, 1) kp_panel_kernel(const KPParams p)
     }
 
     KP_MARK(0, 9);
+    // E's per-lane running maxima of its rows (row ew + 14k in slot k), kept across steps
+    constexpr int kEWarps = (kThreads - 64) / 32;                  // bulk warps
+    constexpr int kERows = (kB + kEWarps - 1) / kEWarps;          // rows per bulk warp
+    unsigned long long emax[kERows];
+#pragma unroll
+    for (int k = 0; k < kERows; ++k) emax[k] = 0ull;
     for (int s = 0; s < kB; ++s) {
         const int ms = m - s;  // active width before pivot s
         const unsigned tag = p.tag0 + (unsigned)s;
@@ -569,28 +575,26 @@ __global__ void __launch_bounds__(kThreads, 1) kp_panel_kernel(const KPParams p)
             PUT(COL(s + 1, g, r), pack(xc, tag1, 0));
             if (r > s + 1) s_rmax2[r] = fmax(s_rmax2[r], mx);
         } else {
-            // ---- E. bulk (the other warps): rows > s+1, all columns except pc / lc, with
-            //         the reference's two roundings (condense.py:118).  Work units are
-            //         (row, 256-column segment) per warp, each lane two adjacent columns per
-            //         16-byte access; the segment's max is two redux ops + one shared
-            //         atomicMax.  Only the (rare) units holding pc or lc take the checked path.
-            constexpr int kSeg = 256;
-            const int nseg = (wn + kSeg - 1) / kSeg;
-            const int units = (kB - 2 - s) * nseg;
-            constexpr int kBulkWarps = (kThreads - kLA) / 32;
-            for (int u = warp - kLA / 32; u < units; u += kBulkWarps) {
-                const int q = u / nseg;
-                const int r = s + 2 + q;
-                const int c0 = (u - q * nseg) * kSeg;
-                const int c1 = min(wn, c0 + kSeg);
+            // ---- E. bulk (warps 2..15): rows > s+1, all columns except pc / lc, with the
+            //         reference's two roundings (condense.py:118).  Row r belongs to warp
+            //         2 + (r mod 14) for the whole panel, so each lane keeps its running
+            //         |.| maximum of the row in a register across steps; the warp folds it
+            //         into s_rmax once, at the step after which the row is next (D1 reads
+            //         it) -- no per-step reductions or shared atomics.  Each lane does two
+            //         adjacent columns per 16-byte access (cw <= 256: one pass of 4).
+            const int ew = warp - kLA / 32;  // 0..13
+            const bool chk = pc >= 0 || lc >= 0;
+#pragma unroll
+            for (int k = 0; k < kERows; ++k) {
+                const int r = ew + kEWarps * k;
+                if (r < s + 2 || r >= kB) continue;  // warp-uniform
                 const double mu = s_mult[r];
                 double* row = S + r * cw;
-                unsigned long long mb = 0ull;
-                const bool chk = (pc >= c0 && pc < c1) || (lc >= c0 && lc < c1);
+                unsigned long long mb = emax[k];
 #pragma unroll
-                for (int k = 0; k < kSeg / 64; ++k) {
-                    const int c = c0 + 64 * k + 2 * lane;
-                    if (c < c1) {
+                for (int j = 0; j < 4; ++j) {
+                    const int c = 64 * j + 2 * lane;
+                    if (c < wn) {
                         const double2 x = *reinterpret_cast<const double2*>(row + c);
                         const double2 pv = *reinterpret_cast<const double2*>(us + c);
                         double2 y;
@@ -598,17 +602,29 @@ __global__ void __launch_bounds__(kThreads, 1) kp_panel_kernel(const KPParams p)
                         y.y = __dsub_rn(x.y, __dmul_rn(mu, pv.y));  // c+1 may be a dropped column: harmless
                         if (!chk) {
                             *reinterpret_cast<double2*>(row + c) = y;
-                            mb = max(mb, max(abs_bits(y.x), c + 1 < c1 ? abs_bits(y.y) : 0ull));
+                            mb = max(mb, max(abs_bits(y.x), c + 1 < wn ? abs_bits(y.y) : 0ull));
                         } else {
                             // pc / lc belong to D2, which is updating them right now: never write
                             // them back (not even unchanged), element-wise stores only
                             if (c != pc && c != lc) { row[c] = y.x; mb = max(mb, abs_bits(y.x)); }
-                            if (c + 1 < c1 && c + 1 != pc && c + 1 != lc) { row[c + 1] = y.y; mb = max(mb, abs_bits(y.y)); }
+                            if (c + 1 < wn && c + 1 != pc && c + 1 != lc) { row[c + 1] = y.y; mb = max(mb, abs_bits(y.y)); }
                         }
                     }
                 }
-                mb = warp_max_u64(mb);
-                if (lane == 0) atomicMax(reinterpret_cast<unsigned long long*>(s_rmax) + r, mb);
+                emax[k] = mb;
+            }
+            // row s+2 is D1's row at the next step: fold its lane maxima now
+            const int rn = s + 2;
+            if (rn < kB && rn % kEWarps == ew) {
+                unsigned long long v = 0ull;
+#pragma unroll
+                for (int k = 0; k < kERows; ++k)
+                    if (ew + kEWarps * k == rn) v = emax[k];
+                v = warp_max_u64(v);
+                if (lane == 0) {
+                    unsigned long long* sr = reinterpret_cast<unsigned long long*>(s_rmax) + rn;
+                    *sr = max(*sr, v);
+                }
             }
         }
         KP_MARK(s, 4);
