@@ -96,18 +96,38 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled DURING the timed region."""
+    """SM clocks and throttle reasons sampled DURING the timed region: NVML polled
+    every 2 ms from a thread (short regions such as C4's still get samples); falls
+    back to `nvidia-smi -lms 100` without NVML."""
 
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
 
     def __init__(self, gpu_index: int):
         self.gpu = gpu_index
         self.proc = None
         self.lines = []
+        self.samples = []  # (sm_mhz, max_mhz, reasons)
+        self._stop = threading.Event()
+        self._nvml = None
 
     def __enter__(self):
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+            self._nvml = pynvml
+            self._t = threading.Thread(target=self._poll_nvml, daemon=True)
+            self._t.start()
+            t0 = time.perf_counter()
+            while not self.samples and time.perf_counter() - t0 < 0.2:  # poller running
+                time.sleep(0.0005)
+            return self
+        except Exception:
+            self._nvml = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
@@ -118,11 +138,30 @@ class ClockSampler:
             self.proc = None
         return self
 
+    def _poll_nvml(self):
+        nv = self._nvml
+        bits = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20, "sw_power_cap": 0x4}
+        mx = nv.nvmlDeviceGetMaxClockInfo(self._h, nv.NVML_CLOCK_SM)
+        while not self._stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h) if hasattr(
+                    nv, "nvmlDeviceGetCurrentClocksEventReasons") else nv.nvmlDeviceGetCurrentClocksThrottleReasons(self._h)
+                self.samples.append((float(sm), float(mx), {k for k, b in bits.items() if rs & b}))
+            except Exception:
+                pass
+            self._stop.wait(0.002)
+
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
     def __exit__(self, *exc):
+        if self._nvml is not None:  # one last sample right at the end of the region
+            time.sleep(0.003)
+        self._stop.set()
+        if self._nvml is not None:
+            self._t.join(timeout=1)
         if self.proc:
             self.proc.terminate()
             try:
@@ -132,7 +171,10 @@ class ClockSampler:
 
     def summary(self):
         sm, mx, reasons = [], 0.0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for (c, m, r) in self.samples:
+            sm.append(c)
+            mx = max(mx, m)
+            reasons |= r
         for ln in self.lines:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 9:
@@ -142,13 +184,13 @@ class ClockSampler:
                 mx = max(mx, float(parts[2]))
             except ValueError:
                 continue
-            for nm, v in zip(names, parts[5:9]):
+            for nm, v in zip(self.NAMES, parts[5:9]):
                 if v.lower().startswith("active"):
                     reasons.add(nm)
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "source": "nvml" if self.samples else "nvidia-smi"}
 
 
 def cpu_baseline(a: np.ndarray, budget_s: float):
