@@ -88,7 +88,7 @@ __device__ __forceinline__ bool rec_ok(double2 r, unsigned tag, unsigned* torn) 
 #define KP_LDMODE 0  // microbenchmark knob: 0 relaxed.gpu, 1 __ldcg/__stcg, 2 asm volatile .cg
 #endif
 __device__ __forceinline__ void put(double2* p, double2 v) {
-#if KP_LDMODE == 1
+#if KP_LDMODE == 1 || KP_LDMODE == 3  // 3: weak L2 stores, relaxed polling loads
     __stcg(p, v);
 #elif KP_LDMODE == 2
     asm volatile("st.global.cg.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");

@@ -763,6 +763,9 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
     CUDA_TRY(cudaMemcpyAsync(base + o_int, hi, n_int * sizeof(int32_t), cudaMemcpyHostToDevice, st));
     CUDA_TRY(cudaMemsetAsync(base + o_rec, 0, (size_t)n * sizeof(PivRec), st));
     CUDA_TRY(cudaMemsetAsync(base + o_ctl, 0, sizeof(K1Err) + 16, st));
+    // the panel kernels' record slots: cleared per call, so a record's tag only has to
+    // be unique within the call (its global step + 1)
+    CUDA_TRY(cudaMemsetAsync(base + o_cand, 0, o_lastb + (size_t)64 * 64 * sizeof(double2) - o_cand, st));
     const int32_t* d_int = (const int32_t*)(base + o_int);
     const int32_t* d_iota = d_int;
     const int32_t* d_never = d_iota + n;
@@ -866,7 +869,7 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
         kp.rec = recs + kb;
         kp.pan = gp;
         kp.W = Wout;
-        kp.tag0 = (epoch << 16) ^ (uint32_t)(kb + 1);  // kb + s + 1 < 2^16 for n <= 65472
+        kp.tag0 = (uint32_t)(kb + 1);  // global step + 1: unique within the call (slots cleared per call)
         return kp_launch(kp, st);
     };
     // Panels go in pairs: panel k, then its update of panel k+1's 64 rows, panel
@@ -1193,6 +1196,7 @@ int mg_load(MgHandle* h, const double* src, int64_t lds, cudaStream_t st) {
     h->epoch = h->epoch + 1 + (h->epoch + 1 == 0 ? 1 : 0);
     CUDA_TRY(cudaMemsetAsync(h->recs, 0, (size_t)h->n * sizeof(PivRec), st));
     CUDA_TRY(cudaMemsetAsync(h->err, 0, sizeof(K1Err) + 16, st));
+    CUDA_TRY(cudaMemsetAsync(h->cand, 0, (size_t)((char*)(h->lastb + 64 * 64) - (char*)h->cand), st));
     if (h->lr == 0) return MCND_OK;
     const int64_t ni = std::max<int64_t>(h->n, h->lr);
     K1Params p{};
@@ -1242,7 +1246,7 @@ KPParams mg_kp(MgHandle* h, int64_t lr0, int64_t t, int64_t m, K2Gather* gp, dou
     kp.wit = h->wit;
     kp.rec = h->recs + t;
     kp.epoch = h->epoch;
-    kp.tag0 = (h->epoch << 16) ^ (uint32_t)(t + 1);
+    kp.tag0 = (uint32_t)(t + 1);  // slots cleared by mg_load
     kp.W = W;
     kp.ldw = ldw;
     kp.pan = gp;

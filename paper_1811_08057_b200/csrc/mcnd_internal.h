@@ -98,7 +98,7 @@ struct KPParams {
     const double* wit;        // running witnesses, global row index
     PivRec* rec;              // this panel's 64 pivot records
     uint32_t epoch;
-    uint32_t tag0;            // record tag of step s is tag0 + s (unique per call and panel)
+    uint32_t tag0;            // record tag of step s is tag0 + s (the global step + 1; slots cleared per call)
     double* W;                // out: T^{-1} U, 64 x (m - 64), row stride ldw
     int64_t ldw;
     K2Gather* pan;            // out: panel-start pivot columns (P[0..63]), moved columns
