@@ -421,3 +421,18 @@ def test_blocked_odd_sizes_vs_cusolver(mc, n):
     got = mc.logdet_blocked(a)
     assert got.sign == int(s_ref.item())
     assert abs(got.log_abs - float(l_ref)) <= tol(n, float(l_ref))
+
+
+@pytest.mark.parametrize("dup_row", [5, 1500, 2990])
+def test_blocked_singular_mid_panel_and_tail(mc, dup_row):
+    """A row duplicated at a position handled by a panel early, mid-matrix, or in the
+    K1 tail: SINGULAR (condense.py:90 / 153-158), every later launch aborted, no hang;
+    the same handle (workspace) then serves a regular matrix."""
+    n = 3000
+    a = np.random.default_rng(dup_row).uniform(-1, 1, (n, n))
+    a[dup_row] = a[dup_row // 2]
+    assert mc.logdet_blocked(a) == mc.SINGULAR
+    b = np.random.default_rng(1).uniform(-1, 1, (n, n))
+    got = mc.logdet_blocked(b)
+    ref = mc.logdet_condensation(b)
+    assert got.sign == ref.sign and abs(got.log_abs - ref.log_abs) <= tol(n, ref.log_abs)
