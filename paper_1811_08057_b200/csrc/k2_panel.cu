@@ -373,9 +373,13 @@ __global__ void __launch_bounds__(kThreads, 1) kp_panel_kernel(const KPParams p)
                     {
                         const unsigned nb = __ballot_sync(kFull, need != 0);
                         if (lane == (int)(__ffs(nb) - 1) && atomicCAS(&p.err->dbg[0], 0u, 1u) == 0u) {
-                            int k = __ffs(need) - 1;
+                            const int k = __ffs(need) - 1;
+                            unsigned t4 = 0u, t5 = 0u;  // static indexing only: keeps c/w in registers
+#pragma unroll
+                            for (int kk = 0; kk < kPer; ++kk)
+                                if (kk == k) { t4 = tag_of(c[kk]); t5 = tag_of(w[kk]); }
                             p.err->dbg[1] = (unsigned)g; p.err->dbg[2] = (unsigned)s; p.err->dbg[3] = (unsigned)(lane + 32 * k);
-                            p.err->dbg[4] = tag_of(c[k]); p.err->dbg[5] = tag_of(w[k]); p.err->dbg[6] = tag;
+                            p.err->dbg[4] = t4; p.err->dbg[5] = t5; p.err->dbg[6] = tag;
                             p.err->dbg[7] = (unsigned)G;
                         }
                     }

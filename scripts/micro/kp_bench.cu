@@ -32,6 +32,18 @@ int main(int argc, char** argv) {
     p.W = W; p.ldw = ld; p.pan = pan; p.abort = abort; p.cand = cand; p.wrec = wrec; p.colbuf = colb; p.lastbuf = lastb;
     p.err = err; p.timeout_ns = 5000000000ull; p.cluster = cl;
     if (cl) printf("cluster fits: %d\n", kp_cluster_fits(G, cw));
+    if (argc > 4 && atoi(argv[4])) {  // second panel of a pair: the r1 prologue (rank-64 update of the rows)
+        K2Gather hg{};
+        for (int k = 0; k < 64; ++k) hg.P[k] = k;
+        hg.n_moved = 0;
+        K2Gather* dg; cudaMalloc(&dg, sizeof(K2Gather)); cudaMemcpy(dg, &hg, sizeof(hg), cudaMemcpyHostToDevice);
+        double* W0; cudaMalloc(&W0, (size_t)64 * ld * 8);
+        std::vector<double> hw((size_t)64 * ld);
+        for (auto& x : hw) x = 1e-3 * U(rng);
+        cudaMemcpy(W0, hw.data(), hw.size() * 8, cudaMemcpyHostToDevice);
+        p.r1_g0 = dg; p.r1_W = W0; p.r1_ldw = ld;
+        printf("with the r1 prologue\n");
+    }
     for (int it = 0; it < 3; ++it) {
         cudaMemcpy(ws, h.data(), h.size() * 8, cudaMemcpyHostToDevice);
         p.tag0 = (unsigned)(1000 + it * 100);
