@@ -1275,10 +1275,8 @@ int mg_pair(MgHandle* h, int64_t lr0, int64_t t, int64_t m, double* W, int64_t l
                     (long long)t);
     K2Gather* gp0 = h->gp;
     K2Gather* gp1 = h->gp + 1;
-    double* L = h->L;
     KPParams kp = mg_kp(h, lr0, t, m, gp0, W, ldw);
     cudaError_t e = kp_launch(kp, st);
-    (void)L;
     if (e == cudaSuccess) {
         KPParams kp1 = mg_kp(h, lr0 + b, t + b, m - b, gp1, W + b * ldw, ldw);
         kp1.r1_g0 = gp0; kp1.r1_W = W; kp1.r1_ldw = ldw;  // + the first panel's update of these rows
