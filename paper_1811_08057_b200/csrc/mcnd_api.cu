@@ -727,8 +727,8 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
     const size_t o_rec = take((size_t)n * sizeof(PivRec));
     const size_t o_L = take((size_t)2 * std::max<int64_t>(n, 1) * 2 * b * sizeof(double));  // x2: by pair parity
     const size_t o_W = take((size_t)2 * 2 * b * ld * sizeof(double));
-    const size_t o_pan = take(3 * sizeof(K2Gather));
-    const size_t o_Wp = take((size_t)b * b * sizeof(double));
+    const size_t o_pan = take(4 * sizeof(K2Gather));           // gp0, gp1, gpair x2 (pair parity)
+    const size_t o_Wp = take((size_t)2 * b * b * sizeof(double));  // x2 (pair parity)
     const size_t o_cand = take((size_t)64 * kKPMaxG * sizeof(double2));
     const size_t o_wrec = take((size_t)64 * kKPMaxG * sizeof(double2));
     const size_t o_colb = take((size_t)64 * kKPMaxG * 64 * sizeof(double2));
@@ -781,8 +781,8 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
     double* Wb = (double*)(base + o_W);
     K2Gather* gp0 = (K2Gather*)(base + o_pan);
     K2Gather* gp1 = gp0 + 1;
-    K2Gather* gpair = gp0 + 2;
-    double* Wp = (double*)(base + o_Wp);
+    K2Gather* const gpair2 = gp0 + 2;  // by pair parity, like L and W: the side stream of
+    double* const Wp2 = (double*)(base + o_Wp);  // pair q may still gather while pair q+1 preps
     K1Err* err = (K1Err*)(base + o_ctl);
     unsigned* abort = (unsigned*)(base + o_ctl + sizeof(K1Err));
     const uint32_t epoch = ++B->epoch;
@@ -889,6 +889,7 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
     const bool fuse_pp = env_long("MCND_K2_FUSE_PP", 1) != 0;
     const bool fuse_r1 = env_long("MCND_K2_FUSE_R1", 1) != 0;
     const int64_t min_budget = env_long("MCND_K2_MIN_BUDGET", B->sms / 4);
+    const bool side_after = env_long("MCND_K2_SIDE_AFTER", 1) != 0;
     bool side_pending = false;
     cudaStream_t side = B->side;
     auto join_side = [&]() -> cudaError_t {
@@ -915,6 +916,8 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
         const int64_t kb = k * b, m = n - kb;
         double* const Wq = Wb + (size_t)par * 2 * b * ld;
         double* const Lq = Lb + (size_t)par * std::max<int64_t>(n, 1) * 2 * b;
+        double* const Wp = Wp2 + (size_t)par * b * b;
+        K2Gather* const gpair = gpair2 + par;
         if (pairs && k + 1 < n_panels) {
             e = run_kp(kb, gp0, Wq);
             mark("kp1");
@@ -977,9 +980,12 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
                 if (ss == st) mark("trailing");
                 return ee;
             };
-            // side stream: W, Wp and the gather descriptor are final once pair prep is done
-            if (e == cudaSuccess && ahead < nr) e = cudaEventRecord(B->ev_a, st);
+            // side stream: W, Wp and the gather descriptor are final once pair prep is done;
+            // started only after the critical rows' update (MCND_K2_SIDE_AFTER=0: right away), so the side
+            // kernels do not take the SMs the critical ones need
+            if (e == cudaSuccess && ahead < nr && !side_after) e = cudaEventRecord(B->ev_a, st);
             if (e == cudaSuccess) e = trailing(0, ahead, st, 0);  // the critical rows first
+            if (e == cudaSuccess && ahead < nr && side_after) e = cudaEventRecord(B->ev_a, st);
             if (e == cudaSuccess && ahead < nr) {
                 e = cudaStreamWaitEvent(side, B->ev_a, 0);
                 if (e == cudaSuccess) e = trailing(ahead, nr - ahead, side, prio ? -1 : (int)budget);
