@@ -109,3 +109,34 @@ def read_matrix_device(path, device=None, chunk_bytes: int = 64 << 20, check_fin
     if check_finite and not bool(torch.isfinite(out).all()):
         raise ValueError("matrix entries must be finite (no NaN/Inf)")
     return out
+
+
+def write_matrix_csv(m, path) -> None:
+    """matrix.py:154-160: one row per line, comma-separated repr() floats, no header."""
+    a = as_matrix(m)
+    with open(path, "w") as f:
+        for row in a:
+            f.write(",".join(repr(float(v)) for v in row))
+            f.write("\n")
+
+
+def read_matrix_csv(path) -> np.ndarray:
+    """matrix.py:163-180: blank lines skipped; a bad token or a ragged row -> FormatError
+    naming the line."""
+    rows = []
+    with open(path) as f:
+        for line_no, line in enumerate(f, 1):
+            line = line.strip()
+            if not line:
+                continue
+            try:
+                rows.append([float(tok) for tok in line.split(",")])
+            except ValueError as exc:
+                raise FormatError(f"line {line_no}: {exc}") from exc
+    if not rows:
+        raise FormatError("empty CSV matrix")
+    width = len(rows[0])
+    for line_no, row in enumerate(rows, 1):
+        if len(row) != width:
+            raise FormatError(f"line {line_no}: ragged row width {len(row)} != {width}")
+    return as_matrix(rows)
