@@ -351,7 +351,7 @@ __global__ void __launch_bounds__(kThreads, 1) kp_panel_kernel(const KPParams p)
 #pragma unroll
             for (int k = 0; k < kPer; ++k)
                 if (lane + 32 * k < G) need |= 1u << k;
-            for (;;) {
+            for (unsigned it = 0;; ++it) {
 #pragma unroll
                 for (int k = 0; k < kPer; ++k)
                     if (need & (1u << k)) {
@@ -363,7 +363,7 @@ __global__ void __launch_bounds__(kThreads, 1) kp_panel_kernel(const KPParams p)
                     if ((need & (1u << k)) && rec_ok(c[k], tag, &p.err->pad) && rec_ok(w[k], tag, &p.err->pad))
                         need &= ~(1u << k);
                 if (__all_sync(kFull, need == 0)) break;
-                if (globaltimer() - t_start > p.timeout_ns) {
+                if ((it & 7u) == 7u && globaltimer() - t_start > p.timeout_ns) {
 #ifdef KP_DEBUG
                     for (int k = 0; k < kPer; ++k)
                         if (need & (1u << k))
@@ -514,14 +514,22 @@ __global__ void __launch_bounds__(kThreads, 1) kp_panel_kernel(const KPParams p)
                 if (lane == 0 && wi == INT_MAX) { s_lv[warp] = 0.0; s_li[warp] = INT_MAX; s_lm[warp] = 0.0; }
                 asm volatile("bar.sync 1, %0;" ::"n"(kD1));
                 KP_MARK(s, 5);
+                // the D1 warps' results combined by warp 0 (exact redux argmax, ties -> lowest column)
+                double v0 = 0.0, m0 = 0.0;
+                int i0 = INT_MAX;
+                if (warp == 0) {
+                    const bool has = lane < kD1 / 32;
+                    const double lv = has ? s_lv[lane] : 0.0, lm = has ? s_lm[lane] : 0.0;
+                    const int li = has ? s_li[lane] : INT_MAX;
+                    const unsigned long long kb = (li == INT_MAX) ? 0ull : abs_bits(lv);
+                    const unsigned long long mb = warp_max_u64(kb);
+                    i0 = (int)__reduce_min_sync(kFull, kb == mb ? (unsigned)li : 0xffffffffu);
+                    const int src = __ffs(__ballot_sync(kFull, kb == mb && li == i0)) - 1;
+                    v0 = __shfl_sync(kFull, lv, src < 0 ? 0 : src);
+                    if (i0 == INT_MAX) v0 = 0.0;
+                    m0 = __longlong_as_double((long long)warp_max_u64((unsigned long long)__double_as_longlong(lm)));
+                }
                 if (tid == 0) {
-                    double v0 = s_lv[0], m0 = s_lm[0];
-                    int i0 = s_li[0];
-#pragma unroll
-                    for (int k = 1; k < kD1 / 32; ++k) {
-                        if (beats(s_lv[k], s_li[k], v0, i0)) { v0 = s_lv[k]; i0 = s_li[k]; }
-                        m0 = fmax(m0, s_lm[k]);
-                    }
                     s_cv = v0;
                     s_cpos = i0;
                     const double rm = fmax(fmax(s_rmax[s + 1], s_rmax2[s + 1]), m0);
