@@ -268,6 +268,7 @@ class BlockedGroup:
         ev_trc = [torch.cuda.Event(), torch.cuda.Event()]  # crit / side users of W[q & 1] done
         ev_trs = [torch.cuda.Event(), torch.cuda.Event()]
         ev_side = torch.cuda.Event()
+        ev_crit = torch.cuda.Event()  # the next owner's critical rows updated (releases the side update)
         side_pending = False
 
         def ldw_of(m):
@@ -326,9 +327,11 @@ class BlockedGroup:
                 side_pending = False
             if nxt == rank and rows_r > 128:
                 trailing(r0, 128, m, W, ldw, Wp, gp, q, False)
+                ev_crit.record(crit)
                 launch_pair(q + 1)
-                if q >= 1:
-                    side.wait_event(ev_trc[(q - 1) & 1])  # its rows' previous update (crit)
+                # the side update is released only after the critical rows' update (its CTAs
+                # would otherwise take the SMs the critical kernels need; single-GPU schedule)
+                side.wait_event(ev_crit)
                 trailing(r0 + 128, rows_r - 128, m, W, ldw, Wp, gp, q, True)
                 ev_side.record(side)
                 side_pending = True
