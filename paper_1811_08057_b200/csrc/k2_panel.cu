@@ -593,7 +593,7 @@ __global__ void __launch_bounds__(kThreads, 1) kp_panel_kernel(const KPParams p)
             //         |.| maximum of the row in a register across steps; the warp folds it
             //         into s_rmax once, at the step after which the row is next (D1 reads
             //         it) -- no per-step reductions or shared atomics.  Each lane does two
-            //         adjacent columns per 16-byte access (cw <= 256: one pass of 4).
+            //         adjacent columns per 16-byte access (one unrolled pass of 4 covers 256).
             const int ew = warp - kLA / 32;  // 0..13
             const bool chk = pc >= 0 || lc >= 0;
 #pragma unroll
@@ -603,9 +603,7 @@ __global__ void __launch_bounds__(kThreads, 1) kp_panel_kernel(const KPParams p)
                 const double mu = s_mult[r];
                 double* row = S + r * cw;
                 unsigned long long mb = emax[k];
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const int c = 64 * j + 2 * lane;
+                auto seg = [&](int c) {  // two adjacent columns, one 16-byte access
                     if (c < wn) {
                         const double2 x = *reinterpret_cast<const double2*>(row + c);
                         const double2 pv = *reinterpret_cast<const double2*>(us + c);
@@ -622,7 +620,11 @@ __global__ void __launch_bounds__(kThreads, 1) kp_panel_kernel(const KPParams p)
                             if (c + 1 < wn && c + 1 != pc && c + 1 != lc) { row[c + 1] = y.y; mb = max(mb, abs_bits(y.y)); }
                         }
                     }
-                }
+                };
+#pragma unroll
+                for (int j = 0; j < 4; ++j) seg(64 * j + 2 * lane);
+#pragma unroll 1
+                for (int j = 4; 64 * j < wn; ++j) seg(64 * j + 2 * lane);  // chunks wider than 256 columns
                 emax[k] = mb;
             }
             // row s+2 is D1's row at the next step: fold its lane maxima now
@@ -753,6 +755,7 @@ int kp_cluster_fits(int G, int cw) {
 cudaError_t kp_launch(const KPParams& p, cudaStream_t s) {
     const bool cl = p.cluster != 0;
     const size_t smem = kp_smem_bytes(p.cw, cl);
+    if (p.cw < 2 || (p.cw & 1) || p.cw > kKPMaxCw || p.G < 1 || p.G > kKPMaxG) return cudaErrorInvalidValue;
     KPParams pc = p;
     if (cl) {
         cudaError_t e = cudaFuncSetAttribute(kp_panel_kernel<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

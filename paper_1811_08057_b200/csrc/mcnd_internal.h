@@ -125,6 +125,7 @@ struct KPParams {
     int64_t r1_ldw;
 };
 constexpr int kKPMaxG = 160;
+constexpr int kKPMaxCw = 380;  // columns per panel CTA (64 x 380 doubles = 190 KB of shared memory)
 constexpr int kKPClusterMax = 16;
 cudaError_t kp_launch(const KPParams& p, cudaStream_t s);
 size_t kp_smem_bytes(int cw, bool cluster);

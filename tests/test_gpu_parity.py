@@ -342,6 +342,23 @@ def test_blocked_cluster_transport_identical(mc, env_knob):
     assert np.array_equal(got[1], ref[1]) and np.array_equal(got[2], ref[2])
 
 
+@pytest.mark.parametrize("maxg", [6, 7])
+def test_blocked_wide_panel_chunks(mc, env_knob, maxg):
+    """Panel CTAs holding more than 256 columns (what N > 148 x 256 needs on one GPU,
+    forced here at N=2000 by capping the panel grid): the same pivots and log|det| as
+    the default chunking, within tolerance of the oracle."""
+    from oracle import mcnd_oracle as O
+
+    a = np.random.default_rng(33).uniform(-1, 1, (2000, 2000))
+    ref = mc.logdet_blocked(a, return_pivots=True)
+    env_knob("MCND_KP_MAXG", maxg)  # m=2000 -> ~300-334 columns per CTA
+    got = mc.logdet_blocked(a, return_pivots=True)
+    assert got[0] == ref[0]
+    assert np.array_equal(got[1], ref[1]) and np.array_equal(got[2], ref[2])
+    o = O.logdet_condensation(a)
+    assert got[0].sign == o.sign and abs(got[0].log_abs - o.log_abs) <= tol(2000, o.log_abs)
+
+
 @pytest.mark.parametrize("n", [4000, 8000])
 def test_blocked_lookahead_identical(mc, env_knob, n):
     """The look-ahead schedule (trailing update split over two streams, side GEMM
