@@ -720,7 +720,7 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
     if ((n + G0 - 1) / G0 > kK1MaxRowsPerCta) return fail(MCND_EINVAL, "n=%lld too large for one GPU", (long long)n);
     if (n > (int64_t)kKPMaxCw * std::min<int64_t>(B->sms, kKPMaxG))  // panel chunks must fit shared memory
         return fail(MCND_EINVAL, "n=%lld too large for the one-GPU blocked path (at most %d panel columns per SM); "
-                    "use the multi-GPU driver or logdet_condensation", (long long)n, kKPMaxCw);
+                    "use logdet_condensation (unblocked)", (long long)n, kKPMaxCw);
 
     // device layout
     size_t off = 0;
