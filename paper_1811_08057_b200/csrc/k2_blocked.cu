@@ -68,9 +68,10 @@ __global__ void __launch_bounds__(kGLThreads) k2_gather_lcorr_kernel(double* __r
                                                                      const unsigned* __restrict__ abort) {
     __shared__ double sWp[64 * 64];
     if (*(volatile const unsigned*)abort) return;
-    for (int e = threadIdx.x; e < 64 * 64; e += kGLThreads) sWp[e] = Wp[e];
-    __syncthreads();
     const int lane = threadIdx.x & 31;
+    const int stride = gridDim.x * (kGLThreads / 32);
+    int i = blockIdx.x * (kGLThreads / 32) + (threadIdx.x >> 5);
+    // the descriptor, Wp and this warp's first row are all requested before anything waits
     const int nm = gp->n_moved;
     int pk[4];
 #pragma unroll
@@ -79,35 +80,54 @@ __global__ void __launch_bounds__(kGLThreads) k2_gather_lcorr_kernel(double* __r
     const int mc1 = lane + 32 < nm ? gp->moved_c[lane + 32] : 0, ms1 = lane + 32 < nm ? gp->moved_src[lane + 32] : 0;
     const int mc2 = lane + 64 < nm ? gp->moved_c[lane + 64] : 0, ms2 = lane + 64 < nm ? gp->moved_src[lane + 64] : 0;
     const int mc3 = lane + 96 < nm ? gp->moved_c[lane + 96] : 0, ms3 = lane + 96 < nm ? gp->moved_src[lane + 96] : 0;
-    for (int i = blockIdx.x * (kGLThreads / 32) + (threadIdx.x >> 5); i < nrows; i += gridDim.x * (kGLThreads / 32)) {
-        double* row = ws + (int64_t)(rbase + i) * ld;
-        double x[4];
+    double x[4], v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
+    auto gather = [&](int r) {
+        const double* row = ws + (int64_t)(rbase + r) * ld;
 #pragma unroll
         for (int k = 0; k < 4; ++k) x[k] = row[pk[k]];
-        double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
-        if (lane < nm) v0 = row[ms0];
-        if (lane + 32 < nm) v1 = row[ms1];
-        if (lane + 64 < nm) v2 = row[ms2];
-        if (lane + 96 < nm) v3 = row[ms3];
+        v0 = lane < nm ? row[ms0] : 0.0;
+        v1 = lane + 32 < nm ? row[ms1] : 0.0;
+        v2 = lane + 64 < nm ? row[ms2] : 0.0;
+        v3 = lane + 96 < nm ? row[ms3] : 0.0;
+    };
+    if (i < nrows) gather(i);
+    {   // Wp staged with all 16 loads per thread in flight (one L2 round trip, not 16)
+        constexpr int kPer = 64 * 64 / kGLThreads;
+        double w[kPer];
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) w[u] = __ldg(Wp + threadIdx.x + kGLThreads * u);
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) sWp[threadIdx.x + kGLThreads * u] = w[u];
+    }
+    __syncthreads();
+    for (; i < nrows; i += stride) {
+        double* row = ws + (int64_t)(rbase + i) * ld;
         __syncwarp();
         if (lane < nm) row[mc0] = v0;
         if (lane + 32 < nm) row[mc1] = v1;
         if (lane + 64 < nm) row[mc2] = v2;
         if (lane + 96 < nm) row[mc3] = v3;
         const double n00 = -x[0], n01 = -x[1];
-        double n10 = -x[2], n11 = -x[3];
+        // four independent FMA chains per output (k even / odd of each half), summed at the end
+        double a10 = -x[2], a11 = -x[3], b10 = 0.0, b11 = 0.0, c10 = 0.0, c11 = 0.0, d10 = 0.0, d11 = 0.0;
 #pragma unroll 8
-        for (int k = 0; k < 32; ++k) {
-            const double a = __shfl_sync(0xffffffffu, n00, k);
-            n10 = fma(a, sWp[k * 64 + lane], n10);
-            n11 = fma(a, sWp[k * 64 + lane + 32], n11);
+        for (int k = 0; k < 32; k += 2) {
+            const double e0 = __shfl_sync(0xffffffffu, n00, k), e1 = __shfl_sync(0xffffffffu, n00, k + 1);
+            a10 = fma(e0, sWp[k * 64 + lane], a10);
+            a11 = fma(e0, sWp[k * 64 + lane + 32], a11);
+            b10 = fma(e1, sWp[(k + 1) * 64 + lane], b10);
+            b11 = fma(e1, sWp[(k + 1) * 64 + lane + 32], b11);
         }
 #pragma unroll 8
-        for (int k = 0; k < 32; ++k) {
-            const double a = __shfl_sync(0xffffffffu, n01, k);
-            n10 = fma(a, sWp[(k + 32) * 64 + lane], n10);
-            n11 = fma(a, sWp[(k + 32) * 64 + lane + 32], n11);
+        for (int k = 0; k < 32; k += 2) {
+            const double e0 = __shfl_sync(0xffffffffu, n01, k), e1 = __shfl_sync(0xffffffffu, n01, k + 1);
+            c10 = fma(e0, sWp[(k + 32) * 64 + lane], c10);
+            c11 = fma(e0, sWp[(k + 32) * 64 + lane + 32], c11);
+            d10 = fma(e1, sWp[(k + 33) * 64 + lane], d10);
+            d11 = fma(e1, sWp[(k + 33) * 64 + lane + 32], d11);
         }
+        const double n10 = (a10 + b10) + (c10 + d10), n11 = (a11 + b11) + (c11 + d11);
+        if (i + stride < nrows) gather(i + stride);  // the next row's loads overlap the stores below
         double* Lr = L + (int64_t)i * 128;
         Lr[lane] = n00;
         Lr[lane + 32] = n01;
