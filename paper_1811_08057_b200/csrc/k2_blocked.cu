@@ -324,26 +324,29 @@ constexpr int MS_THREADS = 256;               // 8 warps: 2 (M) x 4 (N), warp ti
 // SUB = 2: a "fat" CTA of two independent 256-thread sub-CTAs (own smem ring, own named
 // barrier) that fills a whole SM, so a grid of B fat CTAs occupies exactly B SMs and
 // leaves the rest free for the panel kernel running concurrently on another stream.
-template <int K, int SUB>
-__global__ void __launch_bounds__(MS_THREADS * SUB, 2 / SUB) k2_gemm_ms_kernel(double* __restrict__ ws, int64_t ld, int32_t rbase,
+// BNT: tile width, 128 (8 warps, 2 x 4 of 32 x 32) or 64 (4 warps, 2 x 2): the narrow tiles
+// double the CTA count of a short (critical-path) update so more SMs share it.
+template <int K, int SUB, int BNT = BN>
+__global__ void __launch_bounds__(64 * (BNT / 32) * SUB, 2 / SUB) k2_gemm_ms_kernel(double* __restrict__ ws, int64_t ld, int32_t rbase,
                                                                    int32_t M, int32_t N2, const double* __restrict__ L,
                                                                    int64_t ldl, const double* __restrict__ W, int64_t ldw,
                                                                    unsigned long long* __restrict__ wit,
                                                                    const unsigned* __restrict__ abort) {
     constexpr int KS = K / MS_BK;  // stages per tile
-    constexpr int WN = 4, NJ = 4;
+    constexpr int WN = BNT / 32, NJ = 4, NTH = 64 * WN;  // warps in N, 8x8 tiles per warp in N, threads
+    constexpr int LDW_T = BNT + 8, STAGE_T = BM * MS_LDL + MS_BK * LDW_T;
     extern __shared__ __align__(16) double sh_all[];
     if (*(volatile const unsigned*)abort) return;
-    const int sub = SUB == 2 ? (int)(threadIdx.x >= MS_THREADS) : 0;
-    double* const sh = sh_all + sub * (MS_ST * MS_STAGE);
+    const int sub = SUB == 2 ? (int)(threadIdx.x >= NTH) : 0;
+    double* const sh = sh_all + sub * (MS_ST * STAGE_T);
     auto sync = [&]() {
         if constexpr (SUB == 1) __syncthreads();
-        else asm volatile("bar.sync %0, %1;" ::"r"(1 + sub), "n"(MS_THREADS) : "memory");
+        else asm volatile("bar.sync %0, %1;" ::"r"(1 + sub), "n"(NTH) : "memory");
     };
-    const int tid = (int)threadIdx.x - sub * MS_THREADS, lane = tid & 31, warp = tid >> 5;
+    const int tid = (int)threadIdx.x - sub * NTH, lane = tid & 31, warp = tid >> 5;
     const int wm = warp / WN, wn = warp % WN;
     const int g = lane >> 2, q = lane & 3;
-    const int ntn = (N2 + BN - 1) / BN, ntm = (M + BM - 1) / BM;
+    const int ntn = (N2 + BNT - 1) / BNT, ntm = (M + BM - 1) / BM;
     const int64_t T = (int64_t)ntn * ntm;
     const int64_t vb = (int64_t)blockIdx.x * SUB + sub, vg = (int64_t)gridDim.x * SUB;
     const int64_t t_begin = T * vb / vg, t_end = T * (vb + 1) / vg;
@@ -354,19 +357,19 @@ __global__ void __launch_bounds__(MS_THREADS * SUB, 2 / SUB) k2_gemm_ms_kernel(d
         if (j < nst) {
             const int64_t t = t_begin + j / KS;
             const int kk = (int)(j % KS) * MS_BK;
-            const int row0 = (int)(t / ntn) * BM, col0 = (int)(t % ntn) * BN;
-            double* ls = sh + (int)(j % MS_ST) * MS_STAGE;
+            const int row0 = (int)(t / ntn) * BM, col0 = (int)(t % ntn) * BNT;
+            double* ls = sh + (int)(j % MS_ST) * STAGE_T;
             double* wsm = ls + BM * MS_LDL;
-            for (int i = tid; i < BM * (MS_BK / 2); i += MS_THREADS) {
+            for (int i = tid; i < BM * (MS_BK / 2); i += NTH) {
                 const int r = i / (MS_BK / 2), c2 = i % (MS_BK / 2);
                 double* dst = ls + r * MS_LDL + 2 * c2;
                 if (row0 + r < M) cp_async16(dst, L + (int64_t)(row0 + r) * ldl + kk + 2 * c2);
                 else { dst[0] = 0.0; dst[1] = 0.0; }
             }
-            for (int i = tid; i < MS_BK * (BN / 2); i += MS_THREADS) {
-                const int k = i / (BN / 2), c2 = i % (BN / 2);
+            for (int i = tid; i < MS_BK * (BNT / 2); i += NTH) {
+                const int k = i / (BNT / 2), c2 = i % (BNT / 2);
                 const int col = col0 + 2 * c2;
-                double* dst = wsm + k * LDWS + 2 * c2;
+                double* dst = wsm + k * LDW_T + 2 * c2;
                 if (col < N2) cp_async16(dst, W + (int64_t)(kk + k) * ldw + col);
                 else { dst[0] = 0.0; dst[1] = 0.0; }
             }
@@ -378,7 +381,7 @@ __global__ void __launch_bounds__(MS_THREADS * SUB, 2 / SUB) k2_gemm_ms_kernel(d
     // mid-way through the current tile): the accumulator load then hits L2
     auto prefetch_c = [&](int64_t t) {
         if (MS_PREFETCH_C == 0) return;
-        const int row0 = (int)(t / ntn) * BM, col0 = (int)(t % ntn) * BN;
+        const int row0 = (int)(t / ntn) * BM, col0 = (int)(t % ntn) * BNT;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             const int r = row0 + wm * 32 + i * 8 + g;
@@ -397,7 +400,7 @@ __global__ void __launch_bounds__(MS_THREADS * SUB, 2 / SUB) k2_gemm_ms_kernel(d
     for (int64_t j = 0; j < nst; ++j) {
         const int64_t t = t_begin + j / KS;
         const int ks = (int)(j % KS);
-        const int row0 = (int)(t / ntn) * BM, col0 = (int)(t % ntn) * BN;
+        const int row0 = (int)(t / ntn) * BM, col0 = (int)(t % ntn) * BNT;
         if (ks == 0) {  // C tile -> accumulators (acc = C - L W)
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
@@ -426,7 +429,7 @@ __global__ void __launch_bounds__(MS_THREADS * SUB, 2 / SUB) k2_gemm_ms_kernel(d
         asm volatile("cp.async.wait_group %0;" ::"n"(MS_ST - 2) : "memory");
         sync();  // stage j landed; buffer (j-1) % MS_ST is free
         load_stage(j + MS_ST - 1);
-        const double* ls = sh + (int)(j % MS_ST) * MS_STAGE;
+        const double* ls = sh + (int)(j % MS_ST) * STAGE_T;
         const double* wsm = ls + BM * MS_LDL;
 #pragma unroll
         for (int k0 = 0; k0 < MS_BK; k0 += 4) {
@@ -434,7 +437,7 @@ __global__ void __launch_bounds__(MS_THREADS * SUB, 2 / SUB) k2_gemm_ms_kernel(d
 #pragma unroll
             for (int i = 0; i < 4; ++i) a[i] = ls[(wm * 32 + i * 8 + g) * MS_LDL + k0 + q];
 #pragma unroll
-            for (int jj = 0; jj < NJ; ++jj) b[jj] = wsm[(k0 + q) * LDWS + wn * 32 + jj * 8 + g];
+            for (int jj = 0; jj < NJ; ++jj) b[jj] = wsm[(k0 + q) * LDW_T + wn * 32 + jj * 8 + g];
 #pragma unroll
             for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -555,6 +558,17 @@ cudaError_t k2_gemm(double* ws, int64_t ld, int32_t rbase, int32_t M, int32_t N2
         const int grid_f = (int)std::min<int64_t>((tiles + 1) / 2, sm_budget);
         if (K == 64) k2_gemm_ms_kernel<64, 2><<<grid_f, 2 * MS_THREADS, 2 * smem_ms, s>>>(ws, ld, rbase, M, N2, L, ldl, W, ldw, w, abort);
         else k2_gemm_ms_kernel<128, 2><<<grid_f, 2 * MS_THREADS, 2 * smem_ms, s>>>(ws, ld, rbase, M, N2, L, ldl, W, ldw, w, abort);
+        return cudaGetLastError();
+    }
+    if (ms_mode && M <= 2 * BM && K == 128) {  // a short critical-path update: 64-wide tiles, twice the CTAs
+        static bool attr = false;
+        const size_t smem_n = (size_t)MS_ST * (BM * MS_LDL + MS_BK * (64 + 8)) * sizeof(double);
+        if (!attr) {
+            cudaFuncSetAttribute(k2_gemm_ms_kernel<128, 1, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_n);
+            attr = true;
+        }
+        const int64_t tiles_n = (int64_t)((N2 + 63) / 64) * ((M + BM - 1) / BM);
+        k2_gemm_ms_kernel<128, 1, 64><<<(int)tiles_n, 128, smem_n, s>>>(ws, ld, rbase, M, N2, L, ldl, W, ldw, w, abort);
         return cudaGetLastError();
     }
     if (ms_mode) {
