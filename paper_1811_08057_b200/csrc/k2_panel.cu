@@ -698,7 +698,56 @@ __global__ void __launch_bounds__(kThreads, 1) kp_panel_kernel(const KPParams p)
             }
         }
     }
-    if (p.pp_g0 && g == 0) {  // pair prep right here: this CTA's descriptor is final
+    if (p.pp_g0 && p.pp_bar) {
+        // pair prep spread over every CTA: (a) a slice of Wp[s][s'] = -W_k[s][P1[s']] with
+        // P1 derived from this CTA's own pivot list, CTA 0 meanwhile the composite
+        // descriptor; one grid barrier (every Wp read of W_k done); (b) a slice of W_k's
+        // moved columns, from the descriptor CTA 0 published (k2_pair_prep.cuh, same values)
+        __shared__ int s_P1[kB];
+        if (tid < kB) {
+            int pos = s_l[tid];
+            for (int j = tid - 1; j >= 0; --j) pos = (pos == s_l[j]) ? (m - j - 1) : pos;
+            s_P1[tid] = pos;
+        }
+        __syncthreads();
+        {
+            const int e0 = (int)((int64_t)kB * kB * g / G), e1 = (int)((int64_t)kB * kB * (g + 1) / G);
+            for (int e = e0 + tid; e < e1; e += kThreads) {
+                const int sr = e / kB, sp = e % kB;
+                p.pp_Wp[e] = -__ldcg(p.pp_W + (int64_t)sr * p.pp_ldw + s_P1[sp]);  // negated, as pair_prep_body
+            }
+        }
+        if (g == 0) {
+            __syncthreads();
+            pair_prep_desc<kThreads>(p.pp_g0, p.pan, p.pp_m, p.pp_gpair, s_pp, tid);
+        }
+        __syncthreads();
+        if (tid == 0) {
+            __threadfence();
+            atomicAdd(p.pp_bar, 1u);
+            unsigned v;
+            for (;;) {
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p.pp_bar) : "memory");
+                if (v >= (unsigned)G) break;
+                if (globaltimer() - t_start > p.timeout_ns) {
+                    atomicExch(&p.err->error, 1u);
+                    atomicExch(&p.err->err_step, (unsigned)(p.row0 + kB - 1));
+                    break;
+                }
+            }
+        }
+        __syncthreads();
+        {
+            const int nm1 = __ldcg(&p.pan->n_moved), wf2 = p.pp_m - 2 * kB;
+            const int tot = kB * nm1;
+            const int e0 = (int)((int64_t)tot * g / G), e1 = (int)((int64_t)tot * (g + 1) / G);
+            for (int e = e0 + tid; e < e1; e += kThreads) {
+                const int sr = e / nm1, k = e % nm1;
+                const int c = __ldcg(&p.pan->moved_c[k]);
+                if (c < wf2) p.pp_W[(int64_t)sr * p.pp_ldw + c] = __ldcg(p.pp_W + (int64_t)sr * p.pp_ldw + __ldcg(&p.pan->moved_src[k]));
+            }
+        }
+    } else if (p.pp_g0 && g == 0) {  // pair prep right here: this CTA's descriptor is final
         __syncthreads();
         pair_prep_body<kThreads>(p.pp_g0, p.pan, p.pp_m, p.pp_W, p.pp_ldw, p.pp_Wp, p.pp_gpair, s_pp, tid);
     }

@@ -735,7 +735,7 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
     const size_t o_cand = take((size_t)64 * kKPMaxG * sizeof(double2));
     const size_t o_wrec = take((size_t)64 * kKPMaxG * sizeof(double2));
     const size_t o_colb = take((size_t)64 * kKPMaxG * 64 * sizeof(double2));
-    const size_t o_lastb = take((size_t)64 * 64 * sizeof(double2));
+    const size_t o_lastb = take(kLastBufBytes);
     const size_t o_ctl = take(sizeof(K1Err) + 16);
     // int metadata: iota[n] | never[n] | panel_ptr[b+1] | init_ptr[G0+1] init_rows[n] | tail_ptr[Gt+1] tail_rows[mt]
     const size_t n_int = (size_t)(n + n + (b + 1) + (G0 + 1) + n + (Gt + 1) + mt);
@@ -768,7 +768,7 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
     CUDA_TRY(cudaMemsetAsync(base + o_ctl, 0, sizeof(K1Err) + 16, st));
     // the panel kernels' record slots: cleared per call, so a record's tag only has to
     // be unique within the call (its global step + 1)
-    CUDA_TRY(cudaMemsetAsync(base + o_cand, 0, o_lastb + (size_t)64 * 64 * sizeof(double2) - o_cand, st));
+    CUDA_TRY(cudaMemsetAsync(base + o_cand, 0, o_lastb + kLastBufBytes - o_cand, st));
     const int32_t* d_int = (const int32_t*)(base + o_int);
     const int32_t* d_iota = d_int;
     const int32_t* d_never = d_iota + n;
@@ -894,6 +894,7 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
     const bool fuse_r1 = env_long("MCND_K2_FUSE_R1", 1) != 0;
     const int64_t min_budget = env_long("MCND_K2_MIN_BUDGET", B->sms / 4);
     const bool side_after = env_long("MCND_K2_SIDE_AFTER", 1) != 0;
+    const bool pp_spread = env_long("MCND_K2_PP_SPREAD", 1) != 0;  // pair prep over every CTA of the second panel
     bool side_pending = false;
     cudaStream_t side = B->side;
     auto join_side = [&]() -> cudaError_t {
@@ -936,6 +937,7 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
             }
             if (fuse_pp) {  // the second panel kernel runs the pair prep in its CTA 0
                 kp.pp_g0 = gp0; kp.pp_W = Wq; kp.pp_ldw = ld; kp.pp_Wp = Wp; kp.pp_gpair = gpair; kp.pp_m = (int32_t)m;
+                kp.pp_bar = pp_spread ? reinterpret_cast<unsigned*>(kp.lastbuf + 64 * 64) + kb / (2 * b) : nullptr;
             }
             if (e == cudaSuccess) e = run_kp(kb + b, gp1, Wq + b * ld);
             kp.pp_g0 = nullptr;
@@ -1155,7 +1157,7 @@ int mg_create(int64_t n, int64_t lr, MgHandle** out) {
     const size_t o_cand = take((size_t)64 * kKPMaxG * sizeof(double2));
     const size_t o_wrec = take((size_t)64 * kKPMaxG * sizeof(double2));
     const size_t o_colb = take((size_t)64 * kKPMaxG * 64 * sizeof(double2));
-    const size_t o_lastb = take((size_t)64 * 64 * sizeof(double2));
+    const size_t o_lastb = take(kLastBufBytes);
     const size_t o_ctl = take(sizeof(K1Err) + 16);
     const int64_t ni = std::max<int64_t>(n, lrr);
     const size_t n_int = (size_t)(ni + lrr + (h->g0 + 1) + lrr);
@@ -1206,7 +1208,7 @@ int mg_load(MgHandle* h, const double* src, int64_t lds, cudaStream_t st) {
     h->epoch = h->epoch + 1 + (h->epoch + 1 == 0 ? 1 : 0);
     CUDA_TRY(cudaMemsetAsync(h->recs, 0, (size_t)h->n * sizeof(PivRec), st));
     CUDA_TRY(cudaMemsetAsync(h->err, 0, sizeof(K1Err) + 16, st));
-    CUDA_TRY(cudaMemsetAsync(h->cand, 0, (size_t)((char*)(h->lastb + 64 * 64) - (char*)h->cand), st));
+    CUDA_TRY(cudaMemsetAsync(h->cand, 0, (size_t)((char*)h->lastb + kLastBufBytes - (char*)h->cand), st));
     if (h->lr == 0) return MCND_OK;
     const int64_t ni = std::max<int64_t>(h->n, h->lr);
     K1Params p{};
@@ -1292,6 +1294,8 @@ int mg_pair(MgHandle* h, int64_t lr0, int64_t t, int64_t m, double* W, int64_t l
         KPParams kp1 = mg_kp(h, lr0 + b, t + b, m - b, gp1, W + b * ldw, ldw);
         kp1.r1_g0 = gp0; kp1.r1_W = W; kp1.r1_ldw = ldw;  // + the first panel's update of these rows
         kp1.pp_g0 = gp0; kp1.pp_W = W; kp1.pp_ldw = ldw; kp1.pp_Wp = Wp; kp1.pp_gpair = gpair; kp1.pp_m = (int32_t)m;
+        kp1.pp_bar = (env_long("MCND_K2_PP_SPREAD", 1) != 0 && t / (2 * b) < kPPBars)
+                         ? reinterpret_cast<unsigned*>(h->lastb + 64 * 64) + t / (2 * b) : nullptr;
         e = kp_launch(kp1, st);  // + the pair prep in its CTA 0
     }
     if (e != cudaSuccess) return fail(MCND_ECUDA, "mg_pair: %s", cudaGetErrorString(e));

@@ -123,8 +123,15 @@ struct KPParams {
     const K2Gather* r1_g0;    // the first panel's descriptor (nullptr: rows already updated)
     const double* r1_W;       // its W (64 rows, row stride r1_ldw)
     int64_t r1_ldw;
+    // pair prep spread over every CTA of the second panel (Wp rows and W's moved columns
+    // in slices, the composite descriptor in CTA 0) around one grid barrier on this
+    // counter (zeroed per call, one per pair); nullptr: CTA 0 does all of it
+    unsigned* pp_bar;
 };
 constexpr int kKPMaxG = 160;
+// lastbuf allocation: the LAST records [64][64], then the pair-prep barrier counters
+constexpr int kPPBars = 1024;  // pairs per call (n <= 131072)
+constexpr size_t kLastBufBytes = (size_t)64 * 64 * 16 + (size_t)kPPBars * sizeof(unsigned);
 constexpr int kKPMaxCw = 380;  // columns per panel CTA (64 x 380 doubles = 190 KB of shared memory)
 constexpr int kKPClusterMax = 16;
 cudaError_t kp_launch(const KPParams& p, cudaStream_t s);
