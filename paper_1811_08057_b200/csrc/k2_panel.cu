@@ -678,6 +678,7 @@ __global__ void __launch_bounds__(kThreads, 1) kp_panel_kernel(const KPParams p)
                 }
         }
     }
+    KP_MARK(1, 11);
     // ---- panel-start column of each pivot and the moved final columns (CTA 0)
     if (g == 0 && tid < kB) {
         const int s = tid;

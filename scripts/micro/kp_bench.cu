@@ -3,6 +3,7 @@
 #define KP_TRACE 1
 #endif
 #include <cstdio>
+#include <cstring>
 #include <cstdlib>
 #include <vector>
 #include <random>
@@ -69,6 +70,10 @@ int main(int argc, char** argv) {
         long dw = 0, dr = 0;
         for (int t = 0; t < 64; ++t) for (int c = 0; c < m - 64; ++c) dw += w1[(size_t)t * ld + c] != w2[(size_t)t * ld + c];
         for (int t = 0; t < 64; ++t) dr += (r1[t].v != r2[t].v) || (r1[t].l != r2[t].l);
+        unsigned long long hsum = 0;  // bit-pattern checksum of W (compare builds)
+        for (int t = 0; t < 64; ++t) for (int c = 0; c < m - 64; ++c) {
+            unsigned long long b; memcpy(&b, &w1[(size_t)t * ld + c], 8); hsum = hsum * 1099511628211ull ^ b; }
+        printf("W checksum %016llx\n", hsum);
         printf("cross-check vs cluster=%d (%s): W mismatches %ld, pivot mismatches %ld, piv0 %.17g l0 %d\n", !cl,
                cudaGetErrorString(e), dw, dr, r1[0].v, r1[0].l);
     }
@@ -91,7 +96,8 @@ int main(int argc, char** argv) {
             p10 += (double)(tr[s][10] - tr[s][9]); p1 += (double)(tr[s][1] - tr[s][10]); }
         printf("  A detail: poll %.0f  reduce %.0f  fetch %.0f  sync %.0f\n", p8 / 61, p9 / 61, p10 / 61, p1 / 61);
     }
-    printf("  prologue %llu cycles, loop %llu, W %llu\n", tr[0][9] - tr[0][8], tr[0][10] - tr[0][9], tr[0][11] - tr[0][10]);
+    printf("  prologue %llu cycles, loop %llu, W %llu (product %llu, descriptor %llu)\n", tr[0][9] - tr[0][8], tr[0][10] - tr[0][9],
+           tr[0][11] - tr[0][10], tr[1][11] - tr[0][10], tr[0][11] - tr[1][11]);
 #endif
     return 0;
 }
