@@ -254,6 +254,69 @@ __global__ void __launch_bounds__(kThreads, 1) kp_panel_kernel(const KPParams p)
         }
         __syncthreads();
         const double* W0 = p.r1_W + lo;
+#ifndef KP_R1_DMMA
+#define KP_R1_DMMA 1
+#endif
+        if (KP_R1_DMMA) {
+            // on the FP64 tensor cores (mma.sync.m8n8k4.f64, k ascending: the trailing GEMM's
+            // arithmetic): warp w owns the 8-column tiles w, w + 16, ... (two at a time) for
+            // all 64 rows, so every W0 element is read from L2 once per CTA
+            const int gq = lane >> 2, qq = lane & 3;
+            const int ntiles = (wc + 7) >> 3;
+            constexpr int kNW = kThreads / 32;
+            for (int tp = warp; tp < ntiles; tp += 2 * kNW) {
+                const int tl[2] = {tp, tp + kNW};
+                double acc[8][2][2];
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+#pragma unroll
+                    for (int t = 0; t < 2; ++t) {
+                        const int c = tl[t] * 8 + 2 * qq;
+                        const double* sp = S + (8 * i + gq) * cw + c;
+                        acc[i][t][0] = (c < wc) ? sp[0] : 0.0;
+                        acc[i][t][1] = (c + 1 < wc) ? sp[1] : 0.0;
+                    }
+                constexpr int kPF = 4;  // W0 k-steps in a register ring
+                double bq[kPF][2];
+#pragma unroll
+                for (int s4 = 0; s4 < kPF; ++s4)
+#pragma unroll
+                    for (int t = 0; t < 2; ++t) {
+                        const int c = tl[t] * 8 + gq;
+                        bq[s4][t] = (c < wc) ? __ldg(W0 + (int64_t)(4 * s4 + qq) * p.r1_ldw + c) : 0.0;
+                    }
+                for (int k0 = 0; k0 < kB; k0 += 4 * kPF) {
+#pragma unroll
+                    for (int s4 = 0; s4 < kPF; ++s4) {
+                        const int k = k0 + 4 * s4;
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) {
+                            const double av = sTi[8 * i + gq][k + qq];
+#pragma unroll
+                            for (int t = 0; t < 2; ++t)
+                                asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                                    : "+d"(acc[i][t][0]), "+d"(acc[i][t][1]) : "d"(av), "d"(bq[s4][t]));
+                        }
+                        if (k + 4 * kPF < kB) {
+#pragma unroll
+                            for (int t = 0; t < 2; ++t) {
+                                const int c = tl[t] * 8 + gq;
+                                bq[s4][t] = (c < wc) ? __ldg(W0 + (int64_t)(k + 4 * kPF + qq) * p.r1_ldw + c) : 0.0;
+                            }
+                        }
+                    }
+                }
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+#pragma unroll
+                    for (int t = 0; t < 2; ++t) {
+                        const int c = tl[t] * 8 + 2 * qq;
+                        double* const sp = S + (8 * i + gq) * cw + c;
+                        if (c < wc) sp[0] = acc[i][t][0];
+                        if (c + 1 < wc) sp[1] = acc[i][t][1];
+                    }
+            }
+        } else
         for (int tb = warp; tb < kB / 4; tb += kThreads / 32) {
             for (int c0 = 0; c0 < wc; c0 += 128) {
                 double acc[4][4];
