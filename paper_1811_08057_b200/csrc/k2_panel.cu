@@ -712,6 +712,55 @@ __global__ void __launch_bounds__(kThreads, 1) kp_panel_kernel(const KPParams p)
     // ---- W = T^{-1} U on my final columns (T unit upper triangular)
     {
     const int wf = max(0, min(wc, m - kB - lo));
+#ifndef KP_W_DMMA
+#define KP_W_DMMA 1
+#endif
+    if (KP_W_DMMA) {
+        // W = T^{-1} U on the FP64 tensor cores (mma.sync.m8n8k4.f64; A = T^{-1}, B = U, the
+        // chunk itself), straight to global.  Warp w owns the 8-column tiles w, w + 16, ...
+        // (two at a time) for all 64 rows; row block mb joins at its diagonal (k0 >= 8 mb):
+        // the terms below the diagonal are zero and leave the accumulator at +0, so every
+        // element is the FMA chain of the loop below (bitwise, kp_bench W checksums)
+        const int gq = lane >> 2, qq = lane & 3;
+        const int ntiles = (wf + 7) >> 3;
+        constexpr int kNW = kThreads / 32;
+        for (int tp = warp; tp < ntiles; tp += 2 * kNW) {
+            const int tl[2] = {tp, tp + kNW};
+            double acc[8][2][2];
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+                for (int t = 0; t < 2; ++t) { acc[i][t][0] = 0.0; acc[i][t][1] = 0.0; }
+#pragma unroll
+            for (int k0 = 0; k0 < kB; k0 += 4) {
+                double bv[2];
+#pragma unroll
+                for (int t = 0; t < 2; ++t) {
+                    const int c = tl[t] * 8 + gq;
+                    bv[t] = (c < wf) ? S[(k0 + qq) * cw + c] : 0.0;
+                }
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    if (8 * i <= k0 + 3) {  // compile-time after unrolling
+                        const double av = sTi[8 * i + gq][k0 + qq];
+#pragma unroll
+                        for (int t = 0; t < 2; ++t)
+                            asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                                : "+d"(acc[i][t][0]), "+d"(acc[i][t][1]) : "d"(av), "d"(bv[t]));
+                    }
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+                for (int t = 0; t < 2; ++t) {
+                    const int c = tl[t] * 8 + 2 * qq;
+                    double* const wr = p.W + (int64_t)(8 * i + gq) * p.ldw + lo + c;
+                    if (c + 1 < wf) *reinterpret_cast<double2*>(wr) = make_double2(acc[i][t][0], acc[i][t][1]);
+                    else if (c < wf) wr[0] = acc[i][t][0];
+                }
+        }
+    } else {
     // W = T^{-1} U straight to global: warp w owns rows 4w..4w+3, lane owns columns
     // lane + 32k (k < 4) of each 128-column pass: T^{-1} reads are warp broadcasts, U
     // reads and W stores are contiguous across the warp
@@ -740,6 +789,7 @@ __global__ void __launch_bounds__(kThreads, 1) kp_panel_kernel(const KPParams p)
                     if (c < wf) p.W[(int64_t)(4 * tb + i) * p.ldw + lo + c] = acc[i][k];
                 }
         }
+    }
     }
     KP_MARK(1, 11);
     // ---- panel-start column of each pivot and the moved final columns (CTA 0)
