@@ -66,7 +66,7 @@ struct Buffers {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     cudaStream_t side = nullptr;                 // K2: trailing updates overlapped with the next panels (lowest priority)
     cudaStream_t crit = nullptr;                 // K2: the panel chain (highest priority)
-    cudaEvent_t ev_a = nullptr, ev_b = nullptr;  // K2: stream joins
+    cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_c = nullptr;  // K2: stream joins
     cudaEvent_t ev_in = nullptr, ev_out = nullptr;
     int sms = 0;
     uint32_t epoch = 0;
@@ -92,6 +92,7 @@ int init_buffers(Buffers& b, int dev) {
     cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
     if (cudaEventCreateWithFlags(&b.ev_a, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&b.ev_b, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&b.ev_c, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&b.ev_in, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&b.ev_out, cudaEventDisableTiming) != cudaSuccess ||
         cudaStreamCreateWithPriority(&b.side, cudaStreamNonBlocking, prio_lo) != cudaSuccess ||
@@ -728,10 +729,13 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
     const size_t o_ws = take((size_t)n * ld * sizeof(double));
     const size_t o_wit = take((size_t)n * sizeof(double));
     const size_t o_rec = take((size_t)n * sizeof(PivRec));
-    const size_t o_L = take((size_t)2 * std::max<int64_t>(n, 1) * 2 * b * sizeof(double));  // x2: by pair parity
-    const size_t o_W = take((size_t)2 * 2 * b * ld * sizeof(double));
-    const size_t o_pan = take(4 * sizeof(K2Gather));           // gp0, gp1, gpair x2 (pair parity)
-    const size_t o_Wp = take((size_t)2 * b * b * sizeof(double));  // x2 (pair parity)
+    // L, W, Wp and the pair's gather descriptor in a ring of kRing pair slots: the side update
+    // of pair q may still read its slot while pairs q+1 and q+2 factor (depth-2 look-ahead)
+    constexpr int kRing = 3;
+    const size_t o_L = take((size_t)kRing * std::max<int64_t>(n, 1) * 2 * b * sizeof(double));
+    const size_t o_W = take((size_t)kRing * 2 * b * ld * sizeof(double));
+    const size_t o_pan = take((2 + kRing) * sizeof(K2Gather));           // gp0, gp1, gpair ring
+    const size_t o_Wp = take((size_t)kRing * b * b * sizeof(double));
     const size_t o_cand = take((size_t)64 * kKPMaxG * sizeof(double2));
     const size_t o_wrec = take((size_t)64 * kKPMaxG * sizeof(double2));
     const size_t o_colb = take((size_t)64 * kKPMaxG * 64 * sizeof(double2));
@@ -784,8 +788,8 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
     double* Wb = (double*)(base + o_W);
     K2Gather* gp0 = (K2Gather*)(base + o_pan);
     K2Gather* gp1 = gp0 + 1;
-    K2Gather* const gpair2 = gp0 + 2;  // by pair parity, like L and W: the side stream of
-    double* const Wp2 = (double*)(base + o_Wp);  // pair q may still gather while pair q+1 preps
+    K2Gather* const gpair2 = gp0 + 2;  // ring, like L and W
+    double* const Wp2 = (double*)(base + o_Wp);
     K1Err* err = (K1Err*)(base + o_ctl);
     unsigned* abort = (unsigned*)(base + o_ctl + sizeof(K1Err));
     const uint32_t epoch = ++B->epoch;
@@ -895,15 +899,27 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
     const int64_t min_budget = env_long("MCND_K2_MIN_BUDGET", B->sms / 4);
     const bool side_after = env_long("MCND_K2_SIDE_AFTER", 1) != 0;
     const bool pp_spread = env_long("MCND_K2_PP_SPREAD", 1) != 0;  // pair prep over every CTA of the second panel
-    bool side_pending = false;
+    // depth-2 look-ahead (MCND_K2_LA2=1): each pair's side update is split into part A, the
+    // rows of the unit after next (what the NEXT pair's critical update touches), and part
+    // B, the rest; the next pair waits for part A only, so part B overlaps the next pair too
+    const bool la2 = env_long("MCND_K2_LA2", 1) != 0;
+    bool side_pending = false, sideA_pending = false;
     cudaStream_t side = B->side;
-    auto join_side = [&]() -> cudaError_t {
+    auto join_side = [&]() -> cudaError_t {  // all side work
+        sideA_pending = false;
         if (!side_pending) return cudaSuccess;
         side_pending = false;
         return cudaStreamWaitEvent(st, B->ev_b, 0);
     };
+    auto join_rows = [&]() -> cudaError_t {  // the side work the next critical update depends on
+        if (sideA_pending) {
+            sideA_pending = false;
+            return cudaStreamWaitEvent(st, B->ev_c, 0);
+        }
+        return join_side();
+    };
     int64_t k = 0;
-    int par = 0;
+    int par = 0;  // ring slot
     int64_t n_launch = 1;  // kernels launched by this call (K1 init so far)
     // debug timeline (MCND_DEBUG_TIMELINE=1): an event after every critical-stream step,
     // per-label device time printed to stderr at the end of the call
@@ -945,7 +961,7 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
             mark("kp2");
             if (e == cudaSuccess && !fuse_pp) e = k2_pair_prep(gp0, gp1, (int32_t)m, Wq, ld, Wp, gpair, abort, st);
             if (!fuse_pp) mark("pair_prep");
-            if (e == cudaSuccess) e = join_side();  // trailing rows final for the previous pair
+            if (e == cudaSuccess) e = join_rows();  // the critical rows final for the previous pair
             mark("join");
             const int32_t nr = (int32_t)(n - kb - 2 * b);
             // rows the next unit factors: a pair (128), a last single panel (64), or the tail (all)
@@ -994,14 +1010,28 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
             if (e == cudaSuccess && ahead < nr && side_after) e = cudaEventRecord(B->ev_a, st);
             if (e == cudaSuccess && ahead < nr) {
                 e = cudaStreamWaitEvent(side, B->ev_a, 0);
-                if (e == cudaSuccess) e = trailing(ahead, nr - ahead, side, prio ? -1 : (int)budget);
+                // part A: the rows of the unit after next (a pair: 128, a single panel: 64, else
+                // everything left) when the next unit is a pair; the next pair waits for it alone
+                const int64_t k4 = k2 + 2;
+                const int64_t ahead2 = (la2 && k2 + 1 < n_panels && prio)
+                                           ? ((k4 + 1 < n_panels) ? 2 * b : (k4 < n_panels ? b : nr - ahead))
+                                           : 0;
+                if (ahead2 > 0 && ahead2 < nr - ahead) {
+                    if (e == cudaSuccess) e = trailing(ahead, ahead2, side, -1);
+                    if (e == cudaSuccess) e = cudaEventRecord(B->ev_c, side);
+                    sideA_pending = (e == cudaSuccess);
+                    if (e == cudaSuccess) e = trailing(ahead + ahead2, nr - ahead - ahead2, side, -1);
+                    n_launch += 2;
+                } else {
+                    if (e == cudaSuccess) e = trailing(ahead, nr - ahead, side, prio ? -1 : (int)budget);
+                }
                 if (e == cudaSuccess) e = cudaEventRecord(B->ev_b, side);
                 side_pending = (e == cudaSuccess);
                 n_launch += 3;
             }
             n_launch += (fuse_pp ? 7 : 8) - (fuse_lc ? 1 : 0) - (fuse_r1 ? 2 : 0);  // 2 panels, [gather, update], [prep], gather, [L corr], trailing
             k += 2;
-            par ^= 1;
+            par = (par + 1) % kRing;
         } else {
             e = run_kp(kb, gp0, Wq);
             if (e == cudaSuccess) e = join_side();
@@ -1012,7 +1042,7 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
                             abort, st);
             n_launch += 3;
             k += 1;
-            par ^= 1;
+            par = (par + 1) % kRing;
         }
         if (e != cudaSuccess) {
             join_side();
