@@ -153,7 +153,7 @@ __global__ void __launch_bounds__(kPrepThreads) k2_pair_prep_kernel(const K2Gath
 // A-operand register reuse cache usable) ----
 constexpr int BM = 64, BN = 128, BKS = 64;   // tile rows / cols, K per pipeline stage
 constexpr int LDLS = BKS + 4;                // padded smem strides (conflict-free fragment loads)
-constexpr int LDWS = BN + 8;
+constexpr int LDWS = BN + 4;                 // = 4 (mod 16): the B fragment (lanes 4q+g) hits 16 distinct bank pairs per half-warp
 constexpr int kStage = BM * LDLS + BKS * LDWS;  // doubles per stage buffer
 // warps: 2 (M) x WN (N); WN = 8 -> 512 threads, warp tile 32 x 16; WN = 4 -> 256 threads, 32 x 32
 
@@ -166,6 +166,12 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
     const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+
+// zero-filling form: src_bytes = 0 writes 16 zero bytes and reads nothing
+__device__ __forceinline__ void cp_async16_zf(void* smem, const void* gmem, bool valid) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "r"(valid ? 16 : 0) : "memory");
 }
 
 // Persistent: one CTA per SM walks a contiguous range of 64 x 128 output tiles
@@ -334,7 +340,7 @@ __global__ void __launch_bounds__(64 * (BNT / 32) * SUB, 2 / SUB) k2_gemm_ms_ker
                                                                    const unsigned* __restrict__ abort) {
     constexpr int KS = K / MS_BK;  // stages per tile
     constexpr int WN = BNT / 32, NJ = 4, NTH = 64 * WN;  // warps in N, 8x8 tiles per warp in N, threads
-    constexpr int LDW_T = BNT + 8, STAGE_T = BM * MS_LDL + MS_BK * LDW_T;
+    constexpr int LDW_T = BNT + 4, STAGE_T = BM * MS_LDL + MS_BK * LDW_T;
     extern __shared__ __align__(16) double sh_all[];
     if (*(volatile const unsigned*)abort) return;
     const int sub = SUB == 2 ? (int)(threadIdx.x >= NTH) : 0;
@@ -479,6 +485,164 @@ __global__ void __launch_bounds__(64 * (BNT / 32) * SUB, 2 / SUB) k2_gemm_ms_ker
     asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
+// ---- 4-warp variant: 64 x 128 tiles, 2 x 2 warps of 32 x 64 (32 DMMA per 12 fragment
+// loads), fragments double-buffered across k-steps and across stages, one barrier per
+// stage.  Two CTAs per SM with one warp per SM sub-partition each: every warp alone can
+// keep its sub-partition's DMMA pipe busy, so the stall of one CTA (C-tile load,
+// epilogue, barrier) is covered by the other.  Same arithmetic as k2_gemm_ms_kernel
+// (acc starts at C, DMMA k-steps in k order): bitwise the same result.
+constexpr int W4_THREADS = 128;
+template <int K, int S>
+__global__ void __launch_bounds__(W4_THREADS, 2) k2_gemm_w4_kernel(double* __restrict__ ws, int64_t ld, int32_t rbase,
+                                                                    int32_t M, int32_t N2, const double* __restrict__ L,
+                                                                    int64_t ldl, const double* __restrict__ W, int64_t ldw,
+                                                                    unsigned long long* __restrict__ wit,
+                                                                    const unsigned* __restrict__ abort) {
+    constexpr int KS = K / MS_BK;
+    constexpr int MI = 4, NJ = 8;  // warp tile 32 x 64
+    extern __shared__ __align__(16) double sh[];
+    if (*(volatile const unsigned*)abort) return;
+    const int tid = (int)threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm = warp >> 1, wn = warp & 1;
+    const int g = lane >> 2, q = lane & 3;
+    const int ntn = (N2 + BN - 1) / BN, ntm = (M + BM - 1) / BM;
+    const int T = ntn * ntm;  // < 2^31 tiles for any n the panel kernel accepts
+    const int t_begin = (int)((int64_t)T * blockIdx.x / gridDim.x), t_end = (int)((int64_t)T * (blockIdx.x + 1) / gridDim.x);
+    if (t_begin >= t_end) return;
+    const int nst = (t_end - t_begin) * KS;
+
+    // per thread: L rows tid/8 + 16u (u < 4), 16-byte chunk tid%8; W rows tid/64 + 2u (u < 8),
+    // chunk tid%64; out-of-range chunks are zero-filled (no branches)
+    auto load_stage = [&](int j) {
+        if (j < nst) {
+            const int t = t_begin + j / KS;
+            const int kk = (j % KS) * MS_BK;
+            const int row0 = (t / ntn) * BM, col0 = (t % ntn) * BN;
+            double* ls = sh + (j % S) * MS_STAGE;
+            double* wsm = ls + BM * MS_LDL;
+            const int ra = tid >> 3, ca = 2 * (tid & 7);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int r = row0 + ra + 16 * u;
+                const bool ok = r < M;
+                cp_async16_zf(ls + (ra + 16 * u) * MS_LDL + ca, L + (int64_t)(ok ? r : 0) * ldl + kk + ca, ok);
+            }
+            const int kb = tid >> 6, cb = 2 * (tid & 63);
+            const bool okc = col0 + cb < N2;
+            const double* wsrc = W + (int64_t)(kk + kb) * ldw + (okc ? col0 + cb : 0);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) cp_async16_zf(wsm + (kb + 2 * u) * LDWS + cb, wsrc + (int64_t)(2 * u) * ldw, okc);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    auto prefetch_c = [&](int t) {
+        const int row0 = (t / ntn) * BM, col0 = (t % ntn) * BN;
+#pragma unroll
+        for (int i = 0; i < MI; ++i) {
+            const int r = row0 + wm * 32 + i * 8 + g;
+            if (r < M) {  // the warp's 64 columns of row r: four 128-byte lines
+                const int c = col0 + wn * 64 + q * 16;
+                if (c < N2) asm volatile("prefetch.global.L2 [%0];" ::"l"(ws + (int64_t)(rbase + r) * ld + c));
+            }
+        }
+    };
+    double a[2][MI], b[2][NJ];
+    auto load_frags = [&](int buf, int j, int k0) {
+        const double* ls = sh + (int)(j % S) * MS_STAGE;
+        const double* wsm = ls + BM * MS_LDL;
+#pragma unroll
+        for (int i = 0; i < MI; ++i) a[buf][i] = ls[(wm * 32 + i * 8 + g) * MS_LDL + k0 + q];
+#pragma unroll
+        for (int jj = 0; jj < NJ; ++jj) b[buf][jj] = wsm[(k0 + q) * LDWS + wn * 64 + jj * 8 + g];
+    };
+
+    double acc[MI][NJ][2];
+    auto load_c = [&](int t) {  // C tile -> accumulators (acc = C - L W)
+        const int row0 = (t / ntn) * BM, col0 = (t % ntn) * BN;
+        const bool full = row0 + BM <= M && col0 + BN <= N2;
+#pragma unroll
+        for (int i = 0; i < MI; ++i) {
+            const int r = row0 + wm * 32 + i * 8 + g;
+            const double* crow = ws + (int64_t)(rbase + r) * ld + col0 + wn * 64 + 2 * q;
+#pragma unroll
+            for (int jj = 0; jj < NJ; ++jj) {
+                if (full || (r < M && col0 + wn * 64 + jj * 8 + 2 * q < N2)) {
+                    const double2 v = __ldcs(reinterpret_cast<const double2*>(crow + jj * 8));
+                    acc[i][jj][0] = v.x;
+                    acc[i][jj][1] = v.y;
+                } else {
+                    acc[i][jj][0] = 0.0;
+                    acc[i][jj][1] = 0.0;
+                }
+            }
+        }
+    };
+    prefetch_c(t_begin);
+#pragma unroll
+    for (int j = 0; j < S; ++j) load_stage(j);
+    load_c(t_begin);  // in flight together with the first stages
+    asm volatile("cp.async.wait_group %0;" ::"n"(S - 1) : "memory");
+    __syncthreads();
+    load_frags(0, 0, 0);
+    double rmx[MI] = {0.0, 0.0, 0.0, 0.0};
+    for (int j = 0; j < nst; ++j) {
+        const int t = t_begin + j / KS;
+        const int ks = j % KS;
+        const int row0 = (t / ntn) * BM, col0 = (t % ntn) * BN;
+        if (ks == 0 && j > 0) load_c(t);
+        if (ks == KS / 2 && t + 1 < t_end) prefetch_c(t + 1);
+#pragma unroll
+        for (int kq = 0; kq < MS_BK / 4; ++kq) {
+            if (kq == MS_BK / 4 - 1) {
+                // stage j+1 landed; every warp is done reading stage j (its last
+                // fragments are in registers), so its buffer takes stage j+S
+                asm volatile("cp.async.wait_group %0;" ::"n"(S - 2) : "memory");
+                __syncthreads();
+                load_stage(j + S);
+                if (j + 1 < nst) load_frags((kq + 1) & 1, j + 1, 0);
+            } else {
+                load_frags((kq + 1) & 1, j, 4 * (kq + 1));
+            }
+#pragma unroll
+            for (int i = 0; i < MI; ++i)
+#pragma unroll
+                for (int jj = 0; jj < NJ; ++jj) dmma(acc[i][jj][0], acc[i][jj][1], a[kq & 1][i], b[kq & 1][jj]);
+        }
+        if (ks != KS - 1) continue;
+        const int bm = t / ntn;
+        const bool full = row0 + BM <= M && col0 + BN <= N2;
+#pragma unroll
+        for (int i = 0; i < MI; ++i) {
+            const int r = row0 + wm * 32 + i * 8 + g;
+            double* crow = ws + (int64_t)(rbase + r) * ld;
+#pragma unroll
+            for (int jj = 0; jj < NJ; ++jj) {
+                const int c = col0 + wn * 64 + jj * 8 + 2 * q;
+                if (full || (r < M && c + 1 < N2)) {
+                    __stcs(reinterpret_cast<double2*>(crow + c), make_double2(acc[i][jj][0], acc[i][jj][1]));
+                    rmx[i] = fmax(rmx[i], fmax(fabs(acc[i][jj][0]), fabs(acc[i][jj][1])));
+                } else if (r < M && c < N2) {
+                    crow[c] = acc[i][jj][0];
+                    rmx[i] = fmax(rmx[i], fabs(acc[i][jj][0]));
+                }
+            }
+        }
+        const bool flush = (t + 1 == t_end) || ((t + 1) / ntn != bm);
+        if (flush && wit) {
+#pragma unroll
+            for (int i = 0; i < MI; ++i) {
+                double mx = rmx[i];
+                mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+                mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+                const int r = row0 + wm * 32 + i * 8 + g;
+                if (q == 0 && r < M) atomicMax(wit + rbase + r, (unsigned long long)__double_as_longlong(mx));
+                rmx[i] = 0.0;
+            }
+        }
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
 }  // namespace
 
 cudaError_t k2_gather_fix(double* ws, int64_t ld, int32_t rbase, int32_t nrows, int32_t K, const K2Gather* gp,
@@ -546,6 +710,29 @@ cudaError_t k2_gemm(double* ws, int64_t ld, int32_t rbase, int32_t M, int32_t N2
         cudaFuncSetAttribute(k2_gemm_ms_kernel<64, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * (int)smem_ms);
         cudaFuncSetAttribute(k2_gemm_ms_kernel<128, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * (int)smem_ms);
     }
+    // 4-warp kernel (32 x 64 warp tiles): MCND_K2_GEMM_W4=0 selects the 8-warp one.  The overlapped
+    // (side) update runs one tile per CTA, so SMs go back to the next panel tile by tile, unless it is
+    // more than MCND_K2_GEMM_PWAVES waves of 2 CTAs per SM: then the GEMM, not the panel chain, bounds
+    // the pair and a persistent grid (no per-CTA pipeline fill) is faster.  MCND_K2_GEMM_TPC forces
+    // a tiles-per-CTA count (0 = persistent).
+    static long w4 = -1, tpc = -1, pwaves = 40;
+    if (w4 < 0) {
+        const char* v = std::getenv("MCND_K2_GEMM_W4");
+        w4 = v ? std::strtol(v, nullptr, 10) : 1;
+        if (const char* u = std::getenv("MCND_K2_GEMM_TPC")) tpc = std::strtol(u, nullptr, 10);
+        if (const char* u = std::getenv("MCND_K2_GEMM_PWAVES")) pwaves = std::strtol(u, nullptr, 10);
+        const int sm4 = (int)(3 * MS_STAGE * sizeof(double));
+        cudaFuncSetAttribute(k2_gemm_w4_kernel<64, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm4);
+        cudaFuncSetAttribute(k2_gemm_w4_kernel<128, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm4);
+    }
+    auto launch_w4 = [&](int64_t per_cta) {
+        const size_t sm4 = (size_t)3 * MS_STAGE * sizeof(double);
+        const int g4 = (int)(per_cta > 0 ? (tiles + per_cta - 1) / per_cta : std::min<int64_t>(tiles, 2 * (int64_t)sms));
+        if (K == 64) k2_gemm_w4_kernel<64, 3><<<g4, W4_THREADS, sm4, s>>>(ws, ld, rbase, M, N2, L, ldl, W, ldw, w, abort);
+        else k2_gemm_w4_kernel<128, 3><<<g4, W4_THREADS, sm4, s>>>(ws, ld, rbase, M, N2, L, ldl, W, ldw, w, abort);
+        return cudaGetLastError();
+    };
+    if (sm_budget < 0 && w4) return launch_w4(tpc >= 0 ? tpc : (tiles > pwaves * 2 * (int64_t)sms ? 0 : 1));
     if (sm_budget < 0) {  // one tile per CTA: SMs are released tile by tile (priority-scheduled overlap)
         const size_t smem_ms = (size_t)MS_ST * MS_STAGE * sizeof(double);
         const int grid_t = (int)std::min<int64_t>(tiles, 1 << 30);
@@ -571,6 +758,7 @@ cudaError_t k2_gemm(double* ws, int64_t ld, int32_t rbase, int32_t M, int32_t N2
         k2_gemm_ms_kernel<128, 1, 64><<<(int)tiles_n, 128, smem_n, s>>>(ws, ld, rbase, M, N2, L, ldl, W, ldw, w, abort);
         return cudaGetLastError();
     }
+    if (ms_mode && w4) return launch_w4(0);
     if (ms_mode) {
         const size_t smem_ms = (size_t)MS_ST * MS_STAGE * sizeof(double);
         // one tile per CTA (measured faster than a persistent grid: CTAs of the next
