@@ -509,56 +509,66 @@ __global__ void __launch_bounds__(W4_THREADS, 2) k2_gemm_w4_kernel(double* __res
     const int T = ntn * ntm;  // < 2^31 tiles for any n the panel kernel accepts
     const int t_begin = (int)((int64_t)T * blockIdx.x / gridDim.x), t_end = (int)((int64_t)T * (blockIdx.x + 1) / gridDim.x);
     if (t_begin >= t_end) return;
-    const int nst = (t_end - t_begin) * KS;
 
-    // per thread: L rows tid/8 + 16u (u < 4), 16-byte chunk tid%8; W rows tid/64 + 2u (u < 8),
-    // chunk tid%64; out-of-range chunks are zero-filled (no branches)
-    auto load_stage = [&](int j) {
-        if (j < nst) {
-            const int t = t_begin + j / KS;
-            const int kk = (j % KS) * MS_BK;
-            const int row0 = (t / ntn) * BM, col0 = (t % ntn) * BN;
-            double* ls = sh + (j % S) * MS_STAGE;
+    // Loader state (advanced incrementally: no divisions per stage).  Per thread: L rows
+    // tid/8 + 16u (u < 4), 16-byte chunk tid%8; W rows tid/64 + 2u (u < 8), chunk tid%64;
+    // out-of-range chunks are zero-filled.
+    const int ra = tid >> 3, ca = 2 * (tid & 7), kb = tid >> 6, cb = 2 * (tid & 63);
+    int l_t = t_begin, l_ks = 0, l_slot = 0;
+    const double* l_src = nullptr;  // L + row(u = 0) * ldl + kk + ca
+    const double* w_src = nullptr;  // W + (kk + kb) * ldw + col
+    unsigned l_ok = 0;              // bit u: row u in range; bit 4: column chunk in range
+    auto l_tile = [&]() {
+        const int row0 = (l_t / ntn) * BM, col0 = (l_t % ntn) * BN;
+        l_ok = 0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) l_ok |= (unsigned)(row0 + ra + 16 * u < M) << u;
+        const bool okc = col0 + cb < N2;
+        l_ok |= (unsigned)okc << 4;
+        l_src = L + (int64_t)(row0 + ra) * ldl + ca;
+        w_src = W + (int64_t)kb * ldw + (okc ? col0 + cb : 0);
+    };
+    auto load_next = [&]() {  // one stage -> slot l_slot, then advance
+        if (l_t < t_end) {
+            double* ls = sh + l_slot * MS_STAGE;
             double* wsm = ls + BM * MS_LDL;
-            const int ra = tid >> 3, ca = 2 * (tid & 7);
+            const int kk = l_ks * MS_BK;
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                const int r = row0 + ra + 16 * u;
-                const bool ok = r < M;
-                cp_async16_zf(ls + (ra + 16 * u) * MS_LDL + ca, L + (int64_t)(ok ? r : 0) * ldl + kk + ca, ok);
+                const bool ok = (l_ok >> u) & 1u;
+                cp_async16_zf(ls + (ra + 16 * u) * MS_LDL + ca, ok ? l_src + (int64_t)(16 * u) * ldl + kk : L, ok);
             }
-            const int kb = tid >> 6, cb = 2 * (tid & 63);
-            const bool okc = col0 + cb < N2;
-            const double* wsrc = W + (int64_t)(kk + kb) * ldw + (okc ? col0 + cb : 0);
+            const bool okc = (l_ok >> 4) & 1u;
+            const double* wsrc = w_src + (int64_t)kk * ldw;
 #pragma unroll
             for (int u = 0; u < 8; ++u) cp_async16_zf(wsm + (kb + 2 * u) * LDWS + cb, wsrc + (int64_t)(2 * u) * ldw, okc);
+            if (++l_ks == KS) {
+                l_ks = 0;
+                if (++l_t < t_end) l_tile();
+            }
         }
-        asm volatile("cp.async.commit_group;" ::: "memory");
+        asm volatile("cp.async.commit_group;" ::: "memory");  // (possibly empty) group keeps the count
+        l_slot = l_slot + 1 == S ? 0 : l_slot + 1;
     };
-    auto prefetch_c = [&](int t) {
-        const int row0 = (t / ntn) * BM, col0 = (t % ntn) * BN;
+    auto prefetch_c = [&](int row0, int col0) {
 #pragma unroll
         for (int i = 0; i < MI; ++i) {
             const int r = row0 + wm * 32 + i * 8 + g;
-            if (r < M) {  // the warp's 64 columns of row r: four 128-byte lines
-                const int c = col0 + wn * 64 + q * 16;
-                if (c < N2) asm volatile("prefetch.global.L2 [%0];" ::"l"(ws + (int64_t)(rbase + r) * ld + c));
-            }
+            const int c = col0 + wn * 64 + q * 16;  // the warp's 64 columns of row r: four 128-byte lines
+            if (r < M && c < N2) asm volatile("prefetch.global.L2 [%0];" ::"l"(ws + (int64_t)(rbase + r) * ld + c));
         }
     };
     double a[2][MI], b[2][NJ];
-    auto load_frags = [&](int buf, int j, int k0) {
-        const double* ls = sh + (int)(j % S) * MS_STAGE;
+    auto load_frags = [&](int buf, int slot, int k0) {
+        const double* ls = sh + slot * MS_STAGE;
         const double* wsm = ls + BM * MS_LDL;
 #pragma unroll
         for (int i = 0; i < MI; ++i) a[buf][i] = ls[(wm * 32 + i * 8 + g) * MS_LDL + k0 + q];
 #pragma unroll
         for (int jj = 0; jj < NJ; ++jj) b[buf][jj] = wsm[(k0 + q) * LDWS + wn * 64 + jj * 8 + g];
     };
-
     double acc[MI][NJ][2];
-    auto load_c = [&](int t) {  // C tile -> accumulators (acc = C - L W)
-        const int row0 = (t / ntn) * BM, col0 = (t % ntn) * BN;
+    auto load_c = [&](int row0, int col0) {  // C tile -> accumulators (acc = C - L W)
         const bool full = row0 + BM <= M && col0 + BN <= N2;
 #pragma unroll
         for (int i = 0; i < MI; ++i) {
@@ -577,39 +587,47 @@ __global__ void __launch_bounds__(W4_THREADS, 2) k2_gemm_w4_kernel(double* __res
             }
         }
     };
-    prefetch_c(t_begin);
+
+    l_tile();
+    int t = t_begin, row0 = (t / ntn) * BM, col0 = (t % ntn) * BN;
+    prefetch_c(row0, col0);
 #pragma unroll
-    for (int j = 0; j < S; ++j) load_stage(j);
-    load_c(t_begin);  // in flight together with the first stages
+    for (int j = 0; j < S; ++j) load_next();
+    load_c(row0, col0);  // in flight together with the first stages
     asm volatile("cp.async.wait_group %0;" ::"n"(S - 1) : "memory");
     __syncthreads();
     load_frags(0, 0, 0);
     double rmx[MI] = {0.0, 0.0, 0.0, 0.0};
-    for (int j = 0; j < nst; ++j) {
-        const int t = t_begin + j / KS;
-        const int ks = j % KS;
-        const int row0 = (t / ntn) * BM, col0 = (t % ntn) * BN;
-        if (ks == 0 && j > 0) load_c(t);
-        if (ks == KS / 2 && t + 1 < t_end) prefetch_c(t + 1);
-#pragma unroll
-        for (int kq = 0; kq < MS_BK / 4; ++kq) {
-            if (kq == MS_BK / 4 - 1) {
-                // stage j+1 landed; every warp is done reading stage j (its last
-                // fragments are in registers), so its buffer takes stage j+S
-                asm volatile("cp.async.wait_group %0;" ::"n"(S - 2) : "memory");
-                __syncthreads();
-                load_stage(j + S);
-                if (j + 1 < nst) load_frags((kq + 1) & 1, j + 1, 0);
-            } else {
-                load_frags((kq + 1) & 1, j, 4 * (kq + 1));
+    int c_slot = 0;
+    for (;;) {
+#pragma unroll 1
+        for (int ks = 0; ks < KS; ++ks) {
+            if (ks == KS / 2 && t + 1 < t_end) {
+                const int tn = t + 1;
+                prefetch_c((tn / ntn) * BM, (tn % ntn) * BN);
             }
+            const int n_slot = c_slot + 1 == S ? 0 : c_slot + 1;
+            const bool more = ks + 1 < KS || t + 1 < t_end;
 #pragma unroll
-            for (int i = 0; i < MI; ++i)
+            for (int kq = 0; kq < MS_BK / 4; ++kq) {
+                if (kq == MS_BK / 4 - 1) {
+                    // the next stage landed; every warp is done reading this one (its last
+                    // fragments are in registers), so its slot takes the stage S ahead
+                    asm volatile("cp.async.wait_group %0;" ::"n"(S - 2) : "memory");
+                    __syncthreads();
+                    load_next();
+                    if (more) load_frags((kq + 1) & 1, n_slot, 0);
+                } else {
+                    load_frags((kq + 1) & 1, c_slot, 4 * (kq + 1));
+                }
 #pragma unroll
-                for (int jj = 0; jj < NJ; ++jj) dmma(acc[i][jj][0], acc[i][jj][1], a[kq & 1][i], b[kq & 1][jj]);
+                for (int i = 0; i < MI; ++i)
+#pragma unroll
+                    for (int jj = 0; jj < NJ; ++jj) dmma(acc[i][jj][0], acc[i][jj][1], a[kq & 1][i], b[kq & 1][jj]);
+            }
+            c_slot = n_slot;
         }
-        if (ks != KS - 1) continue;
-        const int bm = t / ntn;
+        // epilogue: store the tile, fold the row maxima
         const bool full = row0 + BM <= M && col0 + BN <= N2;
 #pragma unroll
         for (int i = 0; i < MI; ++i) {
@@ -627,18 +645,25 @@ __global__ void __launch_bounds__(W4_THREADS, 2) k2_gemm_w4_kernel(double* __res
                 }
             }
         }
-        const bool flush = (t + 1 == t_end) || ((t + 1) / ntn != bm);
-        if (flush && wit) {
+        const int prow0 = row0;
+        ++t;
+        if (t < t_end) {
+            row0 = (t / ntn) * BM;
+            col0 = (t % ntn) * BN;
+        }
+        if ((t == t_end || row0 != prow0) && wit) {
 #pragma unroll
             for (int i = 0; i < MI; ++i) {
                 double mx = rmx[i];
                 mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
                 mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-                const int r = row0 + wm * 32 + i * 8 + g;
+                const int r = prow0 + wm * 32 + i * 8 + g;
                 if (q == 0 && r < M) atomicMax(wit + rbase + r, (unsigned long long)__double_as_longlong(mx));
                 rmx[i] = 0.0;
             }
         }
+        if (t == t_end) break;
+        load_c(row0, col0);
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
 }
