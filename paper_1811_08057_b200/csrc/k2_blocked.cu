@@ -492,56 +492,60 @@ __global__ void __launch_bounds__(64 * (BNT / 32) * SUB, 2 / SUB) k2_gemm_ms_ker
 // epilogue, barrier) is covered by the other.  Same arithmetic as k2_gemm_ms_kernel
 // (acc starts at C, DMMA k-steps in k order): bitwise the same result.
 constexpr int W4_THREADS = 128;
-template <int K, int S>
-__global__ void __launch_bounds__(W4_THREADS, 2) k2_gemm_w4_kernel(double* __restrict__ ws, int64_t ld, int32_t rbase,
+// WN = warps in N: 2 -> 64 x 128 tiles, 128 threads (the trailing update); 1 -> 64 x 64 tiles,
+// 64 threads (the short critical-path update: twice the CTAs)
+template <int K, int S, int WN = 2>
+__global__ void __launch_bounds__(64 * WN, 2) k2_gemm_w4_kernel(double* __restrict__ ws, int64_t ld, int32_t rbase,
                                                                     int32_t M, int32_t N2, const double* __restrict__ L,
                                                                     int64_t ldl, const double* __restrict__ W, int64_t ldw,
                                                                     unsigned long long* __restrict__ wit,
                                                                     const unsigned* __restrict__ abort) {
     constexpr int KS = K / MS_BK;
     constexpr int MI = 4, NJ = 8;  // warp tile 32 x 64
+    constexpr int NTH = 64 * WN, BNW = 64 * WN, LDW = BNW + 4, STG = BM * MS_LDL + MS_BK * LDW;
+    constexpr int LR = BM * (MS_BK / 2) / NTH;  // L chunks per thread (rows NTH/8 apart)
     extern __shared__ __align__(16) double sh[];
     if (*(volatile const unsigned*)abort) return;
     const int tid = (int)threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int wm = warp >> 1, wn = warp & 1;
+    const int wm = warp / WN, wn = warp % WN;
     const int g = lane >> 2, q = lane & 3;
-    const int ntn = (N2 + BN - 1) / BN, ntm = (M + BM - 1) / BM;
+    const int ntn = (N2 + BNW - 1) / BNW, ntm = (M + BM - 1) / BM;
     const int T = ntn * ntm;  // < 2^31 tiles for any n the panel kernel accepts
     const int t_begin = (int)((int64_t)T * blockIdx.x / gridDim.x), t_end = (int)((int64_t)T * (blockIdx.x + 1) / gridDim.x);
     if (t_begin >= t_end) return;
 
     // Loader state (advanced incrementally: no divisions per stage).  Per thread: L rows
-    // tid/8 + 16u (u < 4), 16-byte chunk tid%8; W rows tid/64 + 2u (u < 8), chunk tid%64;
-    // out-of-range chunks are zero-filled.
-    const int ra = tid >> 3, ca = 2 * (tid & 7), kb = tid >> 6, cb = 2 * (tid & 63);
+    // tid/8 + (NTH/8)u (u < LR), 16-byte chunk tid%8; W rows tid/(BNW/2) + 2u (u < 8), chunk
+    // tid%(BNW/2); out-of-range chunks are zero-filled.
+    const int ra = tid >> 3, ca = 2 * (tid & 7), kb = tid / (BNW / 2), cb = 2 * (tid % (BNW / 2));
     int l_t = t_begin, l_ks = 0, l_slot = 0;
     const double* l_src = nullptr;  // L + row(u = 0) * ldl + kk + ca
     const double* w_src = nullptr;  // W + (kk + kb) * ldw + col
     unsigned l_ok = 0;              // bit u: row u in range; bit 4: column chunk in range
     auto l_tile = [&]() {
-        const int row0 = (l_t / ntn) * BM, col0 = (l_t % ntn) * BN;
+        const int row0 = (l_t / ntn) * BM, col0 = (l_t % ntn) * BNW;
         l_ok = 0;
 #pragma unroll
-        for (int u = 0; u < 4; ++u) l_ok |= (unsigned)(row0 + ra + 16 * u < M) << u;
+        for (int u = 0; u < LR; ++u) l_ok |= (unsigned)(row0 + ra + (NTH / 8) * u < M) << u;
         const bool okc = col0 + cb < N2;
-        l_ok |= (unsigned)okc << 4;
+        l_ok |= (unsigned)okc << 8;
         l_src = L + (int64_t)(row0 + ra) * ldl + ca;
         w_src = W + (int64_t)kb * ldw + (okc ? col0 + cb : 0);
     };
     auto load_next = [&]() {  // one stage -> slot l_slot, then advance
         if (l_t < t_end) {
-            double* ls = sh + l_slot * MS_STAGE;
+            double* ls = sh + l_slot * STG;
             double* wsm = ls + BM * MS_LDL;
             const int kk = l_ks * MS_BK;
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < LR; ++u) {
                 const bool ok = (l_ok >> u) & 1u;
-                cp_async16_zf(ls + (ra + 16 * u) * MS_LDL + ca, ok ? l_src + (int64_t)(16 * u) * ldl + kk : L, ok);
+                cp_async16_zf(ls + (ra + (NTH / 8) * u) * MS_LDL + ca, ok ? l_src + (int64_t)((NTH / 8) * u) * ldl + kk : L, ok);
             }
-            const bool okc = (l_ok >> 4) & 1u;
+            const bool okc = (l_ok >> 8) & 1u;
             const double* wsrc = w_src + (int64_t)kk * ldw;
 #pragma unroll
-            for (int u = 0; u < 8; ++u) cp_async16_zf(wsm + (kb + 2 * u) * LDWS + cb, wsrc + (int64_t)(2 * u) * ldw, okc);
+            for (int u = 0; u < 8; ++u) cp_async16_zf(wsm + (kb + 2 * u) * LDW + cb, wsrc + (int64_t)(2 * u) * ldw, okc);
             if (++l_ks == KS) {
                 l_ks = 0;
                 if (++l_t < t_end) l_tile();
@@ -560,16 +564,16 @@ __global__ void __launch_bounds__(W4_THREADS, 2) k2_gemm_w4_kernel(double* __res
     };
     double a[2][MI], b[2][NJ];
     auto load_frags = [&](int buf, int slot, int k0) {
-        const double* ls = sh + slot * MS_STAGE;
+        const double* ls = sh + slot * STG;
         const double* wsm = ls + BM * MS_LDL;
 #pragma unroll
         for (int i = 0; i < MI; ++i) a[buf][i] = ls[(wm * 32 + i * 8 + g) * MS_LDL + k0 + q];
 #pragma unroll
-        for (int jj = 0; jj < NJ; ++jj) b[buf][jj] = wsm[(k0 + q) * LDWS + wn * 64 + jj * 8 + g];
+        for (int jj = 0; jj < NJ; ++jj) b[buf][jj] = wsm[(k0 + q) * LDW + wn * 64 + jj * 8 + g];
     };
     double acc[MI][NJ][2];
     auto load_c = [&](int row0, int col0) {  // C tile -> accumulators (acc = C - L W)
-        const bool full = row0 + BM <= M && col0 + BN <= N2;
+        const bool full = row0 + BM <= M && col0 + BNW <= N2;
 #pragma unroll
         for (int i = 0; i < MI; ++i) {
             const int r = row0 + wm * 32 + i * 8 + g;
@@ -589,7 +593,7 @@ __global__ void __launch_bounds__(W4_THREADS, 2) k2_gemm_w4_kernel(double* __res
     };
 
     l_tile();
-    int t = t_begin, row0 = (t / ntn) * BM, col0 = (t % ntn) * BN;
+    int t = t_begin, row0 = (t / ntn) * BM, col0 = (t % ntn) * BNW;
     prefetch_c(row0, col0);
 #pragma unroll
     for (int j = 0; j < S; ++j) load_next();
@@ -604,7 +608,7 @@ __global__ void __launch_bounds__(W4_THREADS, 2) k2_gemm_w4_kernel(double* __res
         for (int ks = 0; ks < KS; ++ks) {
             if (ks == KS / 2 && t + 1 < t_end) {
                 const int tn = t + 1;
-                prefetch_c((tn / ntn) * BM, (tn % ntn) * BN);
+                prefetch_c((tn / ntn) * BM, (tn % ntn) * BNW);
             }
             const int n_slot = c_slot + 1 == S ? 0 : c_slot + 1;
             const bool more = ks + 1 < KS || t + 1 < t_end;
@@ -628,7 +632,7 @@ __global__ void __launch_bounds__(W4_THREADS, 2) k2_gemm_w4_kernel(double* __res
             c_slot = n_slot;
         }
         // epilogue: store the tile, fold the row maxima
-        const bool full = row0 + BM <= M && col0 + BN <= N2;
+        const bool full = row0 + BM <= M && col0 + BNW <= N2;
 #pragma unroll
         for (int i = 0; i < MI; ++i) {
             const int r = row0 + wm * 32 + i * 8 + g;
@@ -649,7 +653,7 @@ __global__ void __launch_bounds__(W4_THREADS, 2) k2_gemm_w4_kernel(double* __res
         ++t;
         if (t < t_end) {
             row0 = (t / ntn) * BM;
-            col0 = (t % ntn) * BN;
+            col0 = (t % ntn) * BNW;
         }
         if ((t == t_end || row0 != prow0) && wit) {
 #pragma unroll
@@ -772,7 +776,21 @@ cudaError_t k2_gemm(double* ws, int64_t ld, int32_t rbase, int32_t M, int32_t N2
         else k2_gemm_ms_kernel<128, 2><<<grid_f, 2 * MS_THREADS, 2 * smem_ms, s>>>(ws, ld, rbase, M, N2, L, ldl, W, ldw, w, abort);
         return cudaGetLastError();
     }
-    if (ms_mode && M <= 2 * BM && K == 128) {  // a short critical-path update: 64-wide tiles, twice the CTAs
+    // MCND_K2_GEMM_CRIT_W4=1: the 4-warp kernel with 64-wide tiles for this update (measured: no gain,
+    // 24.6 vs 25.1 us standalone at m = 8000 and slower inside C3/C5)
+    static const long crit_w4 = [] { const char* v = std::getenv("MCND_K2_GEMM_CRIT_W4"); return v ? std::strtol(v, nullptr, 10) : 0L; }();
+    if (ms_mode && M <= 2 * BM && K == 128 && w4 && crit_w4) {  // a short critical-path update: 64-wide tiles, twice the CTAs
+        const int sm1 = (int)(3 * (BM * MS_LDL + MS_BK * (64 + 4)) * sizeof(double));
+        static bool attr1 = false;
+        if (!attr1) {
+            cudaFuncSetAttribute(k2_gemm_w4_kernel<128, 3, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm1);
+            attr1 = true;
+        }
+        const int64_t tiles_n = (int64_t)((N2 + 63) / 64) * ((M + BM - 1) / BM);
+        k2_gemm_w4_kernel<128, 3, 1><<<(int)tiles_n, 64, sm1, s>>>(ws, ld, rbase, M, N2, L, ldl, W, ldw, w, abort);
+        return cudaGetLastError();
+    }
+    if (ms_mode && M <= 2 * BM && K == 128) {
         static bool attr = false;
         const size_t smem_n = (size_t)MS_ST * (BM * MS_LDL + MS_BK * (64 + 8)) * sizeof(double);
         if (!attr) {

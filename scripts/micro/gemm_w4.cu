@@ -72,6 +72,21 @@ int main(int argc, char** argv) {
     run_w4(std::integral_constant<int, 3>{});
     run_w4(std::integral_constant<int, 4>{});
 
+    {   // the critical-path shape: 128 rows x n, 64-wide tiles (8-warp-era kernel vs WN = 1)
+        const int M2 = 128;
+        const size_t sm64 = (size_t)mcnd::MS_ST * (mcnd::BM * mcnd::MS_LDL + mcnd::MS_BK * (64 + 4)) * 8;
+        const size_t sm1 = (size_t)3 * (mcnd::BM * mcnd::MS_LDL + mcnd::MS_BK * (64 + 4)) * 8;
+        cudaFuncSetAttribute(mcnd::k2_gemm_ms_kernel<K, 1, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm64);
+        cudaFuncSetAttribute(mcnd::k2_gemm_w4_kernel<K, 3, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1);
+        const int tn = ((n + 63) / 64) * 2;
+        auto f0 = [&]() { mcnd::k2_gemm_ms_kernel<K, 1, 64><<<tn, 128, sm64>>>(ws, ld, 0, M2, n, L, K, W, ld, w, abort); };
+        auto f1 = [&]() { mcnd::k2_gemm_w4_kernel<K, 3, 1><<<tn, 64, sm1>>>(ws, ld, 0, M2, n, L, K, W, ld, w, abort); };
+        const double fl2 = 2.0 * M2 * (double)n * K;
+        float t0 = timeit(f0, ws, bytes, 20), t1 = timeit(f1, ws, bytes, 20);
+        printf("128 rows: ms<64-wide> %.1f us (%.2f TF), w4<WN=1> %.1f us (%.2f TF)\n", t0 * 1e3, fl2 / t0 / 1e9, t1 * 1e3, fl2 / t1 / 1e9);
+        cudaMemcpy(ws, ws0, bytes, cudaMemcpyDeviceToDevice); f0(); cudaMemcpy(out_a, ws, bytes, cudaMemcpyDeviceToDevice);
+        cudaMemcpy(ws, ws0, bytes, cudaMemcpyDeviceToDevice); f1(); check("WN=1 vs ms 64-wide");
+    }
     cublasHandle_t h; cublasCreate(&h);
     const double one = 1.0, mone = -1.0;
     // row-major C(n x n, ld) -= L(n x K) W(K x n): column-major C^T = C^T - W^T L^T
