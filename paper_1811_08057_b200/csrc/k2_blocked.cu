@@ -494,16 +494,17 @@ __global__ void __launch_bounds__(64 * (BNT / 32) * SUB, 2 / SUB) k2_gemm_ms_ker
 constexpr int W4_THREADS = 128;
 // WN = warps in N: 2 -> 64 x 128 tiles, 128 threads (the trailing update); 1 -> 64 x 64 tiles,
 // 64 threads (the short critical-path update: twice the CTAs)
-template <int K, int S, int WN = 2>
+template <int K, int S, int WN = 2, int BK = MS_BK>
 __global__ void __launch_bounds__(64 * WN, 2) k2_gemm_w4_kernel(double* __restrict__ ws, int64_t ld, int32_t rbase,
                                                                     int32_t M, int32_t N2, const double* __restrict__ L,
                                                                     int64_t ldl, const double* __restrict__ W, int64_t ldw,
                                                                     unsigned long long* __restrict__ wit,
                                                                     const unsigned* __restrict__ abort) {
-    constexpr int KS = K / MS_BK;
+    constexpr int KS = K / BK, LDA = BK + 4;
     constexpr int MI = 4, NJ = 8;  // warp tile 32 x 64
-    constexpr int NTH = 64 * WN, BNW = 64 * WN, LDW = BNW + 4, STG = BM * MS_LDL + MS_BK * LDW;
-    constexpr int LR = BM * (MS_BK / 2) / NTH;  // L chunks per thread (rows NTH/8 apart)
+    constexpr int NTH = 64 * WN, BNW = 64 * WN, LDW = BNW + 4, STG = BM * LDA + BK * LDW;
+    constexpr int LR = BM * (BK / 2) / NTH;     // L chunks per thread (rows NTH/(BK/2) apart)
+    constexpr int WR = BK * (BNW / 2) / NTH;    // W chunks per thread (rows 2 apart)
     extern __shared__ __align__(16) double sh[];
     if (*(volatile const unsigned*)abort) return;
     const int tid = (int)threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -517,7 +518,7 @@ __global__ void __launch_bounds__(64 * WN, 2) k2_gemm_w4_kernel(double* __restri
     // Loader state (advanced incrementally: no divisions per stage).  Per thread: L rows
     // tid/8 + (NTH/8)u (u < LR), 16-byte chunk tid%8; W rows tid/(BNW/2) + 2u (u < 8), chunk
     // tid%(BNW/2); out-of-range chunks are zero-filled.
-    const int ra = tid >> 3, ca = 2 * (tid & 7), kb = tid / (BNW / 2), cb = 2 * (tid % (BNW / 2));
+    const int ra = tid / (BK / 2), ca = 2 * (tid % (BK / 2)), kb = tid / (BNW / 2), cb = 2 * (tid % (BNW / 2));
     int l_t = t_begin, l_ks = 0, l_slot = 0;
     const double* l_src = nullptr;  // L + row(u = 0) * ldl + kk + ca
     const double* w_src = nullptr;  // W + (kk + kb) * ldw + col
@@ -526,26 +527,26 @@ __global__ void __launch_bounds__(64 * WN, 2) k2_gemm_w4_kernel(double* __restri
         const int row0 = (l_t / ntn) * BM, col0 = (l_t % ntn) * BNW;
         l_ok = 0;
 #pragma unroll
-        for (int u = 0; u < LR; ++u) l_ok |= (unsigned)(row0 + ra + (NTH / 8) * u < M) << u;
+        for (int u = 0; u < LR; ++u) l_ok |= (unsigned)(row0 + ra + (NTH / (BK / 2)) * u < M) << u;
         const bool okc = col0 + cb < N2;
-        l_ok |= (unsigned)okc << 8;
+        l_ok |= (unsigned)okc << 16;
         l_src = L + (int64_t)(row0 + ra) * ldl + ca;
         w_src = W + (int64_t)kb * ldw + (okc ? col0 + cb : 0);
     };
     auto load_next = [&]() {  // one stage -> slot l_slot, then advance
         if (l_t < t_end) {
             double* ls = sh + l_slot * STG;
-            double* wsm = ls + BM * MS_LDL;
-            const int kk = l_ks * MS_BK;
+            double* wsm = ls + BM * LDA;
+            const int kk = l_ks * BK;
 #pragma unroll
             for (int u = 0; u < LR; ++u) {
                 const bool ok = (l_ok >> u) & 1u;
-                cp_async16_zf(ls + (ra + (NTH / 8) * u) * MS_LDL + ca, ok ? l_src + (int64_t)((NTH / 8) * u) * ldl + kk : L, ok);
+                cp_async16_zf(ls + (ra + (NTH / (BK / 2)) * u) * LDA + ca, ok ? l_src + (int64_t)((NTH / (BK / 2)) * u) * ldl + kk : L, ok);
             }
-            const bool okc = (l_ok >> 8) & 1u;
+            const bool okc = (l_ok >> 16) & 1u;
             const double* wsrc = w_src + (int64_t)kk * ldw;
 #pragma unroll
-            for (int u = 0; u < 8; ++u) cp_async16_zf(wsm + (kb + 2 * u) * LDW + cb, wsrc + (int64_t)(2 * u) * ldw, okc);
+            for (int u = 0; u < WR; ++u) cp_async16_zf(wsm + (kb + 2 * u) * LDW + cb, wsrc + (int64_t)(2 * u) * ldw, okc);
             if (++l_ks == KS) {
                 l_ks = 0;
                 if (++l_t < t_end) l_tile();
@@ -565,9 +566,9 @@ __global__ void __launch_bounds__(64 * WN, 2) k2_gemm_w4_kernel(double* __restri
     double a[2][MI], b[2][NJ];
     auto load_frags = [&](int buf, int slot, int k0) {
         const double* ls = sh + slot * STG;
-        const double* wsm = ls + BM * MS_LDL;
+        const double* wsm = ls + BM * LDA;
 #pragma unroll
-        for (int i = 0; i < MI; ++i) a[buf][i] = ls[(wm * 32 + i * 8 + g) * MS_LDL + k0 + q];
+        for (int i = 0; i < MI; ++i) a[buf][i] = ls[(wm * 32 + i * 8 + g) * LDA + k0 + q];
 #pragma unroll
         for (int jj = 0; jj < NJ; ++jj) b[buf][jj] = wsm[(k0 + q) * LDW + wn * 64 + jj * 8 + g];
     };
@@ -613,8 +614,8 @@ __global__ void __launch_bounds__(64 * WN, 2) k2_gemm_w4_kernel(double* __restri
             const int n_slot = c_slot + 1 == S ? 0 : c_slot + 1;
             const bool more = ks + 1 < KS || t + 1 < t_end;
 #pragma unroll
-            for (int kq = 0; kq < MS_BK / 4; ++kq) {
-                if (kq == MS_BK / 4 - 1) {
+            for (int kq = 0; kq < BK / 4; ++kq) {
+                if (kq == BK / 4 - 1) {
                     // the next stage landed; every warp is done reading this one (its last
                     // fragments are in registers), so its slot takes the stage S ahead
                     asm volatile("cp.async.wait_group %0;" ::"n"(S - 2) : "memory");
@@ -792,7 +793,7 @@ cudaError_t k2_gemm(double* ws, int64_t ld, int32_t rbase, int32_t M, int32_t N2
     }
     if (ms_mode && M <= 2 * BM && K == 128) {
         static bool attr = false;
-        const size_t smem_n = (size_t)MS_ST * (BM * MS_LDL + MS_BK * (64 + 8)) * sizeof(double);
+        const size_t smem_n = (size_t)MS_ST * (BM * MS_LDL + MS_BK * (64 + 4)) * sizeof(double);
         if (!attr) {
             cudaFuncSetAttribute(k2_gemm_ms_kernel<128, 1, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_n);
             attr = true;

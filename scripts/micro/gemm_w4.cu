@@ -70,7 +70,16 @@ int main(int argc, char** argv) {
         }
     };
     run_w4(std::integral_constant<int, 3>{});
-    run_w4(std::integral_constant<int, 4>{});
+    {   // K per stage 32 (one barrier per 8 k-steps), 2 stages
+        const size_t sm = (size_t)2 * (mcnd::BM * 36 + 32 * mcnd::LDWS) * 8;
+        cudaFuncSetAttribute(mcnd::k2_gemm_w4_kernel<K, 2, 2, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        for (int grid : {(int)T, 2 * sms}) {
+            auto f = [&]() { mcnd::k2_gemm_w4_kernel<K, 2, 2, 32><<<grid, mcnd::W4_THREADS, sm>>>(ws, ld, 0, n, n, L, K, W, ld, w, abort); };
+            float tt = timeit(f, ws, bytes);
+            printf("w4 BK=32 S=2 grid %6d: %.3f ms %.2f TFLOP/s\n", grid, tt, fl / tt / 1e9);
+            cudaMemcpy(ws, ws0, bytes, cudaMemcpyDeviceToDevice); f(); check("vs ms");
+        }
+    }
 
     {   // the critical-path shape: 128 rows x n, 64-wide tiles (8-warp-era kernel vs WN = 1)
         const int M2 = 128;
