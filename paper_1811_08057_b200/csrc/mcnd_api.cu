@@ -68,6 +68,9 @@ struct Buffers {
     cudaStream_t crit = nullptr;                 // K2: the panel chain (highest priority)
     cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_c = nullptr;  // K2: stream joins
     cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+    cudaStream_t cpy = nullptr;                  // K2 host input: row chunks copied while the first pairs run
+    static constexpr int kMaxChunks = 16;
+    cudaEvent_t ev_arr[kMaxChunks] = {};
     int sms = 0;
     uint32_t epoch = 0;
     std::map<std::pair<int64_t, int64_t>, bool> kp_cluster_cache;  // (G, cw) -> co-residency
@@ -96,8 +99,11 @@ int init_buffers(Buffers& b, int dev) {
         cudaEventCreateWithFlags(&b.ev_in, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&b.ev_out, cudaEventDisableTiming) != cudaSuccess ||
         cudaStreamCreateWithPriority(&b.side, cudaStreamNonBlocking, prio_lo) != cudaSuccess ||
-        cudaStreamCreateWithPriority(&b.crit, cudaStreamNonBlocking, prio_hi) != cudaSuccess)
+        cudaStreamCreateWithPriority(&b.crit, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&b.cpy, cudaStreamNonBlocking) != cudaSuccess)
         return fail(MCND_ECUDA, "cudaEventCreate/cudaStreamCreate failed");
+    for (auto& ev : b.ev_arr)
+        if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) return fail(MCND_ECUDA, "cudaEventCreate failed");
     return MCND_OK;
 }
 
@@ -692,9 +698,9 @@ int stage_input(Buffers& B, const double* h_a, int64_t rows, int64_t n, int64_t 
 // launches are asynchronous; a failed witness test raises a device abort flag
 // that turns every later launch into a no-op; one D2H at the end.
 int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaStream_t st_caller, mcnd_logdet* out,
-                double* pivots_out, int32_t* cols_out) {
+                double* pivots_out, int32_t* cols_out, const double* h_src = nullptr) {
     clear_out(out);
-    int rc = check_shape(d_a, n, lda);
+    int rc = check_shape(h_src ? h_src : d_a, n, lda);
     if (rc) return rc;
     int code = MCND_OK;
     Buffers* B = buffers_for_current(&code);
@@ -723,6 +729,63 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
         return fail(MCND_EINVAL, "n=%lld too large for the one-GPU blocked path (at most %d panel columns per SM); "
                     "use logdet_condensation (unblocked)", (long long)n, kKPMaxCw);
 
+    // Streamed host input (a pinned host matrix, the pair schedule with look-ahead): the rows
+    // arrive in chunks on a copy stream while the first pairs run.  A pair's side update
+    // covers only the chunks expected to have landed by then (a static plan from the copy
+    // rate and the pair times; a late chunk only makes the side stream wait for its event);
+    // a chunk first covered at pair q is caught up on the side stream first: its K1 init,
+    // then the updates of pairs 0..q-1 in order, each with that pair's own L/W/descriptor
+    // slot (kept alive: the slot ring grows to the last catch-up).  Every row sees the same
+    // kernels in the same order as with the matrix resident, so the result is bitwise the same.
+    int n_chunks = 1;
+    std::vector<int64_t> cr{0, n};  // chunk row boundaries
+    std::vector<int> cov_of;        // per pair: last chunk covered by its side update
+    int ring = 3;
+    if (h_src && env_long("MCND_K2_STREAM_IN", 1) != 0 && env_long("MCND_K2_PAIRS", 1) != 0 &&
+        env_long("MCND_K2_OVERLAP", 1) != 0 && env_long("MCND_K2_PRIO", 1) != 0 && env_long("MCND_K2_LA2", 1) != 0 &&
+        n_panels >= 8) {
+        cudaPointerAttributes pa{};
+        const bool pinned = cudaPointerGetAttributes(&pa, h_src) == cudaSuccess && pa.type == cudaMemoryTypeHost;
+        cudaGetLastError();
+        const int64_t rows_c = (int64_t)align_up((size_t)std::max<int64_t>(512, (n + Buffers::kMaxChunks - 1) / Buffers::kMaxChunks), 128);
+        if (pinned && rows_c < n) {
+            n_chunks = (int)((n + rows_c - 1) / rows_c);
+            cr.assign(1, 0);
+            for (int c = 0; c < n_chunks; ++c) cr.push_back(std::min<int64_t>(n, cr.back() + rows_c));
+            std::vector<double> arr(n_chunks);  // expected landing times (MCND_K2_STREAM_GBS, default 60 GB/s: C3 sweep 40: 36.7, 50: 35.9, 56: 35.3, 70: 35.2, 200: 37.1 ms e2e)
+            const double gbs = (double)env_long("MCND_K2_STREAM_GBS", 60) * 1e9;
+            double t = 0.0;
+            for (int c = 0; c < n_chunks; ++c) { t += (double)(cr[c + 1] - cr[c]) * (double)n * 8.0 / gbs; arr[c] = t; }
+            auto chunk_of = [&](int64_t row) { return (int)std::min<int64_t>(n_chunks - 1, row / rows_c); };
+            double tq = arr[0];
+            int cov = 0, q_last = 0;
+            for (int64_t k = 0, q = 0; k + 1 < n_panels; k += 2, ++q) {
+                const int64_t kb = k * b, m = n - kb, nr = m - 2 * b;
+                const double t_pan = 2.0 * 64 * 3.4e-6;
+                int c = std::max(cov, chunk_of(std::min<int64_t>(n, kb + 10 * b) - 1));  // through pair q+4's rows
+                while (c + 1 < n_chunks && arr[c + 1] <= tq + t_pan) ++c;
+                if (k + 3 >= n_panels) c = n_chunks - 1;  // the next unit is not a pair: everything
+                if (c > cov || q == 0) q_last = (int)q;
+                cov = c;
+                cov_of.push_back(c);
+                tq += std::max(t_pan, 2.0 * (double)nr * (double)(m - 2 * b) * 128.0 / 26e12) + 60e-6;
+            }
+            if (cov != n_chunks - 1) { n_chunks = 1; cr.assign({0, n}); cov_of.clear(); }
+            else ring = std::max(3, q_last + 3);
+        }
+    }
+    const bool streamed = n_chunks > 1;
+    const int64_t lda_h = lda;
+    if (h_src) {  // host input: staged in din (whole, or chunk by chunk when streamed)
+        rc = ensure_dev(&B->din, &B->din_bytes, (size_t)n * n * sizeof(double));
+        if (rc) return rc;
+        if (!streamed)
+            CUDA_TRY(cudaMemcpy2DAsync(B->din, (size_t)n * sizeof(double), h_src, (size_t)lda * sizeof(double),
+                                       (size_t)n * sizeof(double), (size_t)n, cudaMemcpyHostToDevice, st));
+        d_a = (const double*)B->din;
+        lda = n;
+    }
+
     // device layout
     size_t off = 0;
     auto take = [&](size_t bytes) { size_t o = off; off = align_up(off + bytes, 256); return o; };
@@ -731,7 +794,7 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
     const size_t o_rec = take((size_t)n * sizeof(PivRec));
     // L, W, Wp and the pair's gather descriptor in a ring of kRing pair slots: the side update
     // of pair q may still read its slot while pairs q+1 and q+2 factor (depth-2 look-ahead)
-    constexpr int kRing = 3;
+    const int kRing = ring;
     const size_t o_L = take((size_t)kRing * std::max<int64_t>(n, 1) * 2 * b * sizeof(double));
     const size_t o_W = take((size_t)kRing * 2 * b * ld * sizeof(double));
     const size_t o_pan = take((2 + kRing) * sizeof(K2Gather));           // gp0, gp1, gpair ring
@@ -742,7 +805,8 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
     const size_t o_lastb = take(kLastBufBytes);
     const size_t o_ctl = take(sizeof(K1Err) + 16);
     // int metadata: iota[n] | never[n] | panel_ptr[b+1] | init_ptr[G0+1] init_rows[n] | tail_ptr[Gt+1] tail_rows[mt]
-    const size_t n_int = (size_t)(n + n + (b + 1) + (G0 + 1) + n + (Gt + 1) + mt);
+    //               | per-chunk init_ptr[n_chunks][G0+1] (streamed input; rows dealt inside init_rows)
+    const size_t n_int = (size_t)(n + n + (b + 1) + (G0 + 1) + n + (Gt + 1) + mt + (streamed ? n_chunks * (G0 + 1) : 0));
     const size_t o_int = take(n_int * sizeof(int32_t));
     rc = ensure_dev(&B->dws, &B->dws_bytes, off);
     if (rc) return rc;
@@ -765,7 +829,16 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
         std::vector<int32_t> fill(ptr, ptr + G);
         for (int64_t i = 0; i < count; ++i) rows[fill[(size_t)(i % G)]++] = (int32_t)(first + i);
     };
-    deal(0, n, G0, h_iptr, h_irows);
+    int32_t* h_cptr = h_trows + mt;
+    if (streamed) {
+        for (int c = 0; c < n_chunks; ++c) {
+            int32_t* ptr = h_cptr + (size_t)c * (G0 + 1);
+            deal(cr[c], cr[c + 1] - cr[c], G0, ptr, h_irows + cr[c]);
+            for (int64_t g = 0; g <= G0; ++g) ptr[g] += (int32_t)cr[c];
+        }
+    } else {
+        deal(0, n, G0, h_iptr, h_irows);
+    }
     deal(kb_end, mt, Gt, h_tptr, h_trows);
     CUDA_TRY(cudaMemcpyAsync(base + o_int, hi, n_int * sizeof(int32_t), cudaMemcpyHostToDevice, st));
     CUDA_TRY(cudaMemsetAsync(base + o_rec, 0, (size_t)n * sizeof(PivRec), st));
@@ -781,6 +854,7 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
     const int32_t* d_irows = d_iptr + (G0 + 1);
     const int32_t* d_tptr = d_irows + n;
     const int32_t* d_trows = d_tptr + (Gt + 1);
+    const int32_t* d_cptr = d_trows + mt;
     double* ws = (double*)(base + o_ws);
     double* wit = (double*)(base + o_wit);
     PivRec* recs = (PivRec*)(base + o_rec);
@@ -812,12 +886,28 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
     p.timeout_ns = 20ull * 1000000000ull;
     p.abort_flag = abort;
 
+    if (streamed) {  // the row chunks, in order, on the copy stream
+        CUDA_TRY(cudaEventRecord(B->ev_in, st_caller));
+        CUDA_TRY(cudaStreamWaitEvent(B->cpy, B->ev_in, 0));
+        for (int c = 0; c < n_chunks; ++c) {
+            CUDA_TRY(cudaMemcpy2DAsync((double*)B->din + cr[c] * n, (size_t)n * sizeof(double), h_src + cr[c] * lda_h,
+                                       (size_t)lda_h * sizeof(double), (size_t)n * sizeof(double), (size_t)(cr[c + 1] - cr[c]),
+                                       cudaMemcpyHostToDevice, B->cpy));
+            CUDA_TRY(cudaEventRecord(B->ev_arr[c], B->cpy));
+        }
+    }
     CUDA_TRY(cudaEventRecord(B->ev0, st));
-    // 1. copy + initial witness + finiteness (no pivots)
+    // 1. copy + initial witness + finiteness (no pivots); streamed: chunk 0 now, the others at their catch-up
     p.ncol0 = (int32_t)n; p.n_steps = 0; p.in_place = 0; p.wit_in = nullptr;
     p.seq = d_iota; p.row_pstep = d_never; p.pstep_offset = 0;
     p.cta_row_ptr = d_iptr; p.cta_rows = d_irows; p.ctas_per_group = (int32_t)G0; p.rec[0] = recs;
-    cudaError_t e = k1_launch(p, fast, st);
+    auto init_chunk = [&](int c, cudaStream_t ss) -> cudaError_t {
+        K1Params pc = p;
+        pc.cta_row_ptr = d_cptr + (size_t)c * (G0 + 1);
+        cudaError_t ee = cudaStreamWaitEvent(ss, B->ev_arr[c], 0);
+        return ee == cudaSuccess ? k1_launch(pc, fast, ss) : ee;
+    };
+    cudaError_t e = streamed ? init_chunk(0, st) : k1_launch(p, fast, st);
     if (e != cudaSuccess) return fail(MCND_ECUDA, "K2 init launch: %s", cudaGetErrorString(e));
     // 2. panels: column-distributed panel factorisation, gather, DMMA trailing update
     KPParams kp{};
@@ -921,6 +1011,9 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
     };
     int64_t k = 0;
     int par = 0;  // ring slot
+    struct PairSlot { int64_t kb, m; int par; };
+    std::vector<PairSlot> done_pairs;  // streamed input: the pairs a late chunk catches up on
+    int cov_prev = 0;
     int64_t n_launch = 1;  // kernels launched by this call (K1 init so far)
     // debug timeline (MCND_DEBUG_TIMELINE=1): an event after every critical-stream step,
     // per-label device time printed to stderr at the end of the call
@@ -940,6 +1033,35 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
         double* const Lq = Lb + (size_t)par * std::max<int64_t>(n, 1) * 2 * b;
         double* const Wp = Wp2 + (size_t)par * b * b;
         K2Gather* const gpair = gpair2 + par;
+        int cov_q = n_chunks - 1;
+        if (streamed && pairs && k + 1 < n_panels) {
+            const size_t q = (size_t)(k / 2);
+            cov_q = q < cov_of.size() ? cov_of[q] : n_chunks - 1;
+        }
+        // chunks first covered at this pair: K1 init, then pairs 0..q-1 in order, on the side
+        // stream (after pair q-1's side work, so every slot they read is final; after this
+        // pair's part A, which only touches rows covered two pairs ago)
+        auto catch_up = [&]() -> cudaError_t {
+            cudaError_t ee = cudaSuccess;
+            for (int c = cov_prev + 1; c <= cov_q && ee == cudaSuccess; ++c) {
+                ee = init_chunk(c, side);
+                ++n_launch;
+                for (const PairSlot& ps : done_pairs) {
+                    if (ee != cudaSuccess) break;
+                    const int64_t r0 = cr[c] - (ps.kb + 2 * b);  // rows relative to that pair's trailing block
+                    double* const Lp = Lb + (size_t)ps.par * std::max<int64_t>(n, 1) * 2 * b + r0 * 2 * b;
+                    ee = k2_gather_lcorr(ws, ld, (int32_t)cr[c], (int32_t)(cr[c + 1] - cr[c]), gpair2 + ps.par, Lp,
+                                         Wp2 + (size_t)ps.par * b * b, abort, side);
+                    if (ee == cudaSuccess)
+                        ee = k2_gemm(ws, ld, (int32_t)cr[c], (int32_t)(cr[c + 1] - cr[c]), (int32_t)(ps.m - 2 * b), 128, Lp,
+                                     2 * b, Wb + (size_t)ps.par * 2 * b * ld, ld, wit, abort, side, -1);
+                    n_launch += 2;
+                }
+            }
+            cov_prev = std::max(cov_prev, cov_q);
+            return ee;
+        };
+        const int64_t cov_end = cr[cov_q + 1];  // rows past it are not resident yet
         if (pairs && k + 1 < n_panels) {
             e = run_kp(kb, gp0, Wq);
             mark("kp1");
@@ -1006,6 +1128,14 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
             // side stream: W, Wp and the gather descriptor are final once pair prep is done;
             // started only after the critical rows' update (MCND_K2_SIDE_AFTER=0: right away), so the side
             // kernels do not take the SMs the critical ones need
+            if (streamed && cov_q > cov_prev && ahead >= nr) {  // no side work: new rows caught up first
+                if (e == cudaSuccess) e = cudaEventRecord(B->ev_a, st);
+                if (e == cudaSuccess) e = cudaStreamWaitEvent(side, B->ev_a, 0);
+                if (e == cudaSuccess) e = catch_up();
+                if (e == cudaSuccess) e = cudaEventRecord(B->ev_b, side);
+                side_pending = (e == cudaSuccess);
+                if (e == cudaSuccess) e = join_side();
+            }
             if (e == cudaSuccess && ahead < nr && !side_after) e = cudaEventRecord(B->ev_a, st);
             if (e == cudaSuccess) e = trailing(0, ahead, st, 0);  // the critical rows first
             if (e == cudaSuccess && ahead < nr && side_after) e = cudaEventRecord(B->ev_a, st);
@@ -1021,16 +1151,21 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
                     if (e == cudaSuccess) e = trailing(ahead, ahead2, side, -1);
                     if (e == cudaSuccess) e = cudaEventRecord(B->ev_c, side);
                     sideA_pending = (e == cudaSuccess);
-                    if (e == cudaSuccess) e = trailing(ahead + ahead2, nr - ahead - ahead2, side, -1);
+                    if (e == cudaSuccess && streamed) e = catch_up();
+                    const int64_t rows_b = std::min<int64_t>(nr, cov_end - (kb + 2 * b)) - ahead - ahead2;
+                    if (e == cudaSuccess && rows_b > 0) e = trailing(ahead + ahead2, rows_b, side, -1);
                     n_launch += 2;
                 } else {
-                    if (e == cudaSuccess) e = trailing(ahead, nr - ahead, side, prio ? -1 : (int)budget);
+                    if (e == cudaSuccess && streamed) e = catch_up();
+                    if (e == cudaSuccess) e = trailing(ahead, std::min<int64_t>(nr, cov_end - (kb + 2 * b)) - ahead, side,
+                                                       prio ? -1 : (int)budget);
                 }
                 if (e == cudaSuccess) e = cudaEventRecord(B->ev_b, side);
                 side_pending = (e == cudaSuccess);
                 n_launch += 3;
             }
             n_launch += (fuse_pp ? 7 : 8) - (fuse_lc ? 1 : 0) - (fuse_r1 ? 2 : 0);  // 2 panels, [gather, update], [prep], gather, [L corr], trailing
+            if (streamed) done_pairs.push_back({kb, m, par});
             k += 2;
             par = (par + 1) % kRing;
         } else {
@@ -1522,10 +1657,8 @@ int mcnd_logdet_blocked(const double* h_a, int64_t n, int64_t lda, uint32_t flag
     int code = MCND_OK;
     Buffers* B = buffers_for_current(&code);
     if (!B) return code;
-    const double* d_a = nullptr;
-    rc = stage_input(*B, h_a, n, n, lda, (cudaStream_t)stream, &d_a);
-    if (rc) return rc;
-    return blocked_dev(d_a, n, n, flags, (cudaStream_t)stream, out, pivots_out, cols_out);
+    // staged inside: streamed by row chunks when h_a is pinned (overlaps the first pairs)
+    return blocked_dev(nullptr, n, lda, flags, (cudaStream_t)stream, out, pivots_out, cols_out, h_a);
 }
 
 int32_t mcnd_blocked_panel(void) { return kK2B; }

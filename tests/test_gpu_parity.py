@@ -453,3 +453,42 @@ def test_blocked_singular_mid_panel_and_tail(mc, dup_row):
     got = mc.logdet_blocked(b)
     ref = mc.logdet_condensation(b)
     assert got.sign == ref.sign and abs(got.log_abs - ref.log_abs) <= tol(n, ref.log_abs)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [1500, 4000, 8000])
+def test_blocked_streamed_host_input_identical(mc, n):
+    """A pinned host matrix is streamed in row chunks while the first pairs run (late
+    chunks caught up on the side stream, csrc/mcnd_api.cu blocked_dev): bitwise the
+    result and pivots of the resident-matrix call; a pageable host matrix (one copy,
+    then the same schedule) too."""
+    import torch
+    from paper_1811_08057_b200 import matrix as M
+
+    host = M.config_uniform(n, 3)
+    ref = mc.logdet_blocked(torch.from_numpy(host).cuda(), return_pivots=True)
+    pinned = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
+    pinned.copy_(torch.from_numpy(host))
+    for src in (pinned.numpy(), pinned.numpy(), host):
+        got = mc.logdet_blocked(src, return_pivots=True)
+        assert got[0] == ref[0]
+        assert np.array_equal(got[1], ref[1]) and np.array_equal(got[2], ref[2])
+
+
+@pytest.mark.gpu
+def test_blocked_streamed_host_input_errors(mc):
+    """Non-finite entries in the last streamed chunk still raise ValueError; a singular
+    matrix (zero row in a late chunk) still returns SINGULAR."""
+    import torch
+
+    n = 4000
+    rng = np.random.default_rng(11)
+    pinned = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
+    pinned.copy_(torch.from_numpy(rng.uniform(-1, 1, (n, n))))
+    h = pinned.numpy()
+    h[n - 5, 17] = np.nan
+    with pytest.raises(ValueError):
+        mc.logdet_blocked(h)
+    h[n - 5, 17] = 0.5
+    h[n - 700, :] = 0.0
+    assert mc.logdet_blocked(h) == mc.SINGULAR
