@@ -97,6 +97,8 @@ int mcnd_mc_parallel(const double* h_a, int64_t n, int64_t lda, int32_t p, uint3
  * No reference counterpart (PAPER.md:89 leaves it to future work). */
 int mcnd_logdet_blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, void* stream,
                             mcnd_logdet* out, double* pivots_out, int32_t* cols_out);
+/* Host input: a pinned (page-locked) h_a is copied in row chunks that overlap the first
+ * panel pairs (bitwise the result of the _dev call); a pageable h_a is copied whole first. */
 int mcnd_logdet_blocked(const double* h_a, int64_t n, int64_t lda, uint32_t flags, void* stream,
                         mcnd_logdet* out, double* pivots_out, int32_t* cols_out);
 int32_t mcnd_blocked_panel(void);
