@@ -69,7 +69,7 @@ struct Buffers {
     cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_c = nullptr;  // K2: stream joins
     cudaEvent_t ev_in = nullptr, ev_out = nullptr;
     cudaStream_t cpy = nullptr;                  // K2 host input: row chunks copied while the first pairs run
-    static constexpr int kMaxChunks = 16;
+    static constexpr int kMaxChunks = 32;
     cudaEvent_t ev_arr[kMaxChunks] = {};
     int sms = 0;
     uint32_t epoch = 0;
@@ -747,7 +747,10 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
         cudaPointerAttributes pa{};
         const bool pinned = cudaPointerGetAttributes(&pa, h_src) == cudaSuccess && pa.type == cudaMemoryTypeHost;
         cudaGetLastError();
-        const int64_t rows_c = (int64_t)align_up((size_t)std::max<int64_t>(512, (n + Buffers::kMaxChunks - 1) / Buffers::kMaxChunks), 128);
+        // chunk 0 (>= 512 rows) holds the rows pairs 0 and 1 update on the critical stream and in
+        // their part A; later parts A touch rows covered two pairs earlier
+        const int64_t min_rows = std::max<int64_t>(512, env_long("MCND_K2_STREAM_ROWS", 1024));
+        const int64_t rows_c = (int64_t)align_up((size_t)std::max<int64_t>(min_rows, (n + Buffers::kMaxChunks - 1) / Buffers::kMaxChunks), 128);
         if (pinned && rows_c < n) {
             n_chunks = (int)((n + rows_c - 1) / rows_c);
             cr.assign(1, 0);
@@ -1148,6 +1151,8 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
                                            ? ((k4 + 1 < n_panels) ? 2 * b : (k4 < n_panels ? b : nr - ahead))
                                            : 0;
                 if (ahead2 > 0 && ahead2 < nr - ahead) {
+                    // (defensive: part A's rows not resident yet -> catch up first)
+                    if (e == cudaSuccess && streamed && kb + 2 * b + ahead + ahead2 > cr[cov_prev + 1]) e = catch_up();
                     if (e == cudaSuccess) e = trailing(ahead, ahead2, side, -1);
                     if (e == cudaSuccess) e = cudaEventRecord(B->ev_c, side);
                     sideA_pending = (e == cudaSuccess);
