@@ -980,11 +980,11 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
     // half is corrected for panel k by a 64-wide DMMA update: L1 -= L0 * W_k[:, P_{k+1}].
     //
     // Look-ahead: the trailing update is split.  The rows the NEXT pair factors are
-    // updated first on the caller's stream; the remaining rows go to a side stream as
-    // "fat" GEMM CTAs on (SMs - panel CTAs) SMs, running while the next two panels
-    // are factored on the SMs left free.  The next pair's own trailing gather waits
-    // for that side update (one event each way).  L and W are double-buffered by
-    // pair parity so the side GEMM can read pair q's while pair q+1 writes its own.
+    // updated first on the critical (highest-priority) stream; the rest goes to the
+    // lowest-priority side stream (part A: the rows of the pair after next, part B: the
+    // remainder), running while the next panels are factored.  The next pair's critical
+    // update waits for part A only.  L, W, Wp and the pair descriptor live in a ring of
+    // pair slots so the side GEMM can read pair q's while pairs q+1, q+2 write theirs.
     const bool pairs = env_long("MCND_K2_PAIRS", 1) != 0;
     const bool overlap = pairs && env_long("MCND_K2_OVERLAP", 1) != 0;
     const bool fuse_lc = env_long("MCND_K2_FUSE_LC", 1) != 0;
