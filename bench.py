@@ -53,6 +53,9 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--force-dist", action="store_true",
                     help="use the multi-GPU block-row driver even with one rank (test hook)")
+    ap.add_argument("--no-c5", action="store_true", help="skip the C5 sub-record of the default (C3) line")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="CPU check of the multi-rank launcher and schedule (gloo, no GPU work)")
     return ap.parse_args()
 
 
@@ -82,8 +85,33 @@ def workload(cfg: str):
     raise ValueError(cfg)
 
 
-FP64_PEAK_TFLOPS = 35.47  # cuBLAS DGEMM 8192^3 measured on this pool (profiles/r1_fp64_peak.json);
-#                           DMMA-only register microbenchmark: 37.0 (profiles/r1_dmma_peak.txt)
+def fp64_peak(local: int) -> dict:
+    """The FP64 roofline denominator, measured in this run: cuBLAS DGEMM (torch.matmul,
+    float64, 8192^3; FP64 tensor cores, DMMA), best of 5 with CUDA events, SM clocks
+    sampled meanwhile.  (MEASURED_PEAKS.json has no FP64 entry; a DMMA register-only
+    microbenchmark gives 37.0 TFLOP/s, profiles/r1_dmma_peak.txt.)"""
+    import torch
+
+    n = 8192
+    g = torch.Generator(device="cuda").manual_seed(0)
+    x = torch.rand((n, n), dtype=torch.float64, device="cuda", generator=g)
+    y = torch.rand((n, n), dtype=torch.float64, device="cuda", generator=g)
+    for _ in range(2):
+        torch.matmul(x, y)
+    torch.cuda.synchronize()
+    best = float("inf")
+    with ClockSampler(local) as clk:
+        for _ in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            torch.matmul(x, y)
+            e1.record()
+            torch.cuda.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+    del x, y
+    return {"tflops": 2.0 * n ** 3 / (best * 1e-3) / 1e12, "ms": best,
+            "how": "cuBLAS DGEMM (torch.matmul float64) 8192^3, best of 5, measured in this run",
+            "clocks": clk.summary()}
 
 
 def peaks():
@@ -193,29 +221,63 @@ class ClockSampler:
                 "samples": len(sm), "source": "nvml" if self.samples else "nvidia-smi"}
 
 
-def cpu_baseline(a: np.ndarray, budget_s: float):
-    """Oracle (C port, OpenMP) on a bounded prefix of the condensation, extrapolated by sum m^2."""
-    from oracle import mcnd_oracle as O
+def prefix_work_fraction(n: int, steps: int) -> float:
+    """Share of the condensation work (sum over steps of (m-1)^2, m = active width) done
+    by the first `steps` steps: the extrapolation factor of a bounded CPU sample."""
+    m = np.arange(n, 1, -1, dtype=np.float64)
+    return float(np.sum((m[:steps] - 1) ** 2) / np.sum((m - 1) ** 2))
 
-    n = a.shape[0]
-    threads = os.cpu_count() or 1
-    O.condense_prefix(a[:64, :64], 8, threads)  # load + spin up the thread pool
-    steps = min(n - 1, 16)
-    for _ in range(3):  # grow the prefix until it takes about budget_s
+
+class CpuSample:
+    """The reference's CPU path (oracle: plain-C port of condense.py:134-160 /
+    runtime.py:123-229, OpenMP over rows, all host threads) on a bounded prefix of the
+    workload: the first S condensation steps (S calibrated once so that one sample takes
+    about `budget_s`), serial top-to-bottom order at one GPU and the p-worker block-row
+    schedule (mc_parallel(a, p)) at p GPUs."""
+
+    def __init__(self, a: np.ndarray, budget_s: float, p: int = 1):
+        from oracle import mcnd_oracle as O
+
+        self.O, self.a, self.p = O, a, p
+        self.n = a.shape[0]
+        self.threads = os.cpu_count() or 1
+        self.total = self.n - p  # broadcast steps of the full run
+        self._run(min(self.total, 8))  # load the library, spin up the thread pool
+        steps = min(self.total, 16)
+        for _ in range(4):  # grow the prefix until one sample takes about budget_s
+            t = self._run(steps)
+            if t >= 0.6 * budget_s or steps == self.total:
+                break
+            steps = int(min(self.total, max(steps + 1, steps * 0.9 * budget_s / max(t, 1e-3))))
+        self.steps = steps
+        self.frac = prefix_work_fraction(self.n, steps)
+
+    def _run(self, steps: int) -> float:
         t0 = time.perf_counter()
-        O.condense_prefix(a, steps, threads)
-        t = time.perf_counter() - t0
-        if t >= 0.5 * budget_s or steps == n - 1:
-            break
-        steps = int(min(n - 1, max(steps + 1, steps * 0.9 * budget_s / max(t, 1e-3))))
-    m = np.arange(n, 1, -1, dtype=np.float64)  # active size at each step
-    w_all = float(np.sum((m - 1) ** 2))
-    w_pre = float(np.sum((m[:steps] - 1) ** 2))
-    t_full = t * w_all / w_pre
-    return {"value": flops(n) / t_full / 1e9, "unit": "GFLOP/s", "cores": threads, "kind": "port",
-            "sample": f"first {steps} of {n - 1} condensation steps of the same matrix "
-                      f"({t:.1f} s, {100 * w_pre / w_all:.1f}% of the work), extrapolated by sum m^2",
-            "time_to_logdet_s_extrapolated": t_full}
+        if self.p == 1:
+            self.O.condense_prefix(self.a, steps, self.threads)
+        else:
+            self.O.mc_parallel(self.a, self.p, self.threads, max_steps=steps)
+        return time.perf_counter() - t0
+
+    def time_one(self) -> float:
+        return self._run(self.steps)
+
+    def describe(self, t: float) -> dict:
+        """cpu_baseline object for one measured sample time t (seconds)."""
+        call = "logdet_condensation" if self.p == 1 else f"mc_parallel(a, {self.p})"
+        return {"value": flops(self.n) * self.frac / t / 1e9, "unit": "GFLOP/s", "cores": self.threads,
+                "kind": "port",
+                "sample": (f"reference {call} (oracle C port, {self.threads} threads): first {self.steps} of "
+                           f"{self.total} condensation steps of the same matrix, {100 * self.frac:.1f}% of the "
+                           f"work, {t:.2f} s measured; value = that work / that time"),
+                "sample_seconds": t,
+                "time_to_logdet_s_extrapolated": t / self.frac}
+
+
+def cpu_baseline(a: np.ndarray, budget_s: float, p: int = 1):
+    s = CpuSample(a, budget_s, p)
+    return s.describe(s.time_one())
 
 
 def dist_env():
@@ -225,43 +287,73 @@ def dist_env():
     return rank, world, local
 
 
+def default_method(args, n: int) -> str:
+    return args.method or ("unblocked" if n < 2048 else "blocked")
+
+
+def bench_config(args, name: str, n: int, world: int, batch: int | None = None) -> dict:
+    """The workload `config` both arms print (the driver compares them)."""
+    if batch is not None:
+        return {"workload": name, "batch": batch, "n": n, "l2": "L2 flushed between iterations",
+                "parallelism": "1 GPU" if world == 1 else f"batch sharded x{world} GPUs"}
+    method = default_method(args, n)
+    if world == 1:
+        par = "1 GPU"
+    elif method == "blocked":
+        par = (f"block rows x{world} GPUs: panel pairs from the rank with the most live rows, "
+               "W broadcast (NCCL), local rank-128 updates")
+    else:
+        par = f"block-row x{world} GPUs, pivot rows pushed over NVLink"
+    return {"workload": name, "n": n, "method": method, "mode": "fast-fma" if args.fast else "reference-exact",
+            "l2": ("input larger than L2 (%.0f MB vs 126 MB); workspace re-read from the caller's matrix each step"
+                   % (8 * n * n / 1e6)) if 8 * n * n > 126e6 else "input fits L2 (%.0f MB)" % (8 * n * n / 1e6),
+            "parallelism": par}
+
+
 def run_reference(args):
+    """--impl reference: the reference's CPU path (oracle port, all host threads) on this
+    arm's workload, rank 0 only; every timed step is one bounded sample (the first S
+    condensation steps, S calibrated during the warm-up), so steps x ms_per_step is the
+    time actually measured."""
     rank, world, _ = dist_env()
     if rank != 0:
-        return
+        return 0
+    p = max(world, args.gpus)
     name, a, n = workload(args.config)
     if not isinstance(a, np.ndarray):  # C5 is generated on the GPU; the CPU port gets a host copy
         a = a.cpu().numpy()
+    threads = os.cpu_count() or 1
     if a.ndim == 3:
         from oracle import mcnd_oracle as O
 
-        threads = os.cpu_count() or 1
-        times = []
         for _ in range(args.warmup):
             O.logdet_batched(a[:256], threads)
+        times = []
         for _ in range(args.steps):
             t0 = time.perf_counter()
             O.logdet_batched(a, threads)
             times.append(time.perf_counter() - t0)
         t = statistics.mean(times)
         val = a.shape[0] * flops(n) / t / 1e9
-        cb = {"value": val, "unit": "GFLOP/s", "cores": threads, "kind": "port", "sample": "full batch"}
+        cb = {"value": val, "unit": "GFLOP/s", "cores": threads, "kind": "port",
+              "sample": f"full batch of {a.shape[0]} matrices per step (oracle C port, {threads} threads)"}
+        cfg = bench_config(args, name, n, p, batch=a.shape[0])
     else:
-        budget = max(2.0, min(args.cpu_seconds, 150.0 / max(args.steps + args.warmup, 1)))
-        for _ in range(args.warmup):
-            cpu_baseline(a, budget / 4)
-        vals = [cpu_baseline(a, budget) for _ in range(args.steps)]
-        val = statistics.mean(v["value"] for v in vals)
-        cb = dict(vals[-1])
-        cb["value"] = val
-        t = flops(n) / (val * 1e9)
+        total_budget = 150.0  # seconds of CPU work for the whole --steps/--warmup run
+        budget = max(1.0, min(args.cpu_seconds, total_budget / max(args.steps + 1, 1)))
+        smp = CpuSample(a, budget, p)  # its calibration samples are the warm-up
+        times = [smp.time_one() for _ in range(args.steps)]
+        t = statistics.mean(times)
+        cb = smp.describe(t)
+        val = cb["value"]
+        cfg = bench_config(args, name, n, p)
     line = {"impl": "reference", "metric": metric_name(args.config), "value": val, "unit": "GFLOP/s",
-            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+            "n_gpus": p, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (numpy PCG64)", "config": {"workload": name, "n": n},
-            "cpu_baseline": cb,
+            "data": "synthetic (numpy PCG64)", "config": cfg, "cpu_baseline": cb,
             "e2e": {"value": val, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+    return 0
 
 
 def metric_name(cfg):
@@ -294,7 +386,7 @@ def run_single(args):
     # default: the blocked rank-64 variant where the unblocked rank-1 chain is HBM-bound
     # (north_star (2)); C1 stays unblocked (L2/latency-bound, 8 MB).  The other variant
     # is measured too and reported under "alt" (unblocked = bitwise-reference arithmetic).
-    method = args.method or ("unblocked" if n < 2048 else "blocked")
+    method = default_method(args, n)
     fn = mc.logdet_blocked if method == "blocked" else mc.logdet_condensation
     if isinstance(a, np.ndarray):
         d = torch.from_numpy(a).cuda()
@@ -315,6 +407,7 @@ def run_single(args):
     torch.cuda.synchronize()
     kernel_ms = []
     launches = 0
+    torn = 0
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         ev0.record(stream)
@@ -322,6 +415,7 @@ def run_single(args):
             res, piv, cols, kms = fn(d, fast=args.fast, return_pivots=True)
             kernel_ms.append(kms)
             launches += mc._lib.LAST_LAUNCHES  # counted by the library per call
+            torn += mc._lib.LAST_TORN_READS if method == "blocked" else 0
         ev1.record(stream)
         torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1) / args.steps
@@ -336,16 +430,17 @@ def run_single(args):
     e1.record(stream)
     torch.cuda.synchronize()
     ms_e2e = e0.elapsed_time(e1) / args.steps
-    assert res_e2e == res
+    assert res_e2e == res, (res_e2e, res)
 
     kms = statistics.mean(kernel_ms)
     hbm, peak_kind = peaks()
+    fp64 = fp64_peak(local)
     if method == "blocked":
         achieved = flops(n) / (kms * 1e-3) / 1e12  # the pivot chain, not DMMA, bounds small N
-        roof = {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
-                "peak_kind": "measured here (cuBLAS DGEMM, FP64 DMMA)", "unit": "TFLOP/s",
-                "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic_from_profiles(args.config + "_blocked"),
-                "algorithmic_flops_per_launch": flops(n)}
+        roof = {"bound": "tensor", "achieved": achieved, "peak": fp64["tflops"],
+                "peak_kind": fp64["how"], "unit": "TFLOP/s",
+                "frac": achieved / fp64["tflops"], "traffic": traffic_from_profiles(args.config + "_blocked"),
+                "algorithmic_flops_per_launch": flops(n), "peak_clocks": fp64["clocks"]}
         chain = panel_chain(mc, d, args.fast)
         if chain:
             roof["panel_chain"] = chain
@@ -372,17 +467,16 @@ def run_single(args):
         "vs_baseline_note": "paper Table 3 (PAPER.md:193): N=8000, 1 CPU processor, 170.80 s" if args.config == "c3" else None,
         "dtype": "f64",
         "data": "synthetic (seeded, BASELINE recipe)",
-        "config": {"workload": name, "n": n, "method": method,
-                   "mode": "fast-fma" if args.fast else "reference-exact",
-                   "l2": "input larger than L2 (%.0f MB vs 126 MB); workspace re-read from the caller's matrix each step" % (8 * n * n / 1e6),
-                   "parallelism": "1 GPU"},
-        "result": {"sign": res.sign, "log_abs": res.log_abs, "parity": parity},
+        "config": bench_config(args, name, n, 1),
+        "result": {"sign": res.sign, "log_abs": res.log_abs, "parity": parity,
+                   "panel_torn_reads": torn if method == "blocked" else None},
         "roofline": roof,
         "e2e": {"value": flops(n) / (ms_e2e * 1e-3) / 1e9, "unit": "GFLOP/s", "ms_per_step": ms_e2e,
                 "h2d_bytes_per_step": 8 * n * n, "d2h_bytes_per_step": 12 * n + 16},
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }
+    bad = [parity] if parity.startswith("MISMATCH") else []
     if args.method is None and args.config in ("c2", "c3"):
         other = mc.logdet_condensation if method == "blocked" else mc.logdet_blocked
         other(d, fast=args.fast)
@@ -392,17 +486,85 @@ def run_single(args):
             oms.append(k2)
         okms = statistics.mean(oms)
         omethod = "unblocked" if method == "blocked" else "blocked"
+        opar = check_parity(args.config, r2, args.fast or omethod == "blocked")
+        bad += [opar] if opar.startswith("MISMATCH") else []
         alt = {"method": omethod, "kernel_ms": okms, "value": flops(n) / (okms * 1e-3) / 1e9, "unit": "GFLOP/s",
-               "result": {"sign": r2.sign, "log_abs": r2.log_abs,
-                          "parity": check_parity(args.config, r2, args.fast or omethod == "blocked")}}
+               "result": {"sign": r2.sign, "log_abs": r2.log_abs, "parity": opar}}
         if omethod == "unblocked":
             B = algorithmic_bytes(n)
             alt["roofline"] = {"bound": "hbm", "achieved": B / (okms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
                                "frac": B / (okms * 1e-3) / 1e9 / hbm, "traffic": traffic_from_profiles(args.config)}
         line["alt"] = alt
+    if args.config == "c3" and not args.no_c5:
+        del d
+        torch.cuda.empty_cache()
+        c5 = c5_record(args, mc, fp64, local)
+        line["c5"] = c5
+        if c5["parity"].startswith("MISMATCH"):
+            bad.append("C5 " + c5["parity"])
     if not args.no_cpu_baseline and a is not None:
         line["cpu_baseline"] = cpu_baseline(a, args.cpu_seconds)
     print(json.dumps(line), flush=True)
+    if bad:
+        print("bench.py: PARITY FAILURE: " + "; ".join(bad), file=sys.stderr, flush=True)
+        return 3
+    return 0
+
+
+def c5_record(args, mc, fp64, local: int) -> dict:
+    """C5 (N=32768 SPD, 8.6 GB, blocked b=64 on the FP64 tensor cores) as a sub-record of
+    the default line: device time per logdet against the in-run DGEMM peak, cuSOLVER LU
+    (torch.linalg.slogdet, getrf) on the same matrix as the library reference point and
+    the value oracle (the reference CPU path is infeasible at this size)."""
+    import torch
+
+    from paper_1811_08057_b200 import matrix as M
+
+    n = 32768
+    a = M.config_spd_device(n, 5)
+    stream = torch.cuda.current_stream()
+    mc.logdet_blocked(a)
+    torch.cuda.synchronize()
+    times, kms, launches = [], [], 0
+    with ClockSampler(local) as clk:
+        for _ in range(3):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            res, _, _, k = mc.logdet_blocked(a, return_pivots=True)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1))
+            kms.append(k)
+            launches += mc._lib.LAST_LAUNCHES
+    torn = mc._lib.LAST_TORN_READS
+    cus = []
+    for _ in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        s_ref, l_ref = torch.linalg.slogdet(a)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        cus.append(e0.elapsed_time(e1))
+    s_ref, l_ref = int(s_ref.item()), float(l_ref.item())
+    tol = max(1e-8 * n, 1e-10 * abs(l_ref))
+    d = abs(res.log_abs - l_ref)
+    parity = (f"within tolerance of cuSOLVER LU slogdet (|d|={d:.3e} <= {tol:.2e})"
+              if res.sign == s_ref and d <= tol else
+              f"MISMATCH vs cuSOLVER LU slogdet ({res.sign},{res.log_abs}) != ({s_ref},{l_ref})")
+    ms = statistics.mean(times)
+    ach = flops(n) / (ms * 1e-3) / 1e12
+    del a
+    torch.cuda.empty_cache()
+    return {"workload": "C5 SPD X X^T/N + 1e-2 I, N=32768 (X from a seeded CUDA generator, seed 5)",
+            "method": "blocked", "ms_per_step": ms, "kernel_ms": statistics.mean(kms), "steps": len(times),
+            "value": flops(n) / (ms * 1e-3) / 1e9, "unit": "GFLOP/s",
+            "roofline": {"bound": "tensor", "achieved": ach, "peak": fp64["tflops"], "peak_kind": fp64["how"],
+                         "unit": "TFLOP/s", "frac": ach / fp64["tflops"],
+                         "traffic": traffic_from_profiles("c5_blocked")},
+            "result": {"sign": res.sign, "log_abs": res.log_abs, "panel_torn_reads": torn},
+            "parity": parity,
+            "cusolver_getrf_ms": statistics.mean(cus), "speedup_vs_cusolver": statistics.mean(cus) / ms,
+            "gpu_launches": launches, "clocks": clk.summary()}
 
 
 def panel_chain(mc, d, fast):
@@ -480,7 +642,7 @@ def run_batched(args, name, a, n):
     line = {"metric": metric_name("c4"), "value": fl / (ms * 1e-3) / 1e9, "unit": "GFLOP/s", "n_gpus": 1,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (numpy PCG64 seed 4)",
-            "config": {"workload": name, "batch": a.shape[0], "n": n, "l2": "L2 flushed between iterations"},
+            "config": bench_config(args, name, n, 1, batch=a.shape[0]),
             "roofline": {"bound": "hbm", "achieved": B / (ms * 1e-3) / 1e9, "peak": hbm, "peak_kind": peak_kind,
                          "unit": "GB/s", "frac": B / (ms * 1e-3) / 1e9 / hbm, "traffic": traffic_from_profiles("c4")},
             "e2e": {"value": fl / (ms_e2e * 1e-3) / 1e9, "unit": "GFLOP/s", "ms_per_step": ms_e2e,
@@ -497,13 +659,69 @@ def run_batched(args, name, a, n):
         line["cpu_baseline"] = {"value": sub.shape[0] * flops(n) / t / 1e9, "unit": "GFLOP/s", "cores": threads,
                                 "kind": "port", "sample": "first 1024 of 4096 matrices"}
     print(json.dumps(line), flush=True)
+    return 0
+
+
+def spawn(args) -> int:
+    """`bench.py --gpus N` outside torchrun: launch N ranks (one process per GPU) through
+    torch.distributed.run on 127.0.0.1 and return their exit status; rank 0 prints the line."""
+    import socket
+
+    if not args.dry_run:
+        import torch
+
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            print(f"bench.py: --gpus {args.gpus} but only {have} CUDA device(s) visible", file=sys.stderr)
+            return 2
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def dry_run(args) -> int:
+    """CPU check of the multi-rank plumbing (gloo): every rank derives its block rows and
+    the blocked pair schedule, the ranks agree on them, rank 0 prints the line it would
+    print (no GPU work, value null)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1811_08057_b200 import dist as D
+    from paper_1811_08057_b200.runtime import plan_blocks
+
+    rank, world, _ = dist_env()
+    dist.init_process_group("gloo")
+    n = {"c1": 1000, "c2": 4000, "c3": 8000, "c5": 32768}.get(args.config, 8000)
+    start, rows = plan_blocks(n, world).assignments[rank]
+    sched = D.blocked_schedule(n, world)
+    mine = torch.tensor([rows, len(sched[0])], dtype=torch.int64)
+    allv = [torch.zeros_like(mine) for _ in range(world)]
+    dist.all_gather(allv, mine)
+    ok = sum(int(v[0]) for v in allv) == n and len({int(v[1]) for v in allv}) == 1
+    if rank == 0:
+        print(json.dumps({"metric": metric_name(args.config), "value": None, "unit": "GFLOP/s", "n_gpus": world,
+                          "steps": 0, "warmup": 0, "dry_run": True, "schedule_consistent": ok,
+                          "config": {"workload": args.config, "n": n, "ranks_rows": [int(v[0]) for v in allv]}}),
+              flush=True)
+    dist.destroy_process_group()
+    return 0 if ok else 1
 
 
 def main():
     args = parse()
-    if args.impl == "reference":
-        return run_reference(args)
     rank, world, local = dist_env()
+    if args.impl == "reference":  # CPU only: rank 0 runs it (torchrun or not), p = the GPU count
+        return run_reference(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn(args)
+    if args.gpus > 1 and world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        return 2
+    if args.dry_run:
+        return dry_run(args)
     if world > 1 or args.force_dist:
         from paper_1811_08057_b200 import dist
 
@@ -512,4 +730,4 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main())

@@ -53,6 +53,8 @@ typedef struct mcnd_logdet {
     double device_ms;        /* device time of the condensation (CUDA events)   */
     int64_t steps;           /* condensation steps executed                      */
     int64_t launches;        /* GPU kernels this call launched (0 if not counted) */
+    int64_t torn_reads;      /* blocked: panel records observed half-written (one 8-byte word
+                                of the new store, one stale) and re-polled; informational */
 } mcnd_logdet;
 
 /* Communication accounting of the block-row driver (runtime.py:47-66). */

@@ -33,14 +33,15 @@ def _load():
     global _lib
     if _lib is not None:
         return _lib
-    if not os.path.exists(LIB_PATH):
+    src = os.path.join(HERE, "mcnd_oracle.c")
+    if not os.path.exists(LIB_PATH) or os.path.getmtime(src) > os.path.getmtime(LIB_PATH):
         build()
     lib = ctypes.CDLL(LIB_PATH)
     P = ctypes.c_void_p
     i64, i32 = ctypes.c_int64, ctypes.c_int
     lib.oracle_logdet_condensation.argtypes = [P, i64, P, i32, P, P, P, P, P, P]
     lib.oracle_logdet_lu.argtypes = [P, i64, P, P, P]
-    lib.oracle_mc_parallel.argtypes = [P, i64, i64, i32, P, P, P, P, P, P, P, P, P, P]
+    lib.oracle_mc_parallel.argtypes = [P, i64, i64, i32, P, P, P, P, P, P, P, P, P, P, i64]
     lib.oracle_logdet_batched.argtypes = [P, i64, i64, i32, P, P]
     lib.oracle_condense_steps.argtypes = [P, i64, P, i32, P, P, P, P, P, P, i64]
     lib.oracle_condense_steps.restype = ctypes.c_int
@@ -127,7 +128,9 @@ class OracleParallel(NamedTuple):
     rem_wit: np.ndarray      # its witnesses
 
 
-def mc_parallel(a, p: int, threads: int = 0) -> OracleParallel:
+def mc_parallel(a, p: int, threads: int = 0, max_steps: int | None = None) -> OracleParallel:
+    """runtime.py:123-229; max_steps bounds the number of broadcast steps (a prefix of the
+    workload for the CPU-baseline timing; the result is then the partial accumulators)."""
     lib = _load()
     a = np.ascontiguousarray(a, dtype=np.float64)
     n = a.shape[0]
@@ -145,7 +148,7 @@ def mc_parallel(a, p: int, threads: int = 0) -> OracleParallel:
     rem_wit = np.zeros(p, dtype=np.float64)
     lib.oracle_mc_parallel(_ptr(a), n, p, threads, ctypes.byref(sign), ctypes.byref(la), _ptr(stats),
                            _ptr(payload), _ptr(rows), _ptr(owners), _ptr(piv), _ptr(cols), _ptr(rem),
-                           _ptr(rem_wit))
+                           _ptr(rem_wit), ctypes.c_int64(n if max_steps is None else int(max_steps)))
     aborted = int(stats[3])
     n_bcast_payload = (aborted if aborted >= 0 else n - p)
     return OracleParallel(int(sign.value), float(la.value), int(stats[0]), int(stats[1]),

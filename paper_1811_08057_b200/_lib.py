@@ -28,7 +28,7 @@ class McndLogDet(ctypes.Structure):
     _fields_ = [("sign", ctypes.c_int32), ("singular", ctypes.c_int32), ("log_abs", ctypes.c_double),
                 ("singular_step", ctypes.c_int64), ("invalid_step", ctypes.c_int64),
                 ("invalid_row", ctypes.c_int64), ("device_ms", ctypes.c_double), ("steps", ctypes.c_int64),
-                ("launches", ctypes.c_int64)]
+                ("launches", ctypes.c_int64), ("torn_reads", ctypes.c_int64)]
 
 
 class McndCommStats(ctypes.Structure):
@@ -39,6 +39,7 @@ class McndCommStats(ctypes.Structure):
 
 _lock = threading.Lock()
 LAST_LAUNCHES = 0  # GPU kernels launched by the most recent single-matrix call (bench accounting)
+LAST_TORN_READS = 0  # panel records the most recent blocked call saw half-written (re-polled)
 _lib = None
 
 EXPORTS = (

@@ -146,6 +146,7 @@ def logdet_blocked(a, *, fast: bool = False, return_pivots: bool = False):
                                      cols.ctypes.data)
     _lib.check(rc)
     _lib.LAST_LAUNCHES = int(out.launches)
+    _lib.LAST_TORN_READS = int(out.torn_reads)
     res = SINGULAR if out.singular else LogDet(int(out.sign), float(out.log_abs))
     if return_pivots:
         k = int(out.steps) + (0 if out.singular else 1)

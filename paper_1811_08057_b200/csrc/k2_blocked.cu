@@ -30,6 +30,14 @@
 namespace mcnd {
 namespace {
 
+constexpr int kMaxDevices = 64;
+int device_sms(int dev) {  // SM count per device (cached; calls are serialised by the host runtime)
+    static int cache[kMaxDevices] = {};
+    if (dev < 0 || dev >= kMaxDevices) return 148;
+    if (!cache[dev]) cudaDeviceGetAttribute(&cache[dev], cudaDevAttrMultiProcessorCount, dev);
+    return cache[dev] > 0 ? cache[dev] : 148;
+}
+
 
 // One warp per trailing row: L[r, 0:K] = A[r, P], then the moved columns.
 template <int K>
@@ -151,11 +159,8 @@ __global__ void __launch_bounds__(kPrepThreads) k2_pair_prep_kernel(const K2Gath
 // ---- DMMA GEMM: C[M x N2] (rows rbase.., in ws) += NL[M x K] * W[K x N2], K = 64 or 128, where
 // NL = -L is stored negated by the gather so the DMMA operands carry no negation (keeps the
 // A-operand register reuse cache usable) ----
-constexpr int BM = 64, BN = 128, BKS = 64;   // tile rows / cols, K per pipeline stage
-constexpr int LDLS = BKS + 4;                // padded smem strides (conflict-free fragment loads)
+constexpr int BM = 64, BN = 128;             // tile rows / cols
 constexpr int LDWS = BN + 4;                 // = 4 (mod 16): the B fragment (lanes 4q+g) hits 16 distinct bank pairs per half-warp
-constexpr int kStage = BM * LDLS + BKS * LDWS;  // doubles per stage buffer
-// warps: 2 (M) x WN (N); WN = 8 -> 512 threads, warp tile 32 x 16; WN = 4 -> 256 threads, 32 x 32
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -174,145 +179,6 @@ __device__ __forceinline__ void cp_async16_zf(void* smem, const void* gmem, bool
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "r"(valid ? 16 : 0) : "memory");
 }
 
-// Persistent: one CTA per SM walks a contiguous range of 64 x 128 output tiles
-// (row-block major, so L is reused from L2 and W streams from L2).  K is
-// consumed in stages of 64: the operands of stage j+1 (next K half or next
-// tile) are copied into the other shared-memory buffer with cp.async while the
-// DMMAs of stage j run, and the C fragments of tile t+1 are loaded into
-// registers during tile t; stores are streaming and fire-and-forget.  Row
-// maxima (the running witness) stay in registers and are flushed with one
-// atomicMax per row-block change (skipped when wit == nullptr).
-template <int K, int WN>
-__global__ void __launch_bounds__(64 * WN, 1) k2_gemm_kernel(double* __restrict__ ws, int64_t ld, int32_t rbase,
-                                                               int32_t M, int32_t N2, const double* __restrict__ L,
-                                                               int64_t ldl, const double* __restrict__ W, int64_t ldw,
-                                                               unsigned long long* __restrict__ wit,
-                                                               const unsigned* __restrict__ abort) {
-    constexpr int NS = K / BKS;  // stages per tile
-    constexpr int kGThreads = 64 * WN, WTN = BN / WN, NJ = WTN / 8;
-    extern __shared__ __align__(16) double sh[];
-    if (*(volatile const unsigned*)abort) return;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int wm = warp / WN, wn = warp % WN;
-    const int g = lane >> 2, q = lane & 3;
-    const int ntn = (N2 + BN - 1) / BN, ntm = (M + BM - 1) / BM;
-    const int64_t T = (int64_t)ntn * ntm;
-    const int64_t t_begin = T * blockIdx.x / gridDim.x, t_end = T * (blockIdx.x + 1) / gridDim.x;
-    if (t_begin >= t_end) return;
-
-    // stage j of this CTA = (tile t_begin + j / NS, K half j % NS), buffer j & 1
-    auto load_stage = [&](int64_t j) {
-        const int64_t t = t_begin + j / NS;
-        const int kh = (int)(j % NS);
-        const int row0 = (int)(t / ntn) * BM, col0 = (int)(t % ntn) * BN;
-        double* ls = sh + (j & 1) * kStage;
-        double* wsm = ls + BM * LDLS;
-        for (int i = tid; i < BM * (BKS / 2); i += kGThreads) {
-            const int r = i / (BKS / 2), c2 = i % (BKS / 2);
-            double* dst = ls + r * LDLS + 2 * c2;
-            if (row0 + r < M) cp_async16(dst, L + (int64_t)(row0 + r) * ldl + kh * BKS + 2 * c2);
-            else { dst[0] = 0.0; dst[1] = 0.0; }
-        }
-        for (int i = tid; i < BKS * (BN / 2); i += kGThreads) {
-            const int k = i / (BN / 2), c2 = i % (BN / 2);
-            const int col = col0 + 2 * c2;
-            double* dst = wsm + k * LDWS + 2 * c2;
-            if (col < N2) cp_async16(dst, W + (int64_t)(kh * BKS + k) * ldw + col);
-            else { dst[0] = 0.0; dst[1] = 0.0; }
-        }
-        asm volatile("cp.async.commit_group;" ::: "memory");
-    };
-    double cn[4][NJ][2];
-    auto load_c = [&](int64_t t) {
-        const int row0 = (int)(t / ntn) * BM, col0 = (int)(t % ntn) * BN;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int r = row0 + wm * 32 + i * 8 + g;
-            const double* crow = ws + (int64_t)(rbase + r) * ld;
-#pragma unroll
-            for (int j = 0; j < NJ; ++j) {
-                const int c = col0 + wn * WTN + j * 8 + 2 * q;
-                if (r < M && c < N2) {
-                    const double2 v = __ldcs(reinterpret_cast<const double2*>(crow + c));
-                    cn[i][j][0] = v.x;
-                    cn[i][j][1] = v.y;
-                } else {
-                    cn[i][j][0] = 0.0;
-                    cn[i][j][1] = 0.0;
-                }
-            }
-        }
-    };
-
-    const int64_t nstages = (t_end - t_begin) * NS;
-    load_stage(0);
-    load_c(t_begin);
-    double rmx[4] = {0.0, 0.0, 0.0, 0.0};
-    double acc[4][NJ][2];
-    for (int64_t j = 0; j < nstages; ++j) {
-        const int64_t t = t_begin + j / NS;
-        const int kh = (int)(j % NS);
-        asm volatile("cp.async.wait_all;" ::: "memory");
-        __syncthreads();  // stage j landed; everybody is done with buffer (j+1)&1
-        if (kh == 0) {
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-#pragma unroll
-                for (int jj = 0; jj < NJ; ++jj) { acc[i][jj][0] = cn[i][jj][0]; acc[i][jj][1] = cn[i][jj][1]; }
-        }
-        if (j + 1 < nstages) load_stage(j + 1);
-        if (kh == 0 && t + 1 < t_end) load_c(t + 1);
-        const double* ls = sh + (j & 1) * kStage;
-        const double* wsm = ls + BM * LDLS;
-#pragma unroll 4
-        for (int k0 = 0; k0 < BKS; k0 += 4) {
-            double a[4], b[NJ];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) a[i] = ls[(wm * 32 + i * 8 + g) * LDLS + k0 + q];
-#pragma unroll
-            for (int jj = 0; jj < NJ; ++jj) b[jj] = wsm[(k0 + q) * LDWS + wn * WTN + jj * 8 + g];
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-#pragma unroll
-                for (int jj = 0; jj < NJ; ++jj) dmma(acc[i][jj][0], acc[i][jj][1], a[i], b[jj]);
-        }
-        if (kh != NS - 1) continue;
-        // epilogue of tile t: store, fold |.| into the per-row maxima
-        const int bm = (int)(t / ntn);
-        const int row0 = bm * BM, col0 = (int)(t % ntn) * BN;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int r = row0 + wm * 32 + i * 8 + g;
-            double* crow = ws + (int64_t)(rbase + r) * ld;
-#pragma unroll
-            for (int jj = 0; jj < NJ; ++jj) {
-                const int c = col0 + wn * WTN + jj * 8 + 2 * q;
-                if (r < M && c < N2) {
-                    if (c + 1 < N2) {
-                        __stcs(reinterpret_cast<double2*>(crow + c), make_double2(acc[i][jj][0], acc[i][jj][1]));
-                        rmx[i] = fmax(rmx[i], fmax(fabs(acc[i][jj][0]), fabs(acc[i][jj][1])));
-                    } else {
-                        crow[c] = acc[i][jj][0];
-                        rmx[i] = fmax(rmx[i], fabs(acc[i][jj][0]));
-                    }
-                }
-            }
-        }
-        const bool flush = (t + 1 == t_end) || ((int)((t + 1) / ntn) != bm);
-        if (flush && wit) {
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                double mx = rmx[i];
-                mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-                mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-                const int r = row0 + wm * 32 + i * 8 + g;
-                if (q == 0 && r < M) atomicMax(wit + rbase + r, (unsigned long long)__double_as_longlong(mx));
-                rmx[i] = 0.0;
-            }
-        }
-    }
-}
-
 // ---- multistage variant: 2 CTAs per SM, K consumed in stages of 16 through a
 // 4-deep cp.async ring (CUTLASS-style multistage mainloop).  The C tile is loaded
 // into the accumulators at the start of each tile: its latency is hidden by the
@@ -322,10 +188,6 @@ __global__ void __launch_bounds__(64 * WN, 1) k2_gemm_kernel(double* __restrict_
 constexpr int MS_BK = 16, MS_ST = 4;          // K per stage, ring depth
 constexpr int MS_LDL = MS_BK + 4;             // 20 doubles: conflict-free A fragments
 constexpr int MS_STAGE = BM * MS_LDL + MS_BK * LDWS;
-constexpr int MS_THREADS = 256;               // 8 warps: 2 (M) x 4 (N), warp tile 32 x 32
-#ifndef MS_PREFETCH_C
-#define MS_PREFETCH_C 1
-#endif
 
 // SUB = 2: a "fat" CTA of two independent 256-thread sub-CTAs (own smem ring, own named
 // barrier) that fills a whole SM, so a grid of B fat CTAs occupies exactly B SMs and
@@ -386,7 +248,6 @@ __global__ void __launch_bounds__(64 * (BNT / 32) * SUB, 2 / SUB) k2_gemm_ms_ker
     // C tiles are pulled into L2 ahead of use (the first at entry, each next one
     // mid-way through the current tile): the accumulator load then hits L2
     auto prefetch_c = [&](int64_t t) {
-        if (MS_PREFETCH_C == 0) return;
         const int row0 = (int)(t / ntn) * BM, col0 = (int)(t % ntn) * BNT;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
@@ -416,14 +277,9 @@ __global__ void __launch_bounds__(64 * (BNT / 32) * SUB, 2 / SUB) k2_gemm_ms_ker
                 for (int jj = 0; jj < NJ; ++jj) {
                     const int c = col0 + wn * 32 + jj * 8 + 2 * q;
                     if (r < M && c < N2) {
-#ifdef MS_NO_CLOAD  // microbenchmark knob: cost of the C-tile load
-                        acc[i][jj][0] = 0.0;
-                        acc[i][jj][1] = 0.0;
-#else
                         const double2 v = __ldcs(reinterpret_cast<const double2*>(crow + c));
                         acc[i][jj][0] = v.x;
                         acc[i][jj][1] = v.y;
-#endif
                     } else {
                         acc[i][jj][0] = 0.0;
                         acc[i][jj][1] = 0.0;
@@ -689,12 +545,9 @@ cudaError_t k2_gather_fix(double* ws, int64_t ld, int32_t rbase, int32_t nrows, 
 cudaError_t k2_gather_lcorr(double* ws, int64_t ld, int32_t rbase, int32_t nrows, const K2Gather* gp, double* L,
                             const double* Wp, const unsigned* abort, cudaStream_t s) {
     if (nrows <= 0) return cudaSuccess;
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    }
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const int sms = device_sms(dev);
     const int per = kGLThreads / 32;
     const int grid = (int)std::min<int64_t>(((int64_t)nrows + per - 1) / per, 4 * (int64_t)sms);
     k2_gather_lcorr_kernel<<<grid, kGLThreads, 0, s>>>(ws, ld, rbase, nrows, gp, L, Wp, abort);
@@ -712,115 +565,41 @@ cudaError_t k2_gemm(double* ws, int64_t ld, int32_t rbase, int32_t M, int32_t N2
                     int sm_budget) {
     if (M <= 0 || N2 <= 0) return cudaSuccess;
     if (K != 64 && K != 128) return cudaErrorInvalidValue;
-    const size_t smem = (size_t)2 * kStage * sizeof(double);
-    static int sms = 0;
-    static long wn = 8;
-    if (!sms) {
-        const void* fns[] = {(const void*)k2_gemm_kernel<64, 8>, (const void*)k2_gemm_kernel<128, 8>,
-                             (const void*)k2_gemm_kernel<64, 4>, (const void*)k2_gemm_kernel<128, 4>};
-        for (const void* f : fns) {
-            cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            if (e != cudaSuccess) return e;
-        }
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (const char* v = std::getenv("MCND_K2_GEMM_WN")) wn = std::strtol(v, nullptr, 10) == 4 ? 4 : 8;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const int sms = device_sms(dev);
+    // shared-memory opt-in: a per-device (context) attribute, set once per device
+    static bool attr_done[kMaxDevices] = {};
+    const int sm4 = (int)(3 * MS_STAGE * sizeof(double));
+    const int smn = (int)((size_t)MS_ST * (BM * MS_LDL + MS_BK * (64 + 4)) * sizeof(double));
+    if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
+    if (!attr_done[dev]) {
+        if ((e = cudaFuncSetAttribute(k2_gemm_w4_kernel<64, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm4)) != cudaSuccess ||
+            (e = cudaFuncSetAttribute(k2_gemm_w4_kernel<128, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm4)) != cudaSuccess ||
+            (e = cudaFuncSetAttribute(k2_gemm_ms_kernel<128, 1, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smn)) != cudaSuccess)
+            return e;
+        attr_done[dev] = true;
     }
-    const int64_t tiles = (int64_t)((N2 + BN - 1) / BN) * ((M + BM - 1) / BM);
-    const int grid = (int)std::min<int64_t>(tiles, sms);
     auto* w = reinterpret_cast<unsigned long long*>(row_wit);
-    static long ms_mode = -1;
-    if (ms_mode < 0) {
-        const char* v = std::getenv("MCND_K2_GEMM_MS");
-        ms_mode = v ? std::strtol(v, nullptr, 10) : 1;
-        const size_t smem_ms = (size_t)MS_ST * MS_STAGE * sizeof(double);
-        cudaFuncSetAttribute(k2_gemm_ms_kernel<64, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_ms);
-        cudaFuncSetAttribute(k2_gemm_ms_kernel<128, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_ms);
-        cudaFuncSetAttribute(k2_gemm_ms_kernel<64, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * (int)smem_ms);
-        cudaFuncSetAttribute(k2_gemm_ms_kernel<128, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * (int)smem_ms);
-    }
-    // 4-warp kernel (32 x 64 warp tiles): MCND_K2_GEMM_W4=0 selects the 8-warp one.  The overlapped
-    // (side) update runs one tile per CTA, so SMs go back to the next panel tile by tile, unless it is
-    // more than MCND_K2_GEMM_PWAVES waves of 2 CTAs per SM: then the GEMM, not the panel chain, bounds
-    // the pair and a persistent grid (no per-CTA pipeline fill) is faster.  MCND_K2_GEMM_TPC forces
-    // a tiles-per-CTA count (0 = persistent).
-    static long w4 = -1, tpc = -1, pwaves = 40;
-    if (w4 < 0) {
-        const char* v = std::getenv("MCND_K2_GEMM_W4");
-        w4 = v ? std::strtol(v, nullptr, 10) : 1;
-        if (const char* u = std::getenv("MCND_K2_GEMM_TPC")) tpc = std::strtol(u, nullptr, 10);
-        if (const char* u = std::getenv("MCND_K2_GEMM_PWAVES")) pwaves = std::strtol(u, nullptr, 10);
-        const int sm4 = (int)(3 * MS_STAGE * sizeof(double));
-        cudaFuncSetAttribute(k2_gemm_w4_kernel<64, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm4);
-        cudaFuncSetAttribute(k2_gemm_w4_kernel<128, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm4);
-    }
-    auto launch_w4 = [&](int64_t per_cta) {
-        const size_t sm4 = (size_t)3 * MS_STAGE * sizeof(double);
-        const int g4 = (int)(per_cta > 0 ? (tiles + per_cta - 1) / per_cta : std::min<int64_t>(tiles, 2 * (int64_t)sms));
-        if (K == 64) k2_gemm_w4_kernel<64, 3><<<g4, W4_THREADS, sm4, s>>>(ws, ld, rbase, M, N2, L, ldl, W, ldw, w, abort);
-        else k2_gemm_w4_kernel<128, 3><<<g4, W4_THREADS, sm4, s>>>(ws, ld, rbase, M, N2, L, ldl, W, ldw, w, abort);
-        return cudaGetLastError();
-    };
-    if (sm_budget < 0 && w4) return launch_w4(tpc >= 0 ? tpc : (tiles > pwaves * 2 * (int64_t)sms ? 0 : 1));
-    if (sm_budget < 0) {  // one tile per CTA: SMs are released tile by tile (priority-scheduled overlap)
-        const size_t smem_ms = (size_t)MS_ST * MS_STAGE * sizeof(double);
-        const int grid_t = (int)std::min<int64_t>(tiles, 1 << 30);
-        if (K == 64) k2_gemm_ms_kernel<64, 1><<<grid_t, MS_THREADS, smem_ms, s>>>(ws, ld, rbase, M, N2, L, ldl, W, ldw, w, abort);
-        else k2_gemm_ms_kernel<128, 1><<<grid_t, MS_THREADS, smem_ms, s>>>(ws, ld, rbase, M, N2, L, ldl, W, ldw, w, abort);
-        return cudaGetLastError();
-    }
-    if (sm_budget > 0) {  // fat CTAs on at most sm_budget SMs
-        const size_t smem_ms = (size_t)MS_ST * MS_STAGE * sizeof(double);
-        const int grid_f = (int)std::min<int64_t>((tiles + 1) / 2, sm_budget);
-        if (K == 64) k2_gemm_ms_kernel<64, 2><<<grid_f, 2 * MS_THREADS, 2 * smem_ms, s>>>(ws, ld, rbase, M, N2, L, ldl, W, ldw, w, abort);
-        else k2_gemm_ms_kernel<128, 2><<<grid_f, 2 * MS_THREADS, 2 * smem_ms, s>>>(ws, ld, rbase, M, N2, L, ldl, W, ldw, w, abort);
-        return cudaGetLastError();
-    }
-    // MCND_K2_GEMM_CRIT_W4=1: the 4-warp kernel with 64-wide tiles for this update (measured: no gain,
-    // 24.6 vs 25.1 us standalone at m = 8000 and slower inside C3/C5)
-    static const long crit_w4 = [] { const char* v = std::getenv("MCND_K2_GEMM_CRIT_W4"); return v ? std::strtol(v, nullptr, 10) : 0L; }();
-    if (ms_mode && M <= 2 * BM && K == 128 && w4 && crit_w4) {  // a short critical-path update: 64-wide tiles, twice the CTAs
-        const int sm1 = (int)(3 * (BM * MS_LDL + MS_BK * (64 + 4)) * sizeof(double));
-        static bool attr1 = false;
-        if (!attr1) {
-            cudaFuncSetAttribute(k2_gemm_w4_kernel<128, 3, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm1);
-            attr1 = true;
-        }
+    if (sm_budget >= 0 && M <= 2 * BM && K == 128) {
+        // a short critical-path update (the next pair's 128 rows): 64 x 64 tiles, twice the
+        // CTAs of the 64 x 128 kernel, so more SMs share it (measured faster than the 4-warp
+        // kernel with 64-wide tiles: 24.6 vs 25.1 us at m = 8000, and inside C3/C5)
         const int64_t tiles_n = (int64_t)((N2 + 63) / 64) * ((M + BM - 1) / BM);
-        k2_gemm_w4_kernel<128, 3, 1><<<(int)tiles_n, 64, sm1, s>>>(ws, ld, rbase, M, N2, L, ldl, W, ldw, w, abort);
+        k2_gemm_ms_kernel<128, 1, 64><<<(int)tiles_n, 128, smn, s>>>(ws, ld, rbase, M, N2, L, ldl, W, ldw, w, abort);
         return cudaGetLastError();
     }
-    if (ms_mode && M <= 2 * BM && K == 128) {
-        static bool attr = false;
-        const size_t smem_n = (size_t)MS_ST * (BM * MS_LDL + MS_BK * (64 + 4)) * sizeof(double);
-        if (!attr) {
-            cudaFuncSetAttribute(k2_gemm_ms_kernel<128, 1, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_n);
-            attr = true;
-        }
-        const int64_t tiles_n = (int64_t)((N2 + 63) / 64) * ((M + BM - 1) / BM);
-        k2_gemm_ms_kernel<128, 1, 64><<<(int)tiles_n, 128, smem_n, s>>>(ws, ld, rbase, M, N2, L, ldl, W, ldw, w, abort);
-        return cudaGetLastError();
-    }
-    if (ms_mode && w4) return launch_w4(0);
-    if (ms_mode) {
-        const size_t smem_ms = (size_t)MS_ST * MS_STAGE * sizeof(double);
-        // one tile per CTA (measured faster than a persistent grid: CTAs of the next
-        // wave overlap the previous CTAs' epilogues); MCND_K2_GEMM_PERSIST=1 for the other
-        const char* pv = std::getenv("MCND_K2_GEMM_PERSIST");
-        const long persist = pv ? std::strtol(pv, nullptr, 10) : 0;
-        const int grid_ms = (int)(persist ? std::min<int64_t>(tiles, 2 * (int64_t)sms) : std::min<int64_t>(tiles, 1 << 30));
-        if (K == 64) k2_gemm_ms_kernel<64, 1><<<grid_ms, MS_THREADS, smem_ms, s>>>(ws, ld, rbase, M, N2, L, ldl, W, ldw, w, abort);
-        else k2_gemm_ms_kernel<128, 1><<<grid_ms, MS_THREADS, smem_ms, s>>>(ws, ld, rbase, M, N2, L, ldl, W, ldw, w, abort);
-        return cudaGetLastError();
-    }
-    if (wn == 8) {
-        if (K == 64) k2_gemm_kernel<64, 8><<<grid, 512, smem, s>>>(ws, ld, rbase, M, N2, L, ldl, W, ldw, w, abort);
-        else k2_gemm_kernel<128, 8><<<grid, 512, smem, s>>>(ws, ld, rbase, M, N2, L, ldl, W, ldw, w, abort);
-    } else {
-        if (K == 64) k2_gemm_kernel<64, 4><<<grid, 256, smem, s>>>(ws, ld, rbase, M, N2, L, ldl, W, ldw, w, abort);
-        else k2_gemm_kernel<128, 4><<<grid, 256, smem, s>>>(ws, ld, rbase, M, N2, L, ldl, W, ldw, w, abort);
-    }
+    // 4-warp kernel (64 x 128 tiles, 32 x 64 warp tiles).  An overlapped (side, sm_budget < 0)
+    // update runs one tile per CTA, so SMs go back to the next panel tile by tile, unless it is
+    // more than 40 waves of 2 CTAs per SM: then the GEMM, not the panel chain, bounds the pair
+    // and a persistent grid (no per-CTA pipeline fill) is faster.  Critical-stream updates
+    // (sm_budget >= 0) always run persistent.
+    const int64_t tiles = (int64_t)((N2 + BN - 1) / BN) * ((M + BM - 1) / BM);
+    const bool one_tile = sm_budget < 0 && tiles <= 40 * 2 * (int64_t)sms;
+    const int g4 = (int)(one_tile ? tiles : std::min<int64_t>(tiles, 2 * (int64_t)sms));
+    if (K == 64) k2_gemm_w4_kernel<64, 3><<<g4, W4_THREADS, sm4, s>>>(ws, ld, rbase, M, N2, L, ldl, W, ldw, w, abort);
+    else k2_gemm_w4_kernel<128, 3><<<g4, W4_THREADS, sm4, s>>>(ws, ld, rbase, M, N2, L, ldl, W, ldw, w, abort);
     return cudaGetLastError();
 }
 

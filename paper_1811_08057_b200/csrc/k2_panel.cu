@@ -52,63 +52,48 @@ __device__ __forceinline__ unsigned long long globaltimer() {
     return t;
 }
 
-// Record = {value, tag:32 | check:16 | aux:16}.  The 16-bit check (a hash of the
-// value bits) detects a torn 16-byte read (new tag, stale value): such a record is
-// treated as not yet arrived.  aux carries a candidate position (< 2^16 - 1).
-__device__ __forceinline__ unsigned h16(double v) {
+// Record = two 8-byte words {tag:16 | aux:16 | hi32(value)}, {tag:16 | aux:16 | lo32(value)}
+// written with ONE 16-byte store and polled with relaxed gpu-scope loads.  Each 8-byte
+// word is single-copy atomic on its own, so a reader that finds the wanted tag in BOTH
+// words holds the value and aux of that store -- whatever the atomicity of the 16-byte
+// access as a whole.  A torn read (one word of this store, one stale) shows a tag
+// mismatch in one word, is counted and re-polled: deterministic, no hash.  A slot's tag
+// (the pivot's global step + 1, < 65535: n <= kKPMaxCw * kKPMaxG) is unique within a call
+// and the slots are cleared per call.  aux carries a candidate position (< 2^16 - 1).
+using Rec = ulonglong2;
+__device__ __forceinline__ Rec pack(double v, unsigned tag, int aux) {
     const unsigned long long b = (unsigned long long)__double_as_longlong(v);
-    const unsigned x = (unsigned)b ^ (unsigned)(b >> 32) ^ 0x9e3779b9u;
-    return (x ^ (x >> 16)) & 0xffffu;
-}
-__device__ __forceinline__ double2 pack(double v, unsigned tag, int aux) {
     const unsigned a16 = (aux == INT_MAX) ? 0xffffu : ((unsigned)aux & 0xffffu);
-    return make_double2(v, __longlong_as_double((long long)(((unsigned long long)tag << 32) | (h16(v) << 16) | a16)));
+    const unsigned long long hdr = ((unsigned long long)(tag & 0xffffu) << 48) | ((unsigned long long)a16 << 32);
+    return make_ulonglong2(hdr | (b >> 32), hdr | (b & 0xffffffffull));
 }
-__device__ __forceinline__ unsigned tag_of(double2 r) {
-    return (unsigned)((unsigned long long)__double_as_longlong(r.y) >> 32);
+__device__ __forceinline__ double val_of(Rec r) {
+    return __longlong_as_double((long long)(((r.x & 0xffffffffull) << 32) | (r.y & 0xffffffffull)));
 }
-__device__ __forceinline__ int aux_of(double2 r) {
-    const unsigned a16 = (unsigned)__double_as_longlong(r.y) & 0xffffu;
+__device__ __forceinline__ unsigned tag_of(Rec r) { return (unsigned)(r.x >> 48); }
+__device__ __forceinline__ int aux_of(Rec r) {
+    const unsigned a16 = (unsigned)(r.x >> 32) & 0xffffu;
     return a16 == 0xffffu ? INT_MAX : (int)a16;
 }
-#ifndef KP_HASH
-#define KP_HASH 1
-#endif
-__device__ __forceinline__ bool rec_ok(double2 r, unsigned tag, unsigned* torn) {
-    if (tag_of(r) != tag) return false;
-    if (!KP_HASH) return true;
-    if ((((unsigned)__double_as_longlong(r.y) >> 16) & 0xffffu) == h16(r.x)) return true;
-    atomicAdd(torn, 1u);
+__device__ __forceinline__ bool rec_ok(Rec r, unsigned tag, unsigned* torn) {
+    const unsigned t = tag & 0xffffu;
+    const bool a = (unsigned)(r.x >> 48) == t, b = (unsigned)(r.y >> 48) == t;
+    if (a && b) return true;
+    if (a != b) atomicAdd(torn, 1u);  // one word of this store, one stale: re-polled
     return false;
 }
-// Record traffic goes through L2 with relaxed gpu-scope accesses.  The polling
-// loads MUST be asm volatile: a plain __ldcg in a spin loop may legally be hoisted
-// by the compiler (it did, depending on the surrounding code), hanging the panel.
-#ifndef KP_LDMODE
-#define KP_LDMODE 0  // microbenchmark knob: 0 relaxed.gpu, 1 __ldcg/__stcg, 2 asm volatile .cg
-#endif
-__device__ __forceinline__ void put(double2* p, double2 v) {
-#if KP_LDMODE == 1 || KP_LDMODE == 3  // 3: weak L2 stores, relaxed polling loads
-    __stcg(p, v);
-#elif KP_LDMODE == 2
-    asm volatile("st.global.cg.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
-#else
-    asm volatile("st.relaxed.gpu.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
-#endif
+// Record traffic goes through L2 with relaxed gpu-scope accesses.  The polling loads
+// MUST be asm volatile: a plain __ldcg in a spin loop may legally be hoisted by the
+// compiler (it was, depending on the surrounding code), hanging the panel.
+__device__ __forceinline__ void put(Rec* p, Rec v) {
+    asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(v.x), "l"(v.y) : "memory");
 }
-__device__ __forceinline__ double2 get(const double2* p) {
-#if KP_LDMODE == 1
-    return __ldcg(p);
-#else
-    double2 v;
-#if KP_LDMODE == 2
-    asm volatile("ld.global.cg.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p) : "memory");
-#else
-    asm volatile("ld.relaxed.gpu.global.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p) : "memory");
-#endif
+__device__ __forceinline__ Rec get(const Rec* p) {
+    Rec v;
+    asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(v.x), "=l"(v.y) : "l"(p) : "memory");
     return v;
-#endif
 }
+__device__ __forceinline__ Rec get1(const Rec* p) { return __ldcg(p); }  // one-shot read (never in a spin loop)
 
 // Exact warp max of non-negative 64-bit patterns (|double| bits order like the values).
 __device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v) {
@@ -120,27 +105,6 @@ __device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v)
 __device__ __forceinline__ unsigned long long abs_bits(double x) {
     return (unsigned long long)__double_as_longlong(x) & 0x7fffffffffffffffull;
 }
-
-// Cluster transport (kCl): every record is pushed into the same shared-memory slot of
-// every CTA of the cluster (DSMEM), and read back from the local copy.
-__device__ __forceinline__ void st_cluster(const double2* local, unsigned rank, double2 v) {
-    const unsigned a = (unsigned)__cvta_generic_to_shared(local);
-    unsigned r;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
-    asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};" ::"r"(r), "d"(v.x), "d"(v.y) : "memory");
-}
-__device__ __forceinline__ double2 ld_shared_volatile(const double2* q) {
-    double2 v;
-    const unsigned a = (unsigned)__cvta_generic_to_shared(q);
-    asm volatile("ld.volatile.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a) : "memory");
-    return v;
-}
-__device__ __forceinline__ void cluster_sync_all() {
-    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-// receive slots per CTA: cand[2][16], wrec[2][16], last[2][64], col[2][16][64] (by step parity)
-constexpr int kClMax = kKPClusterMax;
-constexpr int kRcSlots = 4 * kClMax + 2 * kK2B + 2 * kClMax * kK2B;
 
 // Span log of the panel launches (CTA 0: globaltimer at entry and exit), read by
 // mcnd_debug_kp_spans() for schedule analysis; two stores per panel.
@@ -158,7 +122,7 @@ __device__ unsigned long long g_kp_trace[64][12];
 #endif
 
 // KPER: candidate records per lane of the reducing warp (G <= 32 * KPER)
-template <bool kCl, int KPER>
+template <int KPER>
 __global__ void __launch_bounds__(kThreads, 1) kp_panel_kernel(const KPParams p) {
     extern __shared__ __align__(16) double S[];  // [kB][cw]
     __shared__ double sTi[kB][kB + 1];  // T^{-1}, built one column per step
@@ -185,35 +149,12 @@ __global__ void __launch_bounds__(kThreads, 1) kp_panel_kernel(const KPParams p)
         g_kp_span[span_slot][0] = t_start;
     }
     if (*(volatile const unsigned*)p.abort) return;  // uniform: set only by earlier launches
-    // Record slots: global [step][CTA] history (grid variant) or parity-double-buffered
-    // local slots filled by DSMEM pushes (cluster variant: a step-s+1 push can only be
-    // issued after every CTA has consumed its step-s-1 records, see A below).
-    double2* const rc = reinterpret_cast<double2*>(S + kB * cw);
-    auto CAND = [&](int s, int h) -> double2* { return kCl ? rc + (s & 1) * kClMax + h : p.cand + s * G + h; };
-    auto WREC = [&](int s, int h) -> double2* {
-        return kCl ? rc + 2 * kClMax + (s & 1) * kClMax + h : p.wrec + s * G + h;
-    };
-    auto LAST = [&](int s, int r) -> double2* { return kCl ? rc + 4 * kClMax + (s & 1) * kB + r : p.lastbuf + s * kB + r; };
-    auto COL = [&](int s, int h, int r) -> double2* {
-        return kCl ? rc + 4 * kClMax + 2 * kB + ((s & 1) * kClMax + h) * kB + r : p.colbuf + ((int64_t)s * G + h) * kB + r;
-    };
-    auto PUT = [&](double2* q, double2 v) {
-        if constexpr (kCl) {
-            for (int h = 0; h < G; ++h) st_cluster(q, (unsigned)h, v);
-        } else {
-            put(q, v);
-        }
-    };
-    auto GET = [&](const double2* q) -> double2 {
-        if constexpr (kCl) return ld_shared_volatile(q);
-        else return get(q);
-    };
-    auto GET1 = [&](const double2* q) -> double2 {  // one-shot read (never inside a spin loop)
-        if constexpr (kCl) return ld_shared_volatile(q);
-        else return __ldcg(q);
-    };
-    if constexpr (kCl)
-        for (int e = tid; e < kRcSlots; e += kThreads) rc[e] = make_double2(0.0, 0.0);
+    // Record slots: [step][CTA] history in global memory (L2), reused by every panel
+    // (the tags tell the panels apart)
+    auto CAND = [&](int s, int h) -> Rec* { return p.cand + s * G + h; };
+    auto WREC = [&](int s, int h) -> Rec* { return p.wrec + s * G + h; };
+    auto LAST = [&](int s, int r) -> Rec* { return p.lastbuf + s * kB + r; };
+    auto COL = [&](int s, int h, int r) -> Rec* { return p.colbuf + ((int64_t)s * G + h) * kB + r; };
 
     // ---- load my chunk of the 64 panel rows; running max per row; candidate of row 0
     for (int r = warp; r < kB; r += kThreads / 32) {  // row per warp, 16-byte loads (ld, lo, cw even)
@@ -254,10 +195,7 @@ __global__ void __launch_bounds__(kThreads, 1) kp_panel_kernel(const KPParams p)
         }
         __syncthreads();
         const double* W0 = p.r1_W + lo;
-#ifndef KP_R1_DMMA
-#define KP_R1_DMMA 1
-#endif
-        if (KP_R1_DMMA) {
+        {
             // on the FP64 tensor cores (mma.sync.m8n8k4.f64, k ascending: the trailing GEMM's
             // arithmetic): warp w owns the 8-column tiles w, w + 16, ... (two at a time) for
             // all 64 rows, so every W0 element is read from L2 once per CTA
@@ -316,43 +254,6 @@ __global__ void __launch_bounds__(kThreads, 1) kp_panel_kernel(const KPParams p)
                         if (c + 1 < wc) sp[1] = acc[i][t][1];
                     }
             }
-        } else
-        for (int tb = warp; tb < kB / 4; tb += kThreads / 32) {
-            for (int c0 = 0; c0 < wc; c0 += 128) {
-                double acc[4][4];
-#pragma unroll
-                for (int i = 0; i < 4; ++i)
-#pragma unroll
-                    for (int kk = 0; kk < 4; ++kk) {
-                        const int c = c0 + lane + 32 * kk;
-                        acc[i][kk] = (c < wc) ? S[(4 * tb + i) * cw + c] : 0.0;
-                    }
-                for (int k0 = 0; k0 < kB; k0 += 8) {  // 32 W loads in flight per thread
-                    double w[8][4];
-#pragma unroll
-                    for (int u = 0; u < 8; ++u)
-#pragma unroll
-                        for (int kk = 0; kk < 4; ++kk) {
-                            const int c = c0 + lane + 32 * kk;
-                            w[u][kk] = (c < wc) ? __ldg(W0 + (int64_t)(k0 + u) * p.r1_ldw + c) : 0.0;
-                        }
-#pragma unroll
-                    for (int u = 0; u < 8; ++u)
-#pragma unroll
-                        for (int i = 0; i < 4; ++i) {
-                            const double a = sTi[4 * tb + i][k0 + u];
-#pragma unroll
-                            for (int kk = 0; kk < 4; ++kk) acc[i][kk] = fma(a, w[u][kk], acc[i][kk]);
-                        }
-                }
-#pragma unroll
-                for (int i = 0; i < 4; ++i)
-#pragma unroll
-                    for (int kk = 0; kk < 4; ++kk) {
-                        const int c = c0 + lane + 32 * kk;
-                        if (c < wc) S[(4 * tb + i) * cw + c] = acc[i][kk];
-                    }
-            }
         }
         __syncthreads();
         for (int e = tid; e < kB * (kB + 1); e += kThreads) {
@@ -382,15 +283,14 @@ __global__ void __launch_bounds__(kThreads, 1) kp_panel_kernel(const KPParams p)
         if (r == 0 && j == 0) { s_cv = bv; s_cpos = bi; }
     }
     __syncthreads();
-    if constexpr (kCl) cluster_sync_all();  // every CTA's slots cleared before the first push
 
     // ---- publish the proposal for pivot 0 (row 0's candidate from the load pass)
     if (tid < kB) {
         const int pos = s_cpos;
-        PUT(COL(0, g, tid), pack(pos != INT_MAX ? S[tid * cw + (pos - lo)] : 0.0, p.tag0, 0));
-        if (lo <= m - 1 && m - 1 < lo + wc) PUT(LAST(0, tid), pack(S[tid * cw + (m - 1 - lo)], p.tag0, 0));
-        if (tid == 0) PUT(CAND(0, g), pack(s_cv, p.tag0, pos));
-        if (tid == 1) PUT(WREC(0, g), pack(s_rmax[0], p.tag0, 0));
+        put(COL(0, g, tid), pack(pos != INT_MAX ? S[tid * cw + (pos - lo)] : 0.0, p.tag0, 0));
+        if (lo <= m - 1 && m - 1 < lo + wc) put(LAST(0, tid), pack(S[tid * cw + (m - 1 - lo)], p.tag0, 0));
+        if (tid == 0) put(CAND(0, g), pack(s_cv, p.tag0, pos));
+        if (tid == 1) put(WREC(0, g), pack(s_rmax[0], p.tag0, 0));
     }
 
     KP_MARK(0, 9);
@@ -409,7 +309,7 @@ __global__ void __launch_bounds__(kThreads, 1) kp_panel_kernel(const KPParams p)
         // ---- A. reduce the G proposals for pivot s: warp 0 polls all tagged records
         if (warp == 0) {
             constexpr int kPer = KPER;
-            double2 c[kPer], w[kPer];
+            Rec c[kPer], w[kPer];
             unsigned need = 0;  // bit k: record lane + 32k still missing
 #pragma unroll
             for (int k = 0; k < kPer; ++k)
@@ -418,12 +318,12 @@ __global__ void __launch_bounds__(kThreads, 1) kp_panel_kernel(const KPParams p)
 #pragma unroll
                 for (int k = 0; k < kPer; ++k)
                     if (need & (1u << k)) {
-                        c[k] = GET(CAND(s, lane + 32 * k));
-                        w[k] = GET(WREC(s, lane + 32 * k));
+                        c[k] = get(CAND(s, lane + 32 * k));
+                        w[k] = get(WREC(s, lane + 32 * k));
                     }
 #pragma unroll
                 for (int k = 0; k < kPer; ++k)
-                    if ((need & (1u << k)) && rec_ok(c[k], tag, &p.err->pad) && rec_ok(w[k], tag, &p.err->pad))
+                    if ((need & (1u << k)) && rec_ok(c[k], tag, &p.err->torn) && rec_ok(w[k], tag, &p.err->torn))
                         need &= ~(1u << k);
                 if (__all_sync(kFull, need == 0)) break;
                 if ((it & 7u) == 7u && globaltimer() - t_start > p.timeout_ns) {
@@ -464,10 +364,11 @@ __global__ void __launch_bounds__(kThreads, 1) kp_panel_kernel(const KPParams p)
             for (int k = 0; k < kPer; ++k) {
                 const int h = lane + 32 * k;
                 if (h < G) {
-                    const unsigned long long xb = abs_bits(c[k].x);
+                    const double xv = val_of(c[k]);
+                    const unsigned long long xb = abs_bits(xv);
                     const int xi = aux_of(c[k]);
-                    if (xb > kb || (xb == kb && xi < bi)) { kb = xb; bi = xi; bv = c[k].x; bg = h; }
-                    wb = max(wb, abs_bits(w[k].x));
+                    if (xb > kb || (xb == kb && xi < bi)) { kb = xb; bi = xi; bv = xv; bg = h; }
+                    wb = max(wb, abs_bits(val_of(w[k])));
                 }
             }
             const unsigned long long mb = warp_max_u64(kb);
@@ -483,16 +384,16 @@ __global__ void __launch_bounds__(kThreads, 1) kp_panel_kernel(const KPParams p)
             if (fabs(bv) > kSingularRtol * bw) {
                 // all four records in flight at once (one round trip); first a plain L2 read
                 // (usually already there), strong re-polls only for what had not arrived
-                double2 cm[2], cl[2];
+                Rec cm[2], cl[2];
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
-                    cm[h] = GET1(COL(s, bg, lane + 32 * h));
-                    cl[h] = GET1(LAST(s, lane + 32 * h));
+                    cm[h] = get1(COL(s, bg, lane + 32 * h));
+                    cl[h] = get1(LAST(s, lane + 32 * h));
                 }
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                     const int r = lane + 32 * h;
-                    while (!rec_ok(cm[h], tag, &p.err->pad) || !rec_ok(cl[h], tag, &p.err->pad)) {
+                    while (!rec_ok(cm[h], tag, &p.err->torn) || !rec_ok(cl[h], tag, &p.err->torn)) {
                         if (globaltimer() - t_start > p.timeout_ns) {
 #ifdef KP_DEBUG
                             printf("KP timeout col: g=%d s=%d row0=%d m=%d G=%d r=%d bg=%d bi=%d coltag %x lasttag %x want %x\n",
@@ -508,11 +409,11 @@ __global__ void __launch_bounds__(kThreads, 1) kp_panel_kernel(const KPParams p)
                             s_stop = 1;
                             break;
                         }
-                        cm[h] = GET(COL(s, bg, r));
-                        cl[h] = GET(LAST(s, r));
+                        cm[h] = get(COL(s, bg, r));
+                        cl[h] = get(LAST(s, r));
                     }
-                    s_mult[r] = cm[h].x;
-                    s_last[r] = cl[h].x;
+                    s_mult[r] = val_of(cm[h]);
+                    s_last[r] = val_of(cl[h]);
                 }
             }
             if (s > 0) KP_MARK(s, 10);
@@ -598,8 +499,8 @@ __global__ void __launch_bounds__(kThreads, 1) kp_panel_kernel(const KPParams p)
                     const double rm = fmax(fmax(s_rmax[s + 1], s_rmax2[s + 1]), m0);
                     s_rmax[s + 1] = rm;
                     // proposal of pivot s+1 goes out now; its column follows in D2
-                    PUT(WREC(s + 1, g), pack(rm, tag1, 0));
-                    PUT(CAND(s + 1, g), pack(v0, tag1, i0));
+                    put(WREC(s + 1, g), pack(rm, tag1, 0));
+                    put(CAND(s + 1, g), pack(v0, tag1, i0));
                     KP_MARK(s, 6);
                 }
             }
@@ -645,9 +546,9 @@ __global__ void __launch_bounds__(kThreads, 1) kp_panel_kernel(const KPParams p)
                     xl = row[lc];
                     if (r > s + 1) { xl = __dsub_rn(xl, __dmul_rn(mu, us[lc])); row[lc] = xl; mx = fmax(mx, fabs(xl)); }
                 }
-                PUT(LAST(s + 1, r), pack(xl, tag1, 0));
+                put(LAST(s + 1, r), pack(xl, tag1, 0));
             }
-            PUT(COL(s + 1, g, r), pack(xc, tag1, 0));
+            put(COL(s + 1, g, r), pack(xc, tag1, 0));
             if (r > s + 1) s_rmax2[r] = fmax(s_rmax2[r], mx);
         } else {
             // ---- E. bulk (warps 2..15): rows > s+1, all columns except pc / lc, with the
@@ -712,10 +613,7 @@ __global__ void __launch_bounds__(kThreads, 1) kp_panel_kernel(const KPParams p)
     // ---- W = T^{-1} U on my final columns (T unit upper triangular)
     {
     const int wf = max(0, min(wc, m - kB - lo));
-#ifndef KP_W_DMMA
-#define KP_W_DMMA 1
-#endif
-    if (KP_W_DMMA) {
+    {
         // W = T^{-1} U on the FP64 tensor cores (mma.sync.m8n8k4.f64; A = T^{-1}, B = U, the
         // chunk itself), straight to global.  Warp w owns the 8-column tiles w, w + 16, ...
         // (two at a time) for all 64 rows; row block mb joins at its diagonal (k0 >= 8 mb):
@@ -760,36 +658,6 @@ __global__ void __launch_bounds__(kThreads, 1) kp_panel_kernel(const KPParams p)
                     else if (c < wf) wr[0] = acc[i][t][0];
                 }
         }
-    } else {
-    // W = T^{-1} U straight to global: warp w owns rows 4w..4w+3, lane owns columns
-    // lane + 32k (k < 4) of each 128-column pass: T^{-1} reads are warp broadcasts, U
-    // reads and W stores are contiguous across the warp
-    for (int tb = warp; tb < kB / 4; tb += kThreads / 32) {
-        for (int c0 = 0; c0 < wf; c0 += 128) {
-            double acc[4][4] = {};
-            for (int j = 4 * tb; j < kB; ++j) {
-                double u[4];
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const int c = c0 + lane + 32 * k;
-                    u[k] = (c < wf) ? S[j * cw + c] : 0.0;
-                }
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    const double a = sTi[4 * tb + i][j];
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) acc[i][k] = fma(a, u[k], acc[i][k]);
-                }
-            }
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const int c = c0 + lane + 32 * k;
-                    if (c < wf) p.W[(int64_t)(4 * tb + i) * p.ldw + lo + c] = acc[i][k];
-                }
-        }
-    }
     }
     KP_MARK(1, 11);
     // ---- panel-start column of each pivot and the moved final columns (CTA 0)
@@ -868,8 +736,7 @@ __global__ void __launch_bounds__(kThreads, 1) kp_panel_kernel(const KPParams p)
     }
     KP_MARK(0, 11);
     if (g == 0 && tid == 0) g_kp_span[span_slot][1] = globaltimer();
-finish:
-    if constexpr (kCl) cluster_sync_all();  // no CTA leaves while peers may still push into it
+finish:;
 }
 
 }  // namespace
@@ -884,66 +751,20 @@ int kp_debug_spans(unsigned long long* out, int max_spans) {
     return k;
 }
 
-size_t kp_smem_bytes(int cw, bool cluster) {
-    return (size_t)kB * cw * sizeof(double) + (cluster ? kRcSlots * sizeof(double2) : 0);
-}
-
-int kp_cluster_fits(int G, int cw) {
-    if (G < 1 || G > kClMax) return 0;
-    const size_t smem = kp_smem_bytes(cw, true);
-    if (cudaFuncSetAttribute(kp_panel_kernel<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
-        cudaFuncSetAttribute(kp_panel_kernel<true, 1>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
-        cudaGetLastError();
-        return 0;
-    }
-    cudaLaunchConfig_t cfg = {};
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = (unsigned)G;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.gridDim = dim3((unsigned)G);
-    cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = smem;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, kp_panel_kernel<true, 1>, &cfg) != cudaSuccess) {
-        cudaGetLastError();
-        return 0;
-    }
-    return n;
-}
+size_t kp_smem_bytes(int cw) { return (size_t)kB * cw * sizeof(double); }
 
 cudaError_t kp_launch(const KPParams& p, cudaStream_t s) {
-    const bool cl = p.cluster != 0;
-    const size_t smem = kp_smem_bytes(p.cw, cl);
+    const size_t smem = kp_smem_bytes(p.cw);
     if (p.cw < 2 || (p.cw & 1) || p.cw > kKPMaxCw || p.G < 1 || p.G > kKPMaxG) return cudaErrorInvalidValue;
-    KPParams pc = p;
-    if (cl) {
-        cudaError_t e = cudaFuncSetAttribute(kp_panel_kernel<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e == cudaSuccess) e = cudaFuncSetAttribute(kp_panel_kernel<true, 1>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        if (e != cudaSuccess) return e;
-        cudaLaunchConfig_t cfg = {};
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeClusterDimension;
-        at[0].val.clusterDim.x = (unsigned)p.G;
-        at[0].val.clusterDim.y = 1;
-        at[0].val.clusterDim.z = 1;
-        cfg.gridDim = dim3((unsigned)p.G);
-        cfg.blockDim = dim3(kThreads);
-        cfg.dynamicSmemBytes = smem;
-        cfg.stream = s;
-        cfg.attrs = at;
-        cfg.numAttrs = 1;
-        return cudaLaunchKernelEx(&cfg, kp_panel_kernel<true, 1>, pc);
-    }
-    const void* fn = p.G <= 32   ? (const void*)kp_panel_kernel<false, 1>
-                     : p.G <= 64 ? (const void*)kp_panel_kernel<false, 2>
-                     : p.G <= 96 ? (const void*)kp_panel_kernel<false, 3>
-                                 : (const void*)kp_panel_kernel<false, kKPMaxG / 32>;
+    if (p.tag0 < 1 || p.tag0 + kB >= 0xffffu) return cudaErrorInvalidValue;  // 16-bit record tags
+    const void* fn = p.G <= 32   ? (const void*)kp_panel_kernel<1>
+                     : p.G <= 64 ? (const void*)kp_panel_kernel<2>
+                     : p.G <= 96 ? (const void*)kp_panel_kernel<3>
+                                 : (const void*)kp_panel_kernel<kKPMaxG / 32>;
+    // set on every launch: the attribute is per device (context), calls may alternate devices
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
+    KPParams pc = p;
     void* args[] = {&pc};
     return cudaLaunchCooperativeKernel(fn, dim3(p.G), dim3(kThreads), args, smem, s);
 }

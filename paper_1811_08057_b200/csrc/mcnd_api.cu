@@ -73,15 +73,6 @@ struct Buffers {
     cudaEvent_t ev_arr[kMaxChunks] = {};
     int sms = 0;
     uint32_t epoch = 0;
-    std::map<std::pair<int64_t, int64_t>, bool> kp_cluster_cache;  // (G, cw) -> co-residency
-    bool kp_cluster_ok(int64_t G, int64_t cw) {
-        const auto key = std::make_pair(G, cw);
-        auto it = kp_cluster_cache.find(key);
-        if (it != kp_cluster_cache.end()) return it->second;
-        const bool ok = kp_cluster_fits((int)G, (int)cw) > 0;
-        kp_cluster_cache[key] = ok;
-        return ok;
-    }
 };
 std::mutex g_mu;
 std::deque<Buffers> g_bufs;
@@ -802,9 +793,9 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
     const size_t o_W = take((size_t)kRing * 2 * b * ld * sizeof(double));
     const size_t o_pan = take((2 + kRing) * sizeof(K2Gather));           // gp0, gp1, gpair ring
     const size_t o_Wp = take((size_t)kRing * b * b * sizeof(double));
-    const size_t o_cand = take((size_t)64 * kKPMaxG * sizeof(double2));
-    const size_t o_wrec = take((size_t)64 * kKPMaxG * sizeof(double2));
-    const size_t o_colb = take((size_t)64 * kKPMaxG * 64 * sizeof(double2));
+    const size_t o_cand = take((size_t)64 * kKPMaxG * sizeof(ulonglong2));
+    const size_t o_wrec = take((size_t)64 * kKPMaxG * sizeof(ulonglong2));
+    const size_t o_colb = take((size_t)64 * kKPMaxG * 64 * sizeof(ulonglong2));
     const size_t o_lastb = take(kLastBufBytes);
     const size_t o_ctl = take(sizeof(K1Err) + 16);
     // int metadata: iota[n] | never[n] | panel_ptr[b+1] | init_ptr[G0+1] init_rows[n] | tail_ptr[Gt+1] tail_rows[mt]
@@ -920,16 +911,12 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
     kp.epoch = epoch;
     kp.ldw = ld;
     kp.abort = abort;
-    kp.cand = (double2*)(base + o_cand);
-    kp.wrec = (double2*)(base + o_wrec);
-    kp.colbuf = (double2*)(base + o_colb);
-    kp.lastbuf = (double2*)(base + o_lastb);
+    kp.cand = (ulonglong2*)(base + o_cand);
+    kp.wrec = (ulonglong2*)(base + o_wrec);
+    kp.colbuf = (ulonglong2*)(base + o_colb);
+    kp.lastbuf = (ulonglong2*)(base + o_lastb);
     kp.err = err;
     kp.timeout_ns = 20ull * 1000000000ull;
-    // Panel placement: one thread-block cluster of up to kKPClusterMax CTAs (records
-    // pushed over DSMEM) whenever the panel fits its shared memory, else the
-    // grid-wide cooperative variant (records through L2).
-    const int64_t g_cl = std::min<int64_t>(env_long("MCND_KP_CLUSTER", 0), kKPClusterMax);
     auto split = [&](int64_t m, int64_t G, int64_t* cw_out) {
         int64_t cw = 0;
         for (;; --G) {
@@ -955,15 +942,8 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
     auto run_kp = [&](int64_t kb, K2Gather* gp, double* Wout) -> cudaError_t {
         const int64_t m = n - kb;
         int64_t cw = 0, G = 0;
-        kp.cluster = 0;
-        if (g_cl >= 2) {
-            G = split(m, std::min<int64_t>(g_cl, std::max<int64_t>(1, m / 64)), &cw);
-            kp.cluster = (G >= 2 && kp_smem_bytes((int)cw, true) <= 200 * 1024 && B->kp_cluster_ok(G, cw)) ? 1 : 0;
-        }
-        if (!kp.cluster) {
-            G = split(m, kp_ctas(m), &cw);
-            if (kp_smem_bytes((int)cw, false) > 190 * 1024) return cudaErrorInvalidValue;
-        }
+        G = split(m, kp_ctas(m), &cw);
+        if (kp_smem_bytes((int)cw) > 190 * 1024) return cudaErrorInvalidValue;
         kp.row0 = (int32_t)kb;
         kp.m = (int32_t)m;
         kp.G = (int32_t)G;
@@ -1231,7 +1211,7 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
     float ms = 0.f;
     cudaEventElapsedTime(&ms, B->ev0, B->ev1);
     out->device_ms = ms;
-    if (h_err->pad && std::getenv("MCND_DEBUG")) std::fprintf(stderr, "mcnd: %u torn panel records re-read\n", h_err->pad);
+    out->torn_reads = h_err->torn;
     if (h_err->nonfinite) return fail(MCND_EINVAL, "matrix entries must be finite (no NaN/Inf)");
     if (h_err->error)
         return fail(MCND_EDEVICE, "device timeout waiting for pivot %u [%u g=%u s=%u i=%u tags %x %x want %x G/r=%u]",
@@ -1295,7 +1275,7 @@ struct MgHandle {
     PivRec* recs = nullptr;
     double* L = nullptr;       // [2][lr][128]
     K2Gather* gp = nullptr;    // [2]
-    double2 *cand = nullptr, *wrec = nullptr, *colb = nullptr, *lastb = nullptr;
+    ulonglong2 *cand = nullptr, *wrec = nullptr, *colb = nullptr, *lastb = nullptr;
     K1Err* err = nullptr;
     unsigned* abort = nullptr;
     int32_t* d_int = nullptr;  // iota[max(n,lr)] | never[lr] | init deal ptr[G0+1] rows[lr]
@@ -1325,9 +1305,9 @@ int mg_create(int64_t n, int64_t lr, MgHandle** out) {
     const size_t o_rec = take((size_t)n * sizeof(PivRec));
     const size_t o_L = take((size_t)2 * lrr * 2 * b * sizeof(double));
     const size_t o_gp = take(2 * sizeof(K2Gather));
-    const size_t o_cand = take((size_t)64 * kKPMaxG * sizeof(double2));
-    const size_t o_wrec = take((size_t)64 * kKPMaxG * sizeof(double2));
-    const size_t o_colb = take((size_t)64 * kKPMaxG * 64 * sizeof(double2));
+    const size_t o_cand = take((size_t)64 * kKPMaxG * sizeof(ulonglong2));
+    const size_t o_wrec = take((size_t)64 * kKPMaxG * sizeof(ulonglong2));
+    const size_t o_colb = take((size_t)64 * kKPMaxG * 64 * sizeof(ulonglong2));
     const size_t o_lastb = take(kLastBufBytes);
     const size_t o_ctl = take(sizeof(K1Err) + 16);
     const int64_t ni = std::max<int64_t>(n, lrr);
@@ -1345,10 +1325,10 @@ int mg_create(int64_t n, int64_t lr, MgHandle** out) {
     h->recs = (PivRec*)(base + o_rec);
     h->L = (double*)(base + o_L);
     h->gp = (K2Gather*)(base + o_gp);
-    h->cand = (double2*)(base + o_cand);
-    h->wrec = (double2*)(base + o_wrec);
-    h->colb = (double2*)(base + o_colb);
-    h->lastb = (double2*)(base + o_lastb);
+    h->cand = (ulonglong2*)(base + o_cand);
+    h->wrec = (ulonglong2*)(base + o_wrec);
+    h->colb = (ulonglong2*)(base + o_colb);
+    h->lastb = (ulonglong2*)(base + o_lastb);
     h->err = (K1Err*)(base + o_ctl);
     h->abort = (unsigned*)(base + o_ctl + sizeof(K1Err));
     h->d_int = (int32_t*)(base + o_int);
@@ -1441,7 +1421,6 @@ KPParams mg_kp(MgHandle* h, int64_t lr0, int64_t t, int64_t m, K2Gather* gp, dou
     kp.lastbuf = h->lastb;
     kp.err = h->err;
     kp.timeout_ns = 20ull * 1000000000ull;
-    kp.cluster = 0;
     return kp;
 }
 

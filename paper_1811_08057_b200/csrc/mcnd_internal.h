@@ -25,7 +25,7 @@ struct K1Err {
     unsigned error;     // nonzero: device-side timeout
     unsigned err_step;
     unsigned nonfinite; // nonzero: the input held NaN/Inf (-> ValueError)
-    unsigned pad;
+    unsigned torn;      // panel records read torn (one word stale) and re-polled
     unsigned dbg[8];    // diagnostics of the first timeout (panel kernel)
 };
 
@@ -86,8 +86,10 @@ struct K2Gather {
     int32_t moved_src[2 * kK2B];
 };
 // Column-distributed panel factorisation (k2_panel.cu).  Every exchanged
-// value travels in a 16-byte record {value, tag|aux} written with ONE 16-byte
-// store, so readers poll the records themselves (no fences, no counters).
+// value travels in a 16-byte record of two tagged 8-byte words
+// {tag:16 | aux:16 | half of the value} written with ONE 16-byte store, so readers
+// poll the records themselves (no fences, no counters) and detect a torn read
+// deterministically (a tag mismatch in either word).
 struct KPParams {
     double* ws;
     int64_t ld;
@@ -98,18 +100,17 @@ struct KPParams {
     const double* wit;        // running witnesses, global row index
     PivRec* rec;              // this panel's 64 pivot records
     uint32_t epoch;
-    uint32_t tag0;            // record tag of step s is tag0 + s (the global step + 1; slots cleared per call)
+    uint32_t tag0;            // record tag of step s is tag0 + s (the global step + 1 < 65535; slots cleared per call)
     double* W;                // out: T^{-1} U, 64 x (m - 64), row stride ldw
     int64_t ldw;
     K2Gather* pan;            // out: panel-start pivot columns (P[0..63]), moved columns
     unsigned* abort;
-    double2* cand;            // [64][G]   {candidate value, pos | tag}
-    double2* wrec;            // [64][G]   {running max of the pivot row, tag}
-    double2* colbuf;          // [64][G][64] {candidate column values, tag}
-    double2* lastbuf;         // [64][64]  {last active column values, tag}
+    ulonglong2* cand;         // [64][G]   {candidate value, pos, tag}
+    ulonglong2* wrec;         // [64][G]   {running max of the pivot row, tag}
+    ulonglong2* colbuf;       // [64][G][64] {candidate column values, tag}
+    ulonglong2* lastbuf;      // [64][64]  {last active column values, tag}
     K1Err* err;
     unsigned long long timeout_ns;
-    int32_t cluster;          // 1: one thread-block cluster, records pushed over DSMEM (G <= kKPClusterMax)
     // second panel of a pair: CTA 0 also runs the pair prep (k2_pair_prep.cuh) at the end
     const K2Gather* pp_g0;    // the pair's first descriptor (nullptr: no pair prep)
     double* pp_W;             // W of the pair (rows 0..63 = W_k), row stride pp_ldw
@@ -133,11 +134,8 @@ constexpr int kKPMaxG = 160;
 constexpr int kPPBars = 1024;  // pairs per call (n <= 131072)
 constexpr size_t kLastBufBytes = (size_t)64 * 64 * 16 + (size_t)kPPBars * sizeof(unsigned);
 constexpr int kKPMaxCw = 380;  // columns per panel CTA (64 x 380 doubles = 190 KB of shared memory)
-constexpr int kKPClusterMax = 16;
 cudaError_t kp_launch(const KPParams& p, cudaStream_t s);
-size_t kp_smem_bytes(int cw, bool cluster);
-// clusters of G CTAs (chunk width cw) that can be co-resident; 0 if the shape cannot launch
-int kp_cluster_fits(int G, int cw);
+size_t kp_smem_bytes(int cw);
 // debug: (entry, exit) globaltimer of the panel launches since the last call; returns the count
 int kp_debug_spans(unsigned long long* out, int max_spans);
 

@@ -498,14 +498,16 @@ def bench_main(args):
     dist.all_reduce(lt)  # every rank's kernels
     launches = int(lt.item())
     grp.close()
+    peak = B.fp64_peak(local) if (rank == 0 and method == "blocked") else None
     if rank == 0:
         t = float(ms.item())
         hbm, peak_kind = B.peaks()
         if method == "blocked":
             achieved = B.flops(n) / (float(km.item()) * 1e-3) / 1e12
-            roof = {"bound": "tensor", "achieved": achieved, "peak": B.FP64_PEAK_TFLOPS * world,
-                    "peak_kind": f"measured cuBLAS DGEMM x{world}", "unit": "TFLOP/s",
-                    "frac": achieved / (B.FP64_PEAK_TFLOPS * world), "traffic": None}
+            pk = peak["tflops"]
+            roof = {"bound": "tensor", "achieved": achieved, "peak": pk * world,
+                    "peak_kind": peak["how"] + f" (rank 0) x{world}", "unit": "TFLOP/s",
+                    "frac": achieved / (pk * world), "traffic": None}
         else:
             Bb = B.algorithmic_bytes(n)
             achieved = Bb / (float(km.item()) * 1e-3) / 1e9
@@ -518,12 +520,7 @@ def bench_main(args):
             "scaling": "strong",
             "vs_baseline": (B.PAPER_TABLE3_N8000.get(world) / (t / 1e3)) if (args.config == "c3" and world in B.PAPER_TABLE3_N8000) else None,
             "dtype": "f64", "data": "synthetic (numpy PCG64 seed, BASELINE recipe)",
-            "config": {"workload": name, "n": n, "method": method,
-                       "parallelism": (f"block rows x{world} GPUs: panel pairs from the rank with the most live rows, "
-                                       "W broadcast (NCCL), local rank-128 updates") if method == "blocked" else
-                                      f"block-row x{world} GPUs, pivot rows pushed over NVLink",
-                       "mode": "fast-fma" if args.fast else "reference-exact",
-                       "l2": "input larger than L2 per rank" if 8 * n * n / world > 126e6 else "per-rank block fits L2"},
+            "config": B.bench_config(args, name, n, world),
             "result": {"sign": res.sign, "log_abs": res.log_abs},
             "roofline": roof,
             "e2e": {"value": B.flops(n) / (float(ms_e.item()) * 1e-3) / 1e9, "unit": "GFLOP/s",
@@ -589,8 +586,7 @@ def _bench_batched(args, B, name, a, n, rank, world, local):
         line = {"metric": B.metric_name("c4"), "value": fl / (t * 1e-3) / 1e9, "unit": "GFLOP/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": t, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (numpy PCG64 seed 4)",
-                "config": {"workload": name, "batch": a.shape[0], "n": n, "parallelism": f"batch sharded x{world}",
-                           "l2": "L2 flushed between iterations"},
+                "config": B.bench_config(args, name, n, world, batch=a.shape[0]),
                 "roofline": {"bound": "hbm", "achieved": byt / (t * 1e-3) / 1e9, "peak": hbm * world,
                              "peak_kind": peak_kind + f" x{world}", "unit": "GB/s",
                              "frac": byt / (t * 1e-3) / 1e9 / (hbm * world), "traffic": None},

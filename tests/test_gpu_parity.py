@@ -228,6 +228,21 @@ def test_c2_spd_4000_vs_oracle(mc):
     gotp = mc.mc_parallel(a, 2)
     assert (gotp.logdet.sign, gotp.logdet.log_abs) == (refp.sign, refp.log_abs)
     assert gotp.stats.broadcasts == 4000 - 2
+    # the blocked variant (the default method for N >= 2048) on the same bytes: sign exact,
+    # |d log| within the north_star tolerance max(1e-8 N, 1e-10 |log|) = 4e-5, pivot
+    # columns as the reference's rule picks them (SPD: no near-ties)
+    for src in (a, mc_device(a)):
+        got, piv, cols, _ = mc.logdet_blocked(src, return_pivots=True)
+        assert got.sign == ref.sign
+        assert abs(got.log_abs - ref.log_abs) <= tol(4000, ref.log_abs), (got.log_abs, ref.log_abs)
+        assert np.array_equal(cols, ref.cols)
+        assert mc._lib.LAST_TORN_READS == 0
+
+
+def mc_device(a):
+    import torch
+
+    return torch.from_numpy(a).cuda()
 
 
 def test_c3_uniform_8000(mc):
@@ -245,6 +260,37 @@ def test_c3_uniform_8000(mc):
         else:
             got = mc.mc_parallel(a, c["p"]).logdet
         assert (got.sign, got.log_abs) == expect(c), name
+
+
+def test_blocked_c3_vs_reference_golden(mc):
+    """The headline path: blocked C3 (N=8000 U[-1,1] seed 3) against the reference's own
+    logdet_condensation result (condense.py:134-160, the committed 28-minute golden), for
+    a resident device matrix and for the streamed pinned-host input; sign exact and
+    |d log| <= max(1e-8 N, 1e-10 |log|) = 8e-5 (north_star; test_acceptance.py:36-56's
+    10-digit bar is 2.8e-6 here, also met); every pivot column is the reference's."""
+    import torch
+    from paper_1811_08057_b200 import matrix as M
+
+    cases = [c for c in load_cases() if c["name"] == "c3_uniform_8000_s3"]
+    assert cases, "C3 golden missing"
+    c = cases[0]
+    a = M.config_uniform(8000, 3)
+    assert digest(a) == c["input_digest"]
+    sign, la = expect(c)
+    d = torch.from_numpy(a).cuda()
+    # the unblocked path is bitwise the reference (test_c3_uniform_8000): its pivot
+    # columns are the reference's
+    exact, _, ref_cols, _ = mc.logdet_condensation(d, return_pivots=True)
+    assert exact == (sign, la)
+    pinned = torch.empty((8000, 8000), dtype=torch.float64, pin_memory=True)
+    pinned.copy_(torch.from_numpy(a))
+    for src in (d, pinned.numpy()):
+        got, piv, cols, _ = mc.logdet_blocked(src, return_pivots=True)
+        assert got.sign == sign
+        assert abs(got.log_abs - la) <= tol(8000, la), (got.log_abs, la)
+        assert abs(got.log_abs - la) <= 1e-10 * abs(la)
+        assert mc._lib.LAST_TORN_READS == 0
+        assert np.mean(cols == ref_cols) > 0.999
 
 
 def test_batched_c4_vs_oracle(mc):
@@ -328,18 +374,6 @@ def test_blocked_vs_oracle(mc, env_knob, tail):
         assert abs(got.log_abs - ref.log_abs) <= tol(n, ref.log_abs), (n, got.log_abs, ref.log_abs)
         assert np.mean(cols == ref.cols) > 0.99
         assert np.allclose(piv, ref.pivots, rtol=1e-8, atol=1e-12)
-
-
-def test_blocked_cluster_transport_identical(mc, env_knob):
-    """The panel kernel's DSMEM (thread-block cluster) transport performs exactly
-    the grid transport's arithmetic: identical pivots and log|det|."""
-    a = np.random.default_rng(21).uniform(-1, 1, (1500, 1500))
-    env_knob("MCND_KP_CLUSTER", 0)
-    ref = mc.logdet_blocked(a, return_pivots=True)
-    env_knob("MCND_KP_CLUSTER", 16)
-    got = mc.logdet_blocked(a, return_pivots=True)
-    assert got[0] == ref[0]
-    assert np.array_equal(got[1], ref[1]) and np.array_equal(got[2], ref[2])
 
 
 @pytest.mark.parametrize("maxg", [6, 7])
