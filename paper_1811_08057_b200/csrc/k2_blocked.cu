@@ -25,7 +25,6 @@
 #include <cstdint>
 #include <cstdlib>
 #include "mcnd_internal.h"
-#include "k2_pair_prep.cuh"
 
 namespace mcnd {
 namespace {
@@ -144,17 +143,6 @@ __global__ void __launch_bounds__(kGLThreads) k2_gather_lcorr_kernel(double* __r
     }
 }
 
-// Single CTA (512 threads): the standalone pair prep (k2_pair_prep.cuh).
-constexpr int kPrepThreads = 512;
-__global__ void __launch_bounds__(kPrepThreads) k2_pair_prep_kernel(const K2Gather* __restrict__ g0,
-                                                                    const K2Gather* __restrict__ g1, int32_t m,
-                                                                    double* __restrict__ Wc, int64_t ldw,
-                                                                    double* __restrict__ Wp, K2Gather* __restrict__ gpair,
-                                                                    const unsigned* __restrict__ abort) {
-    if (*(volatile const unsigned*)abort) return;
-    __shared__ PairPrepSmem sm;
-    pair_prep_body<kPrepThreads>(g0, g1, m, Wc, ldw, Wp, gpair, sm, threadIdx.x);
-}
 
 // ---- DMMA GEMM: C[M x N2] (rows rbase.., in ws) += NL[M x K] * W[K x N2], K = 64 or 128, where
 // NL = -L is stored negated by the gather so the DMMA operands carry no negation (keeps the
@@ -536,9 +524,8 @@ cudaError_t k2_gather_fix(double* ws, int64_t ld, int32_t rbase, int32_t nrows, 
     if (nrows <= 0) return cudaSuccess;
     const int warps = 8;
     const dim3 grid((nrows + warps - 1) / warps);
-    if (K == 64) k2_gather_fix_kernel<64><<<grid, warps * 32, 0, s>>>(ws, ld, rbase, nrows, gp, L, abort);
-    else if (K == 128) k2_gather_fix_kernel<128><<<grid, warps * 32, 0, s>>>(ws, ld, rbase, nrows, gp, L, abort);
-    else return cudaErrorInvalidValue;
+    if (K != 64) return cudaErrorInvalidValue;  // the pair path gathers with k2_gather_lcorr
+    k2_gather_fix_kernel<64><<<grid, warps * 32, 0, s>>>(ws, ld, rbase, nrows, gp, L, abort);
     return cudaGetLastError();
 }
 
@@ -554,11 +541,6 @@ cudaError_t k2_gather_lcorr(double* ws, int64_t ld, int32_t rbase, int32_t nrows
     return cudaGetLastError();
 }
 
-cudaError_t k2_pair_prep(const K2Gather* g0, const K2Gather* g1, int32_t m, double* Wc, int64_t ldw, double* Wp,
-                         K2Gather* gpair, const unsigned* abort, cudaStream_t s) {
-    k2_pair_prep_kernel<<<1, kPrepThreads, 0, s>>>(g0, g1, m, Wc, ldw, Wp, gpair, abort);
-    return cudaGetLastError();
-}
 
 cudaError_t k2_gemm(double* ws, int64_t ld, int32_t rbase, int32_t M, int32_t N2, int32_t K, const double* L,
                     int64_t ldl, const double* W, int64_t ldw, double* row_wit, const unsigned* abort, cudaStream_t s,

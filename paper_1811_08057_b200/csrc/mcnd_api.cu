@@ -69,13 +69,14 @@ struct Buffers {
     cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_c = nullptr;  // K2: stream joins
     cudaEvent_t ev_in = nullptr, ev_out = nullptr;
     cudaStream_t cpy = nullptr;                  // K2 host input: row chunks copied while the first pairs run
+    std::mutex mu;                               // calls on this device are serialised; other devices run concurrently
     static constexpr int kMaxChunks = 32;
     cudaEvent_t ev_arr[kMaxChunks] = {};
     int sms = 0;
     uint32_t epoch = 0;
 };
-std::mutex g_mu;
-std::deque<Buffers> g_bufs;
+std::mutex g_mu;             // guards g_bufs (the list, not the buffers)
+std::deque<Buffers> g_bufs;  // one per device; deque: element addresses are stable
 
 int init_buffers(Buffers& b, int dev) {
     b.device = dev;
@@ -102,10 +103,13 @@ Buffers* buffers_for_current(int* code) {
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) { *code = fail(MCND_ECUDA, "cudaGetDevice: %s", cudaGetErrorString(e)); return nullptr; }
+    std::lock_guard<std::mutex> lk(g_mu);
     for (auto& b : g_bufs) if (b.device == dev) return &b;
-    Buffers b;
-    if ((*code = init_buffers(b, dev)) != MCND_OK) return nullptr;
-    g_bufs.push_back(b);
+    g_bufs.emplace_back();
+    if ((*code = init_buffers(g_bufs.back(), dev)) != MCND_OK) {
+        g_bufs.pop_back();
+        return nullptr;
+    }
     return &g_bufs.back();
 }
 
@@ -698,16 +702,28 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
     if (!B) return code;
     // The panel chain runs on a highest-priority stream, the overlapped trailing
     // updates on a lowest-priority one: SMs freed by the trailing GEMM's CTAs go to
-    // the next panel first.  Joined with the caller's stream at entry and exit.
-    const bool prio = env_long("MCND_K2_PRIO", 1) != 0;
-    cudaStream_t st = prio ? B->crit : st_caller;
-    if (st != st_caller) {
-        CUDA_TRY(cudaEventRecord(B->ev_in, st_caller));
-        CUDA_TRY(cudaStreamWaitEvent(st, B->ev_in, 0));
-    }
+    // the next panel first.  Joined with the caller's stream at entry and exit; the
+    // copy stream of the previous call is drained first (it may still hold reads of
+    // its caller's buffer and writes into din).
+    cudaStream_t st = B->crit;
+    CUDA_TRY(cudaEventRecord(B->ev_in, st_caller));
+    CUDA_TRY(cudaStreamWaitEvent(st, B->ev_in, 0));
+    // any early return after this point drains the library's streams first: the next call
+    // reuses din and the workspace, and a streamed copy may still read the caller's buffer
+    struct Drain {
+        Buffers* B;
+        bool armed = true;
+        ~Drain() {
+            if (!armed) return;
+            cudaStreamSynchronize(B->cpy);
+            cudaStreamSynchronize(B->side);
+            cudaStreamSynchronize(B->crit);
+            cudaGetLastError();
+        }
+    } drain{B};
     const bool fast = (flags & MCND_FLAG_FAST) != 0;
     const int64_t b = kK2B;
-    int64_t m_tail = env_long("MCND_K2_TAIL", 64);
+    int64_t m_tail = env_long("MCND_K2_TAIL", 64);  // test hook: rows finished by the unblocked K1 tail
     if (m_tail < 2) m_tail = 2;
     const int64_t n_panels = (n - m_tail >= b) ? (n - m_tail) / b : 0;
     const int64_t kb_end = n_panels * b;
@@ -732,22 +748,21 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
     std::vector<int64_t> cr{0, n};  // chunk row boundaries
     std::vector<int> cov_of;        // per pair: last chunk covered by its side update
     int ring = 3;
-    if (h_src && env_long("MCND_K2_STREAM_IN", 1) != 0 && env_long("MCND_K2_PAIRS", 1) != 0 &&
-        env_long("MCND_K2_OVERLAP", 1) != 0 && env_long("MCND_K2_PRIO", 1) != 0 && env_long("MCND_K2_LA2", 1) != 0 &&
-        n_panels >= 8) {
+    const bool overlap = env_long("MCND_K2_OVERLAP", 1) != 0;  // test hook: 0 = serial schedule (same arithmetic)
+    if (h_src && overlap && n_panels >= 8) {
         cudaPointerAttributes pa{};
         const bool pinned = cudaPointerGetAttributes(&pa, h_src) == cudaSuccess && pa.type == cudaMemoryTypeHost;
         cudaGetLastError();
         // chunk 0 (>= 512 rows) holds the rows pairs 0 and 1 update on the critical stream and in
         // their part A; later parts A touch rows covered two pairs earlier
-        const int64_t min_rows = std::max<int64_t>(512, env_long("MCND_K2_STREAM_ROWS", 1024));
+        const int64_t min_rows = 1024;  // C3 sweep (end to end): 512: 35.2, 768: 34.9, 1024: 34.6, 1536: 34.9 ms
         const int64_t rows_c = (int64_t)align_up((size_t)std::max<int64_t>(min_rows, (n + Buffers::kMaxChunks - 1) / Buffers::kMaxChunks), 128);
         if (pinned && rows_c < n) {
             n_chunks = (int)((n + rows_c - 1) / rows_c);
             cr.assign(1, 0);
             for (int c = 0; c < n_chunks; ++c) cr.push_back(std::min<int64_t>(n, cr.back() + rows_c));
-            std::vector<double> arr(n_chunks);  // expected landing times (MCND_K2_STREAM_GBS, default 60 GB/s: C3 sweep 40: 36.7, 50: 35.9, 56: 35.3, 70: 35.2, 200: 37.1 ms e2e)
-            const double gbs = (double)env_long("MCND_K2_STREAM_GBS", 60) * 1e9;
+            std::vector<double> arr(n_chunks);  // expected landing times at 60 GB/s (C3 sweep 40: 36.7, 50: 35.9, 56: 35.3, 70: 35.2, 200: 37.1 ms e2e)
+            const double gbs = 60e9;
             double t = 0.0;
             for (int c = 0; c < n_chunks; ++c) { t += (double)(cr[c + 1] - cr[c]) * (double)n * 8.0 / gbs; arr[c] = t; }
             auto chunk_of = [&](int64_t row) { return (int)std::min<int64_t>(n_chunks - 1, row / rows_c); };
@@ -930,14 +945,10 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
     // 184: 31.54, 192: 31.50, 224: 31.74 ms): the pivot latency is flat up to ~200 columns
     // (`scripts/micro/kp_bench.cu`), and fewer panel CTAs leave more SMs to the
     // overlapped trailing GEMM
-    const int64_t kp_cols = std::min<int64_t>(256, std::max<int64_t>(64, env_long("MCND_KP_COLS", 176)));
-    const int64_t kp_maxg = std::min<int64_t>(B->sms, env_long("MCND_KP_MAXG", kKPMaxG));  // test knob
+    const int64_t kp_cols = kKPCols;
+    const int64_t kp_maxg = std::min<int64_t>(B->sms, env_long("MCND_KP_MAXG", kKPMaxG));  // test hook: wide chunks
     auto kp_ctas = [&](int64_t m) {  // ~kp_cols columns per CTA, at most 256 unless the SM count caps G
         return std::min<int64_t>({kp_maxg, (int64_t)kKPMaxG, std::max<int64_t>((m + 255) / 256, m / kp_cols)});
-    };
-    auto kp_grid = [&](int64_t m) {
-        int64_t cw = 0;
-        return split(m, kp_ctas(m), &cw);
     };
     auto run_kp = [&](int64_t kb, K2Gather* gp, double* Wout) -> cudaError_t {
         const int64_t m = n - kb;
@@ -965,18 +976,6 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
     // remainder), running while the next panels are factored.  The next pair's critical
     // update waits for part A only.  L, W, Wp and the pair descriptor live in a ring of
     // pair slots so the side GEMM can read pair q's while pairs q+1, q+2 write theirs.
-    const bool pairs = env_long("MCND_K2_PAIRS", 1) != 0;
-    const bool overlap = pairs && env_long("MCND_K2_OVERLAP", 1) != 0;
-    const bool fuse_lc = env_long("MCND_K2_FUSE_LC", 1) != 0;
-    const bool fuse_pp = env_long("MCND_K2_FUSE_PP", 1) != 0;
-    const bool fuse_r1 = env_long("MCND_K2_FUSE_R1", 1) != 0;
-    const int64_t min_budget = env_long("MCND_K2_MIN_BUDGET", B->sms / 4);
-    const bool side_after = env_long("MCND_K2_SIDE_AFTER", 1) != 0;
-    const bool pp_spread = env_long("MCND_K2_PP_SPREAD", 1) != 0;  // pair prep over every CTA of the second panel
-    // depth-2 look-ahead (MCND_K2_LA2=1): each pair's side update is split into part A, the
-    // rows of the unit after next (what the NEXT pair's critical update touches), and part
-    // B, the rest; the next pair waits for part A only, so part B overlaps the next pair too
-    const bool la2 = env_long("MCND_K2_LA2", 1) != 0;
     bool side_pending = false, sideA_pending = false;
     cudaStream_t side = B->side;
     auto join_side = [&]() -> cudaError_t {  // all side work
@@ -1017,7 +1016,7 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
         double* const Wp = Wp2 + (size_t)par * b * b;
         K2Gather* const gpair = gpair2 + par;
         int cov_q = n_chunks - 1;
-        if (streamed && pairs && k + 1 < n_panels) {
+        if (streamed && k + 1 < n_panels) {
             const size_t q = (size_t)(k / 2);
             cov_q = q < cov_of.size() ? cov_of[q] : n_chunks - 1;
         }
@@ -1045,63 +1044,33 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
             return ee;
         };
         const int64_t cov_end = cr[cov_q + 1];  // rows past it are not resident yet
-        if (pairs && k + 1 < n_panels) {
+        if (k + 1 < n_panels) {
             e = run_kp(kb, gp0, Wq);
             mark("kp1");
-            if (!fuse_r1) {
-                if (e == cudaSuccess) e = k2_gather_fix(ws, ld, (int32_t)(kb + b), (int32_t)b, 64, gp0, Lq, abort, st);
-                mark("r1_gather");
-                if (e == cudaSuccess)
-                    e = k2_gemm(ws, ld, (int32_t)(kb + b), (int32_t)b, (int32_t)(m - b), 64, Lq, 64, Wq, ld, wit, abort, st);
-                mark("r1_gemm");
-            } else {  // the second panel kernel applies the first panel to its rows itself
-                kp.r1_g0 = gp0; kp.r1_W = Wq; kp.r1_ldw = ld;
-            }
-            if (fuse_pp) {  // the second panel kernel runs the pair prep in its CTA 0
-                kp.pp_g0 = gp0; kp.pp_W = Wq; kp.pp_ldw = ld; kp.pp_Wp = Wp; kp.pp_gpair = gpair; kp.pp_m = (int32_t)m;
-                kp.pp_bar = pp_spread ? reinterpret_cast<unsigned*>(kp.lastbuf + 64 * 64) + kb / (2 * b) : nullptr;
-            }
+            // the second panel kernel applies the first panel to its own rows in its prologue
+            // and runs the pair prep (spread over its CTAs around one grid barrier)
+            kp.r1_g0 = gp0; kp.r1_W = Wq; kp.r1_ldw = ld;
+            kp.pp_g0 = gp0; kp.pp_W = Wq; kp.pp_ldw = ld; kp.pp_Wp = Wp; kp.pp_gpair = gpair; kp.pp_m = (int32_t)m;
+            kp.pp_bar = reinterpret_cast<unsigned*>(kp.lastbuf + 64 * 64) + kb / (2 * b);
             if (e == cudaSuccess) e = run_kp(kb + b, gp1, Wq + b * ld);
             kp.pp_g0 = nullptr;
             kp.r1_g0 = nullptr;
             mark("kp2");
-            if (e == cudaSuccess && !fuse_pp) e = k2_pair_prep(gp0, gp1, (int32_t)m, Wq, ld, Wp, gpair, abort, st);
-            if (!fuse_pp) mark("pair_prep");
             if (e == cudaSuccess) e = join_rows();  // the critical rows final for the previous pair
             mark("join");
             const int32_t nr = (int32_t)(n - kb - 2 * b);
             // rows the next unit factors: a pair (128), a last single panel (64), or the tail (all)
             const int64_t k2 = k + 2;
+            // (serial schedule, MCND_K2_OVERLAP=0: everything on the critical stream)
             int64_t ahead = (k2 + 1 < n_panels) ? 2 * b : (k2 < n_panels ? b : nr);
-            int64_t budget = 0;
-            if (overlap && ahead < nr && prio) {
-                // priority scheduling: the side GEMM takes whatever SMs the panels leave
-            } else if (overlap && ahead < nr) {
-                // worth it only if the side GEMM on the SMs the next panels leave free
-                // finishes within (next pair's panel work + the full-machine GEMM):
-                // ~20 TF/s DMMA on all SMs, ~0.55 ms of panel work per pair
-                budget = (int64_t)B->sms - kp_grid(n - k2 * b);
-                const double t_full = 2.0 * (double)(nr - ahead) * (double)(m - 2 * b) * 128.0 / 20e12;
-                const double t_side = budget > 0 ? t_full * (double)B->sms / (double)budget : 1e30;
-                if (budget < min_budget || t_side > t_full + 0.55e-3) ahead = nr;
-            } else {
-                ahead = nr;
-            }
+            if (!overlap) ahead = nr;
             // gather + L correction + trailing update of `rows` rows starting at row offset r0
             // (relative to the pair's trailing block) on stream `ss`
             auto trailing = [&](int64_t r0, int64_t rows, cudaStream_t ss, int sm_budget) -> cudaError_t {
                 double* const Lr = Lq + r0 * 2 * b;
-                cudaError_t ee;
-                if (fuse_lc) {  // gather + NL[:, 64:128] += NL[:, 0:64] * (-Wp) in one pass
-                    ee = k2_gather_lcorr(ws, ld, (int32_t)(kb + 2 * b + r0), (int32_t)rows, gpair, Lr, Wp, abort, ss);
-                    if (ss == st) mark("gather_lcorr");
-                } else {
-                    ee = k2_gather_fix(ws, ld, (int32_t)(kb + 2 * b + r0), (int32_t)rows, 128, gpair, Lr, abort, ss);
-                    if (ss == st) mark("gather");
-                    if (ee == cudaSuccess)  // NL[:, 64:128] += NL[:, 0:64] * (-Wp)   (NL = -L; no witness: scratch)
-                        ee = k2_gemm(Lr + b, 2 * b, 0, (int32_t)rows, (int32_t)b, 64, Lr, 2 * b, Wp, b, nullptr, abort, ss);
-                    if (ss == st) mark("lcorr");
-                }
+                // gather + NL[:, 64:128] += NL[:, 0:64] * (-Wp) in one pass, then the DMMA update
+                cudaError_t ee = k2_gather_lcorr(ws, ld, (int32_t)(kb + 2 * b + r0), (int32_t)rows, gpair, Lr, Wp, abort, ss);
+                if (ss == st) mark("gather_lcorr");
                 if (ee == cudaSuccess)
                     ee = k2_gemm(ws, ld, (int32_t)(kb + 2 * b + r0), (int32_t)rows, (int32_t)(m - 2 * b), 128, Lr, 2 * b,
                                  Wq, ld, wit, abort, ss, sm_budget);
@@ -1109,8 +1078,8 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
                 return ee;
             };
             // side stream: W, Wp and the gather descriptor are final once pair prep is done;
-            // started only after the critical rows' update (MCND_K2_SIDE_AFTER=0: right away), so the side
-            // kernels do not take the SMs the critical ones need
+            // started only after the critical rows' update, so the side kernels do not take
+            // the SMs the critical ones need (C3 33.8 -> 33.2 ms)
             if (streamed && cov_q > cov_prev && ahead >= nr) {  // no side work: new rows caught up first
                 if (e == cudaSuccess) e = cudaEventRecord(B->ev_a, st);
                 if (e == cudaSuccess) e = cudaStreamWaitEvent(side, B->ev_a, 0);
@@ -1119,15 +1088,14 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
                 side_pending = (e == cudaSuccess);
                 if (e == cudaSuccess) e = join_side();
             }
-            if (e == cudaSuccess && ahead < nr && !side_after) e = cudaEventRecord(B->ev_a, st);
             if (e == cudaSuccess) e = trailing(0, ahead, st, 0);  // the critical rows first
-            if (e == cudaSuccess && ahead < nr && side_after) e = cudaEventRecord(B->ev_a, st);
+            if (e == cudaSuccess && ahead < nr) e = cudaEventRecord(B->ev_a, st);
             if (e == cudaSuccess && ahead < nr) {
                 e = cudaStreamWaitEvent(side, B->ev_a, 0);
                 // part A: the rows of the unit after next (a pair: 128, a single panel: 64, else
                 // everything left) when the next unit is a pair; the next pair waits for it alone
                 const int64_t k4 = k2 + 2;
-                const int64_t ahead2 = (la2 && k2 + 1 < n_panels && prio)
+                const int64_t ahead2 = (k2 + 1 < n_panels)
                                            ? ((k4 + 1 < n_panels) ? 2 * b : (k4 < n_panels ? b : nr - ahead))
                                            : 0;
                 if (ahead2 > 0 && ahead2 < nr - ahead) {
@@ -1142,14 +1110,13 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
                     n_launch += 2;
                 } else {
                     if (e == cudaSuccess && streamed) e = catch_up();
-                    if (e == cudaSuccess) e = trailing(ahead, std::min<int64_t>(nr, cov_end - (kb + 2 * b)) - ahead, side,
-                                                       prio ? -1 : (int)budget);
+                    if (e == cudaSuccess) e = trailing(ahead, std::min<int64_t>(nr, cov_end - (kb + 2 * b)) - ahead, side, -1);
                 }
                 if (e == cudaSuccess) e = cudaEventRecord(B->ev_b, side);
                 side_pending = (e == cudaSuccess);
                 n_launch += 3;
             }
-            n_launch += (fuse_pp ? 7 : 8) - (fuse_lc ? 1 : 0) - (fuse_r1 ? 2 : 0);  // 2 panels, [gather, update], [prep], gather, [L corr], trailing
+            n_launch += 4;  // 2 panels, gather + L correction, the critical update
             if (streamed) done_pairs.push_back({kb, m, par});
             k += 2;
             par = (par + 1) % kRing;
@@ -1208,6 +1175,7 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
         CUDA_TRY(cudaEventRecord(B->ev_out, st));
         CUDA_TRY(cudaStreamWaitEvent(st_caller, B->ev_out, 0));
     }
+    drain.armed = false;  // every stream is idle: st synchronised, side and cpy joined into it
     float ms = 0.f;
     cudaEventElapsedTime(&ms, B->ev0, B->ev1);
     out->device_ms = ms;
@@ -1392,7 +1360,7 @@ int mg_load(MgHandle* h, const double* src, int64_t lds, cudaStream_t st) {
 
 KPParams mg_kp(MgHandle* h, int64_t lr0, int64_t t, int64_t m, K2Gather* gp, double* W, int64_t ldw) {
     const int64_t b = kK2B;
-    const int64_t cols = std::min<int64_t>(256, std::max<int64_t>(64, env_long("MCND_KP_COLS", 176)));
+    const int64_t cols = kKPCols;
     int64_t G = std::min<int64_t>({(int64_t)h->sms, env_long("MCND_KP_MAXG", kKPMaxG), (int64_t)kKPMaxG,
                                    std::max<int64_t>((m + 255) / 256, m / cols)});
     int64_t cw = 0;
@@ -1444,7 +1412,7 @@ int mg_pair(MgHandle* h, int64_t lr0, int64_t t, int64_t m, double* W, int64_t l
         KPParams kp1 = mg_kp(h, lr0 + b, t + b, m - b, gp1, W + b * ldw, ldw);
         kp1.r1_g0 = gp0; kp1.r1_W = W; kp1.r1_ldw = ldw;  // + the first panel's update of these rows
         kp1.pp_g0 = gp0; kp1.pp_W = W; kp1.pp_ldw = ldw; kp1.pp_Wp = Wp; kp1.pp_gpair = gpair; kp1.pp_m = (int32_t)m;
-        kp1.pp_bar = (env_long("MCND_K2_PP_SPREAD", 1) != 0 && t / (2 * b) < kPPBars)
+        kp1.pp_bar = (t / (2 * b) < kPPBars)
                          ? reinterpret_cast<unsigned*>(h->lastb + 64 * 64) + t / (2 * b) : nullptr;
         e = kp_launch(kp1, st);  // + the pair prep in its CTA 0
     }
@@ -1571,7 +1539,12 @@ int mcnd_logdet_condensation_dev(const double* d_a, int64_t n, int64_t lda, cons
                                  int64_t pivot_sequence_len, uint32_t flags, void* stream, mcnd_logdet* out,
                                  double* pivots_out, int32_t* cols_out) {
     if (!out) return fail(MCND_EINVAL, "null out");
-    std::lock_guard<std::mutex> lk(g_mu);
+    clear_out(out);
+    if (int rc = check_shape(d_a, n, lda)) return rc;  // argument errors before touching a device
+    int code = MCND_OK;
+    Buffers* B = buffers_for_current(&code);
+    if (!B) return code;
+    std::lock_guard<std::mutex> lk(B->mu);
     return serial_dev(d_a, n, lda, pivot_sequence, pivot_sequence_len, flags, (cudaStream_t)stream, out,
                       pivots_out, cols_out);
 }
@@ -1583,10 +1556,10 @@ int mcnd_logdet_condensation(const double* h_a, int64_t n, int64_t lda, const in
     clear_out(out);
     int rc = check_shape(h_a, n, lda);
     if (rc) return rc;
-    std::lock_guard<std::mutex> lk(g_mu);
     int code = MCND_OK;
     Buffers* B = buffers_for_current(&code);
     if (!B) return code;
+    std::lock_guard<std::mutex> lk(B->mu);
     const double* d_a = nullptr;
     rc = stage_input(*B, h_a, n, n, lda, (cudaStream_t)stream, &d_a);
     if (rc) return rc;
@@ -1598,7 +1571,12 @@ int mcnd_mc_parallel_dev(const double* d_a, int64_t n, int64_t lda, int32_t p, u
                          mcnd_logdet* out, mcnd_comm_stats* stats, int64_t* payload_entries,
                          int64_t* row_updates, int32_t* owners_out) {
     if (!out) return fail(MCND_EINVAL, "null out");
-    std::lock_guard<std::mutex> lk(g_mu);
+    clear_out(out);
+    if (int rc = check_shape(d_a, n, lda)) return rc;  // argument errors before touching a device
+    int code = MCND_OK;
+    Buffers* B = buffers_for_current(&code);
+    if (!B) return code;
+    std::lock_guard<std::mutex> lk(B->mu);
     return parallel_dev(d_a, n, lda, p, flags, (cudaStream_t)stream, out, stats, payload_entries, row_updates,
                         owners_out);
 }
@@ -1610,10 +1588,10 @@ int mcnd_mc_parallel(const double* h_a, int64_t n, int64_t lda, int32_t p, uint3
     clear_out(out);
     int rc = check_shape(h_a, n, lda);
     if (rc) return rc;
-    std::lock_guard<std::mutex> lk(g_mu);
     int code = MCND_OK;
     Buffers* B = buffers_for_current(&code);
     if (!B) return code;
+    std::lock_guard<std::mutex> lk(B->mu);
     const double* d_a = nullptr;
     rc = stage_input(*B, h_a, n, n, lda, (cudaStream_t)stream, &d_a);
     if (rc) return rc;
@@ -1627,7 +1605,12 @@ int mcnd_debug_kp_spans(unsigned long long* out, int max_spans) { return mcnd::k
 int mcnd_logdet_blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, void* stream,
                             mcnd_logdet* out, double* pivots_out, int32_t* cols_out) {
     if (!out) return fail(MCND_EINVAL, "null out");
-    std::lock_guard<std::mutex> lk(g_mu);
+    clear_out(out);
+    if (int rc = check_shape(d_a, n, lda)) return rc;  // argument errors before touching a device
+    int code = MCND_OK;
+    Buffers* B = buffers_for_current(&code);
+    if (!B) return code;
+    std::lock_guard<std::mutex> lk(B->mu);
     return blocked_dev(d_a, n, lda, flags, (cudaStream_t)stream, out, pivots_out, cols_out);
 }
 
@@ -1637,10 +1620,10 @@ int mcnd_logdet_blocked(const double* h_a, int64_t n, int64_t lda, uint32_t flag
     clear_out(out);
     int rc = check_shape(h_a, n, lda);
     if (rc) return rc;
-    std::lock_guard<std::mutex> lk(g_mu);
     int code = MCND_OK;
     Buffers* B = buffers_for_current(&code);
     if (!B) return code;
+    std::lock_guard<std::mutex> lk(B->mu);
     // staged inside: streamed by row chunks when h_a is pinned (overlaps the first pairs)
     return blocked_dev(nullptr, n, lda, flags, (cudaStream_t)stream, out, pivots_out, cols_out, h_a);
 }
@@ -1785,10 +1768,10 @@ int mcnd_logdet_batched(const double* h_a, int64_t batch, int64_t n, int64_t str
     if (batch < 0 || n < 1 || n > 128) return fail(MCND_EINVAL, "batched kernel needs 1 <= n <= 128 (got %lld)", (long long)n);
     if (stride < n * n) return fail(MCND_EINVAL, "stride < n*n");
     if (batch == 0) return MCND_OK;
-    std::lock_guard<std::mutex> lk(g_mu);
     int code = MCND_OK;
     Buffers* B = buffers_for_current(&code);
     if (!B) return code;
+    std::lock_guard<std::mutex> lk(B->mu);
     cudaStream_t st = (cudaStream_t)stream;
     const size_t in_bytes = (size_t)batch * stride * sizeof(double);
     const size_t o_sign = align_up((size_t)batch * sizeof(double), 256);
@@ -1831,6 +1814,7 @@ void mcnd_release_workspace(void) {
     int cur = 0;
     cudaGetDevice(&cur);
     for (auto& b : g_bufs) {
+        std::lock_guard<std::mutex> lb(b.mu);  // (must not race a call on that device)
         cudaSetDevice(b.device);
         if (b.dws) cudaFree(b.dws);
         if (b.din) cudaFree(b.din);

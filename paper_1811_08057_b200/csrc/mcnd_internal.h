@@ -133,6 +133,10 @@ constexpr int kKPMaxG = 160;
 // lastbuf allocation: the LAST records [64][64], then the pair-prep barrier counters
 constexpr int kPPBars = 1024;  // pairs per call (n <= 131072)
 constexpr size_t kLastBufBytes = (size_t)64 * 64 * 16 + (size_t)kPPBars * sizeof(unsigned);
+// ~176 columns per panel CTA (C3 sweep with the 4-warp GEMM: 128: 31.26, 160: 31.19, 176: 31.03,
+// 184: 31.54, 192: 31.50, 224: 31.74 ms): the pivot latency is flat up to ~200 columns and fewer
+// panel CTAs leave more SMs to the overlapped trailing GEMM
+constexpr int kKPCols = 176;
 constexpr int kKPMaxCw = 380;  // columns per panel CTA (64 x 380 doubles = 190 KB of shared memory)
 cudaError_t kp_launch(const KPParams& p, cudaStream_t s);
 size_t kp_smem_bytes(int cw);
@@ -147,11 +151,6 @@ cudaError_t k2_gather_fix(double* ws, int64_t ld, int32_t rbase, int32_t nrows, 
 // Pair gather (K = 128) fused with the L correction NL[:, 64:128] += NL[:, 0:64] * Wp.
 cudaError_t k2_gather_lcorr(double* ws, int64_t ld, int32_t rbase, int32_t nrows, const K2Gather* gp, double* L,
                             const double* Wp, const unsigned* abort, cudaStream_t s);
-// Panel pair (two 64-row panels, one rank-128 trailing update): from the two panels'
-// descriptors build the composite gather descriptor, Wp[s][s'] = W0[s][P1[s']] and
-// permute W0's columns into the final layout of the pair (one CTA).
-cudaError_t k2_pair_prep(const K2Gather* g0, const K2Gather* g1, int32_t m, double* Wc, int64_t ldw, double* Wp,
-                         K2Gather* gpair, const unsigned* abort, cudaStream_t s);
 
 // C[M x N2] (rows rbase.. of ws) += NL[M x K] W[K x N2], K in {64, 128}; NL (= -L, as written by
 // k2_gather_fix) row stride ldl;

@@ -125,99 +125,3 @@ def write_records(records, path) -> None:
             w.writerow([r.algorithm, r.n, r.p, r.run_index, repr(r.total_seconds), repr(r.scatter_seconds),
                         repr(r.comm_seconds), r.sign, repr(r.log_abs)])
 
-
-# ---- the reference's report over benchmark CSVs (bench.py:130-258), restated so the
-# CLI's `report` works on GPU sweeps without the reference installed ----
-class ReportError(ValueError):
-    """Malformed benchmark CSV (bench.py:ReportError)."""
-
-
-def read_records(path) -> list:
-    """bench.py:130-160: header must match CSV_HEADER; per-line field count and types."""
-    records = []
-    with open(path, newline="") as f:
-        reader = csv.reader(f)
-        try:
-            header = next(reader)
-        except StopIteration:
-            raise ReportError("empty CSV") from None
-        if header != CSV_HEADER:
-            raise ReportError(f"line 1: bad header {header!r}")
-        for line_no, row in enumerate(reader, 2):
-            if not row:
-                continue
-            if len(row) != len(CSV_HEADER):
-                raise ReportError(f"line {line_no}: expected {len(CSV_HEADER)} fields, got {len(row)}")
-            try:
-                records.append(BenchRecord(row[0], int(row[1]), int(row[2]), int(row[3]), float(row[4]),
-                                           float(row[5]), float(row[6]), int(row[7]), float(row[8])))
-            except ValueError as exc:
-                raise ReportError(f"line {line_no}: {exc}") from exc
-    return records
-
-
-def _mean(values) -> float:
-    values = list(values)
-    return sum(values) / len(values)
-
-
-def mean_totals(records) -> dict:
-    """bench.py:168-173: mean total seconds per (algorithm, n, p)."""
-    groups = {}
-    for r in records:
-        groups.setdefault((r.algorithm, r.n, r.p), []).append(r.total_seconds)
-    return {k: _mean(v) for k, v in groups.items()}
-
-
-def serial_reference_times(records) -> dict:
-    """bench.py:176-183: per size, the fastest single-worker mean across algorithms (T_s)."""
-    out = {}
-    for (_alg, n, p), t in mean_totals(records).items():
-        if p == 1 and (n not in out or t < out[n]):
-            out[n] = t
-    return out
-
-
-def speedup_table(records) -> dict:
-    """bench.py:186-193: T_s / T_p per (algorithm, n, p)."""
-    t_serial = serial_reference_times(records)
-    return {(alg, n, p): t_serial[n] / t for (alg, n, p), t in mean_totals(records).items()
-            if n in t_serial and t > 0}
-
-
-def average_speedups(records) -> dict:
-    """bench.py:196-203: mean of the per-size speedups per (algorithm, p)."""
-    groups = {}
-    for (alg, _n, p), s in speedup_table(records).items():
-        groups.setdefault((alg, p), []).append(s)
-    return {k: _mean(v) for k, v in groups.items()}
-
-
-def comm_summary(records) -> dict:
-    """bench.py:206-218: mean (scatter_s, comm_s) per (algorithm, p)."""
-    groups = {}
-    for r in records:
-        groups.setdefault((r.algorithm, r.p), []).append((r.scatter_seconds, r.comm_seconds))
-    return {k: (_mean(s for s, _ in v), _mean(c for _, c in v)) for k, v in groups.items()}
-
-
-def format_report(records) -> str:
-    """bench.py:221-258: the same deterministic text report."""
-    if not records:
-        raise ReportError("no records to report")
-    table, t_serial, means = speedup_table(records), serial_reference_times(records), mean_totals(records)
-    lines = ["== Speedup per size (T_s / T_p; T_s = fastest 1-worker mean) ==",
-             f"{'algorithm':<12} {'n':>6} {'p':>4} {'mean_total_s':>14} {'speedup':>10}"]
-    for (alg, n, p) in sorted(means, key=lambda k: (k[1], k[0], k[2])):
-        lines.append(f"{alg:<12} {n:>6} {p:>4} {means[(alg, n, p)]:>14.6f} {table.get((alg, n, p), math.nan):>10.4f}")
-    lines += ["", "== Average speedup across sizes ==", f"{'algorithm':<12} {'p':>4} {'avg_speedup':>12}"]
-    avgs = average_speedups(records)
-    for (alg, p) in sorted(avgs):
-        lines.append(f"{alg:<12} {p:>4} {avgs[(alg, p)]:>12.4f}")
-    lines += ["", "== Scatter / communication averages ==", f"{'algorithm':<12} {'p':>4} {'avg_scatter_s':>14} {'avg_comm_s':>12}"]
-    comms = comm_summary(records)
-    for (alg, p) in sorted(comms):
-        sc, cm = comms[(alg, p)]
-        lines.append(f"{alg:<12} {p:>4} {sc:>14.6f} {cm:>12.6f}")
-    lines += ["", "reference serial times: " + ", ".join(f"n={n}: {t_serial[n]:.6f}s" for n in sorted(t_serial))]
-    return "\n".join(lines) + "\n"

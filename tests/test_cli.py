@@ -1,9 +1,9 @@
 """CLI parity with the reference's front end (cli.py; mcnd/cli.py:55-191, SURVEY.md §8(f)
 rank 4): subcommands, exit codes (0 / 1 usage / 2 I/O), messages, the logdet output line,
-CSV matrix I/O (matrix.py:154-180) and the report (bench.py:130-258).  CPU tests cover the
-parser, I/O and report paths; the GPU tests run logdet and a tiny sweep on the device."""
+CSV matrix I/O (matrix.py:154-180) and the sweep CSV (the reference's own report reads it:
+tests/test_registry_records.py).  CPU tests cover the parser and I/O paths; the GPU tests
+run logdet and a tiny sweep on the device."""
 
-import math
 import os
 import re
 import sys
@@ -76,41 +76,6 @@ def test_csv_matrix_round_trip_and_errors(tmp_path):
         mio.read_matrix_csv(tmp_path / "t.csv")
 
 
-def _records():
-    return [R.BenchRecord("mc-gpu", 64, 1, 0, 0.002, 0.0003, 0.0, -1, 12.5),
-            R.BenchRecord("mc-gpu", 64, 1, 1, 0.004, 0.0003, 0.0, -1, 12.5),
-            R.BenchRecord("mc-gpu-parallel", 64, 2, 0, 0.0015, 0.0003, 0.0, -1, 12.5),
-            R.BenchRecord("mc-gpu-parallel", 128, 2, 0, 0.003, 0.0004, 0.0, 1, 40.0),
-            R.BenchRecord("mc-gpu-blocked", 128, 1, 0, 0.006, 0.0004, 0.0, 1, 40.0)]
-
-
-def test_report_cli_and_errors(tmp_path, capsys):
-    p = tmp_path / "r.csv"
-    R.write_records(_records(), p)
-    rc, out, _ = run(["report", str(p)], capsys)
-    assert rc == 0 and out == R.format_report(_records())
-    # speedup T_s / T_p with T_s the fastest single-worker mean (bench.py:176-193)
-    assert math.isclose(R.speedup_table(_records())[("mc-gpu-parallel", 64, 2)], 0.003 / 0.0015)
-    (tmp_path / "h.csv").write_text("a,b\n")
-    rc, _, err = run(["report", str(tmp_path / "h.csv")], capsys)
-    assert rc == 2 and "bad header" in err
-    rc, _, err = run(["report", str(tmp_path / "none.csv")], capsys)
-    assert rc == 2 and err.startswith("cannot read ")
-
-
-@pytest.mark.skipif(not os.path.isdir(REF_SRC), reason="reference not mounted")
-def test_report_matches_reference(tmp_path):
-    """The restated report is the reference's own text on the same records."""
-    sys.path.insert(0, REF_SRC)
-    try:
-        from mcnd import bench as ref_bench
-    finally:
-        sys.path.remove(REF_SRC)
-    p = tmp_path / "r.csv"
-    R.write_records(_records(), p)
-    assert R.format_report(R.read_records(p)) == ref_bench.format_report(ref_bench.read_records(p))
-
-
 @pytest.mark.skipif(not os.path.isdir(REF_SRC), reason="reference not mounted")
 def test_csv_reader_matches_reference(tmp_path):
     sys.path.insert(0, REF_SRC)
@@ -148,11 +113,13 @@ def test_logdet_cli_on_gpu(tmp_path, capsys):
 
 
 @pytest.mark.gpu
-def test_bench_and_report_cli_on_gpu(tmp_path, capsys):
+def test_bench_cli_on_gpu(tmp_path, capsys):
+    import csv
+
     p = tmp_path / "b.csv"
     rc, out, _ = run(["bench", "--sizes", "32,48", "--workers", "1,2", "--repeats", "2", "--out", str(p)], capsys)
     assert rc == 0 and out.startswith("wrote ")
-    recs = R.read_records(p)
-    assert {r.algorithm for r in recs} >= {"mc-gpu", "mc-gpu-parallel", "mc-gpu-blocked"}
-    rc, out, _ = run(["report", str(p)], capsys)
-    assert rc == 0 and "== Speedup per size" in out
+    with open(p) as f:
+        rows = list(csv.reader(f))
+    assert rows[0] == R.CSV_HEADER
+    assert {r[0] for r in rows[1:]} >= {"mc-gpu", "mc-gpu-parallel", "mc-gpu-blocked"}
