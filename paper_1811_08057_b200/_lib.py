@@ -52,6 +52,7 @@ EXPORTS = (
     "mcnd_logdet_blocked_dev", "mcnd_logdet_blocked", "mcnd_blocked_panel",
     "mcnd_mg_create", "mcnd_mg_load", "mcnd_mg_pair", "mcnd_mg_trailing", "mcnd_mg_export", "mcnd_mg_tail",
     "mcnd_mg_records", "mcnd_mg_gather_bytes", "mcnd_mg_ld", "mcnd_mg_destroy",
+    "mcnd_nccl_id_bytes", "mcnd_nccl_unique_id", "mcnd_mg_attach", "mcnd_mg_logdet", "mcnd_mg_schedule",
 )
 
 
@@ -114,6 +115,16 @@ def load(path: str | None = None):
             f = getattr(lib, name)
             f.argtypes = args
             f.restype = ctypes.c_int
+        lib.mcnd_nccl_id_bytes.argtypes = []
+        lib.mcnd_nccl_id_bytes.restype = ctypes.c_int32
+        lib.mcnd_nccl_unique_id.argtypes = [P]
+        lib.mcnd_nccl_unique_id.restype = ctypes.c_int
+        lib.mcnd_mg_attach.argtypes = [P, i32, i32, P, i32]
+        lib.mcnd_mg_attach.restype = ctypes.c_int
+        lib.mcnd_mg_logdet.argtypes = [P, P, i64, P, LD]
+        lib.mcnd_mg_logdet.restype = ctypes.c_int
+        lib.mcnd_mg_schedule.argtypes = [i64, i32, i64, P, i64]
+        lib.mcnd_mg_schedule.restype = ctypes.c_int64
         lib.mcnd_mg_gather_bytes.argtypes = []
         lib.mcnd_mg_gather_bytes.restype = ctypes.c_int64
         lib.mcnd_mg_ld.argtypes = [P]

@@ -184,7 +184,7 @@ class BlockedGroup:
     Kernels = the single-GPU K2 kernels ("one broadcast per panel
     of W").  Same result type as logdet_condensation; parity by tolerance."""
 
-    def __init__(self, n: int, group=None, tail: int | None = None):
+    def __init__(self, n: int, group=None, tail: int | None = None, native: bool | None = None):
         import torch
         import torch.distributed as dist
 
@@ -216,6 +216,23 @@ class BlockedGroup:
         self.side = self.crit if os.environ.get("MCND_MG_SERIAL", "0") == "1" else torch.cuda.Stream(priority=0)
         self.last_device_ms = 0.0
         self.last_launches = 0
+        # the native driver (mcnd_mg_logdet: the per-pair loop in C++, NCCL on the library's own
+        # communicator) whenever the group is NCCL or a single rank; the Python loop below stays
+        # for gloo groups (host-staged broadcasts: the CPU / shared-GPU tests)
+        self.native = (self.nccl or self.world == 1) if native is None else bool(native)
+        if self.native:
+            idb = int(lib.mcnd_nccl_id_bytes())
+            uid = bytes(idb)
+            need = self.world > 1 or self.force_comm
+            if need and self.rank == 0:
+                buf = ctypes.create_string_buffer(idb)
+                _lib.check(lib.mcnd_nccl_unique_id(buf))
+                uid = buf.raw
+            if need and self.world > 1:
+                box = [uid]
+                dist.broadcast_object_list(box, src=0, group=self.group)
+                uid = box[0]
+            _lib.check(lib.mcnd_mg_attach(h, self.world, self.rank, uid if need else None, 1 if need else 0))
 
     def _bcast(self, t, src):
         if self.world == 1:
@@ -249,6 +266,13 @@ class BlockedGroup:
             raise ValueError(f"rank {rank} expects its block of shape {(self.rows, n)}, got {tuple(rows.shape)}")
         if rows.dtype != torch.float64 or rows.stride(1) != 1:
             rows = rows.to(torch.float64).contiguous()
+        if self.native:
+            out = _lib.McndLogDet()
+            _lib.check(lib.mcnd_mg_logdet(h, rows.data_ptr(), rows.stride(0), torch.cuda.current_stream().cuda_stream,
+                                          ctypes.byref(out)))
+            self.last_device_ms = float(out.device_ms)
+            self.last_launches = int(out.launches)
+            return SINGULAR if out.singular else LogDet(int(out.sign), float(out.log_abs))
         cur = torch.cuda.current_stream()
         crit, side = self.crit, self.side
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -155,3 +155,20 @@ def test_blocked_pivot_sequence_oracle_consistent():
         got = O.logdet_condensation(a, pivot_sequence=seq)
         assert got.sign == ref.sign
         assert abs(got.log_abs - ref.log_abs) <= max(1e-8 * 600, 1e-10 * abs(ref.log_abs))
+
+
+def test_native_schedule_matches_python():
+    """The C++ pair schedule of the native driver (mcnd_mg_schedule) is dist.blocked_schedule."""
+    import ctypes
+
+    from paper_1811_08057_b200 import _lib
+    from paper_1811_08057_b200 import dist as D
+
+    lib = _lib.load()
+    for n, world, tail in [(300, 1, 2), (1000, 2, 64), (4000, 2, 64), (8000, 8, 64), (8001, 3, 100),
+                           (10007, 5, 256), (32768, 8, 64), (129, 2, 2), (1100, 4, 256)]:
+        pairs, _, _, _ = D.blocked_schedule(n, world, tail)
+        buf = np.zeros((max(len(pairs), 1), 5), dtype=np.int64)
+        k = lib.mcnd_mg_schedule(n, world, tail, buf.ctypes.data, buf.shape[0])
+        assert k == len(pairs)
+        assert [tuple(int(x) for x in r) for r in buf[:k]] == [tuple(p) for p in pairs]
