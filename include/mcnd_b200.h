@@ -105,6 +105,16 @@ int mcnd_logdet_blocked(const double* h_a, int64_t n, int64_t lda, uint32_t flag
                         mcnd_logdet* out, double* pivots_out, int32_t* cols_out);
 int32_t mcnd_blocked_panel(void);
 
+/* ---- Gaussian elimination with row pivoting: replaces mcnd.logdet_lu (gauss.py:34-68), the
+ * paper's comparison baseline.  Bitwise the reference's pivots and log|det| (K1 run on A^T).
+ * row_witness: optional n per-row bounds (DEVICE for _dev, HOST otherwise; NULL = only an exactly
+ * zero pivot is singular).  pivots_out / rows_out: optional HOST arrays of n entries: each
+ * step's pivot value and ORIGINAL pivot row (ge_parallel's owners and accounting, runtime.py:232). */
+int mcnd_logdet_lu_dev(const double* d_a, int64_t n, int64_t lda, const double* d_row_witness, uint32_t flags,
+                       void* stream, mcnd_logdet* out, double* pivots_out, int32_t* rows_out);
+int mcnd_logdet_lu(const double* h_a, int64_t n, int64_t lda, const double* h_row_witness, uint32_t flags,
+                   void* stream, mcnd_logdet* out, double* pivots_out, int32_t* rows_out);
+
 /* Fold per-step pivots and the p x p remainder of the block-row driver into the
  * reference's result and accounting (runtime.py:185-229): sign parity, per-worker
  * log sums reduced in rank order, row-pivoted LU tail (gauss.py:34-68).

@@ -11,6 +11,7 @@ Everything below the Python surface is sm_100a CUDA behind a C ABI
 
 from .batched import logdet_batched
 from .condense import SINGULAR, SINGULAR_RTOL, LogDet, SingularRowError, logdet_blocked, logdet_condensation
+from .gauss import ge_parallel, logdet_lu
 from .io import FormatError, read_matrix, read_matrix_device, write_matrix
 from .matrix import GENERATOR_KINDS, MatrixSpec, as_matrix, generate, require_square
 from .registry import ALGORITHMS, run_algorithm
@@ -25,6 +26,8 @@ __all__ = [
     "logdet_blocked",
     "logdet_batched",
     "mc_parallel",
+    "logdet_lu",
+    "ge_parallel",
     "plan_blocks",
     "WorkerPlan",
     "CommStats",

@@ -53,6 +53,7 @@ EXPORTS = (
     "mcnd_mg_create", "mcnd_mg_load", "mcnd_mg_pair", "mcnd_mg_trailing", "mcnd_mg_export", "mcnd_mg_tail",
     "mcnd_mg_records", "mcnd_mg_gather_bytes", "mcnd_mg_ld", "mcnd_mg_destroy",
     "mcnd_nccl_id_bytes", "mcnd_nccl_unique_id", "mcnd_mg_attach", "mcnd_mg_logdet", "mcnd_mg_schedule",
+    "mcnd_logdet_lu_dev", "mcnd_logdet_lu",
 )
 
 
@@ -100,6 +101,10 @@ def load(path: str | None = None):
             f.argtypes = [P, i64, i64, u32, P, LD, P, P]
             f.restype = ctypes.c_int
         lib.mcnd_blocked_panel.restype = ctypes.c_int32
+        for name in ("mcnd_logdet_lu_dev", "mcnd_logdet_lu"):
+            f = getattr(lib, name)
+            f.argtypes = [P, i64, i64, P, u32, P, LD, P, P]
+            f.restype = ctypes.c_int
         VP = ctypes.POINTER(ctypes.c_void_p)
         sigs = {
             "mcnd_mg_create": [i64, i64, VP],

@@ -71,6 +71,10 @@ __device__ __forceinline__ double upd(double x, double mult, double p) {
     return __dsub_rn(x, __dmul_rn(mult, p));
 }
 
+// GE mode breaks ties by the original row id of the column (gauss.py:49-52 takes the first
+// maximum in the original row order), condensation by the column position (condense.py:88).
+__device__ __forceinline__ int tie_key(const K1Params& p, int c) { return p.ge_ids ? __ldcg(p.ge_ids + c) : c; }
+
 // (value, column) argmax order: larger |value| wins, ties -> lower column.
 __device__ __forceinline__ bool beats(double av, int ai, double bv, int bi) {
     double fa = fabs(av), fb = fabs(bv);
@@ -93,6 +97,7 @@ struct Smem {
     double red_w[kWarps + 1];
     int red_i[kWarps + 1];
     int step_l;
+    int win_pos;  // GE mode: column position of the winning (value, original id)
 };
 
 // Whole-CTA reduction of (argmax value, column) and witness max.  Every thread
@@ -140,7 +145,9 @@ __device__ __forceinline__ void cta_reduce(Smem& sm, double& v, int& i, double& 
 // touches those slots), then the record, then the release flag.  Whole CTA.
 __device__ void publish(const K1Params& p, Smem& sm, int g, int row, int t, int m_pub, double v, int l,
                         double wit) {
-    const bool singular = !(fabs(v) > kSingularRtol * wit);  // condense.py:90
+    // condense.py:90; GE mode: gauss.py:55-58 (exact zero, or the caller's row witness)
+    const bool singular = p.ge_ids ? (v == 0.0 || (p.ge_rowwit && fabs(v) <= kSingularRtol * p.ge_rowwit[p.ge_ids[l]]))
+                                   : !(fabs(v) > kSingularRtol * wit);
     const int wp = m_pub - 1;
     const bool sys = p.sys_scope != 0;
     double* own = p.ws[g] + (int64_t)row * p.ld;
@@ -154,9 +161,14 @@ __device__ void publish(const K1Params& p, Smem& sm, int g, int row, int t, int 
     if (sys) __threadfence_system();
     __syncthreads();
     if (threadIdx.x == 0) {
+        // GE mode: the exchange l <- m-1 moves that column's row id too (ordered before the
+        // flag release, so the next publisher sees the new layout)
+        if (p.ge_ids && wp > 0 && l != wp) p.ge_ids[l] = p.ge_ids[wp];
         for (int h = 0; h < p.n_groups; ++h) {
             p.rec[h][t].v = v;
-            p.rec[h][t].l = singular ? -1 : l;
+            // singular: -1 (condensation); GE mode keeps the position as -(l + 2) (its pivot row
+            // is reported, as gauss.py's loop reached it)
+            p.rec[h][t].l = singular ? (p.ge_ids ? -(l + 2) : -1) : l;
         }
         // single GPU: the gpu-scope release is cumulative over the CTA's row stores
         // (ordered before it by the barrier), no separate fence needed
@@ -239,11 +251,20 @@ __global__ void __launch_bounds__(kThreads, 1) k1_condense(const K1Params p) {
         double* rowp = ws + (int64_t)sm.rows[0] * p.ld;
         double bv = 0.0, bw = 0.0;
         int bi = INT_MAX;
+        int bp = INT_MAX;  // position of the local best (GE: bi is its original id)
         for (int c = tid; c < ncol0; c += kThreads) {
             const double x = rowp[c];
-            if (beats(x, c, bv, bi)) { bv = x; bi = c; }
+            const int key = tie_key(p, c);
+            if (beats(x, key, bv, bi)) { bv = x; bi = key; bp = c; }
         }
+        const int lbi = bi;
+        const double lbv = bv;
         cta_reduce(sm, bv, bi, bw);
+        if (p.ge_ids) {  // the one thread holding the winner knows its position
+            if (lbi == bi && abs_bits(lbv) == abs_bits(bv)) sm.win_pos = bp;
+            __syncthreads();
+            bi = sm.win_pos;
+        }
         publish(p, sm, g, sm.rows[0], 0, ncol0, bv, bi, __longlong_as_double((long long)sm.wit[0]));
     }
 
@@ -294,7 +315,7 @@ __global__ void __launch_bounds__(kThreads, 1) k1_condense(const K1Params p) {
             const double mult = sm.mult[start], lastv = sm.last[start];
             const int npairs = (w + 1) >> 1;
             double bv = 0.0, bw = 0.0;
-            int bi = INT_MAX;
+            int bi = INT_MAX, bp = INT_MAX;  // GE mode: bi = original id, bp = its position
             for (int pj = tid; pj < npairs; pj += kThreads) {
                 const int c = 2 * pj;
                 double2 x = *reinterpret_cast<const double2*>(rowp + c);
@@ -307,14 +328,23 @@ __global__ void __launch_bounds__(kThreads, 1) k1_condense(const K1Params p) {
                 y.x = upd<kFast>(x.x, mult, p0);
                 y.y = upd<kFast>(x.y, mult, p1);
                 *reinterpret_cast<double2*>(rowp + c) = y;
-                if (beats(y.x, c, bv, bi)) { bv = y.x; bi = c; }
+                const int k0 = tie_key(p, c);
+                if (beats(y.x, k0, bv, bi)) { bv = y.x; bi = k0; bp = c; }
                 bw = fmax(bw, fabs(y.x));
                 if (c + 1 < w) {
-                    if (beats(y.y, c + 1, bv, bi)) { bv = y.y; bi = c + 1; }
+                    const int k1 = tie_key(p, c + 1);
+                    if (beats(y.y, k1, bv, bi)) { bv = y.y; bi = k1; bp = c + 1; }
                     bw = fmax(bw, fabs(y.y));
                 }
             }
+            const int lbi = bi;
+            const double lbv = bv;
             cta_reduce(sm, bv, bi, bw);
+            if (p.ge_ids) {
+                if (lbi == bi && abs_bits(lbv) == abs_bits(bv)) sm.win_pos = bp;
+                __syncthreads();
+                bi = sm.win_pos;
+            }
             const double wit = fmax(__longlong_as_double((long long)sm.wit[start]), bw);
             publish(p, sm, g, sm.rows[start], s + 1, w, bv, bi, wit);
             if (tid == 0) sm.wit[start] = (unsigned long long)__double_as_longlong(wit);
@@ -374,7 +404,35 @@ __global__ void __launch_bounds__(kThreads, 1) k1_condense(const K1Params p) {
         p.row_wit[gl][sm.rows[i]] = __longlong_as_double((long long)sm.wit[i]);
 }
 
+// out[c][r] = a[r][c] (n x n, out row stride ldo): 32 x 32 tiles through shared memory,
+// coalesced on both sides.  The GE mode runs K1 on the transpose (gauss.py's column pivots
+// become K1's row pivots; the arithmetic is the same, see mcnd_logdet_lu).
+__global__ void __launch_bounds__(256) transpose_kernel(const double* __restrict__ a, int64_t n, int64_t lda,
+                                                        double* __restrict__ out, int64_t ldo) {
+    __shared__ double t[32][33];
+    const int64_t r0 = (int64_t)blockIdx.y * 32, c0 = (int64_t)blockIdx.x * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+#pragma unroll
+    for (int k = 0; k < 32; k += 8) {
+        const int64_t r = r0 + ty + k, c = c0 + tx;
+        if (r < n && c < n) t[ty + k][tx] = a[r * lda + c];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 32; k += 8) {
+        const int64_t r = c0 + ty + k, c = r0 + tx;  // out row = a column
+        if (r < n && c < n) out[r * ldo + c] = t[tx][ty + k];
+    }
+}
+
 }  // namespace
+
+cudaError_t transpose_launch(const double* a, int64_t n, int64_t lda, double* out, int64_t ldo, cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    const unsigned nb = (unsigned)((n + 31) / 32);
+    transpose_kernel<<<dim3(nb, nb), 256, 0, s>>>(a, n, lda, out, ldo);
+    return cudaGetLastError();
+}
 
 size_t k1_smem_bytes(int chunk) { return (size_t)(chunk + 2) * sizeof(double); }
 

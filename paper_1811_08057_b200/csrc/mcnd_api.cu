@@ -65,6 +65,7 @@ struct Buffers {
     void* dws = nullptr;   size_t dws_bytes = 0;    // condensation workspace(s) + records + metadata
     void* din = nullptr;   size_t din_bytes = 0;    // H2D staging for host-input calls
     void* hpin = nullptr;  size_t hpin_bytes = 0;   // pinned metadata / result staging
+    void* dge = nullptr;   size_t dge_bytes = 0;    // GE: transposed matrix, row ids, witness
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     cudaStream_t side = nullptr;                 // K2: trailing updates overlapped with the next panels (lowest priority)
     cudaStream_t crit = nullptr;                 // K2: the panel chain (highest priority)
@@ -247,6 +248,8 @@ struct K1Launch {
     size_t meta_bytes = 0;
     unsigned long long timeout_ns = 20ull * 1000000000ull;
     bool reset_records = true;
+    int32_t* ge_ids = nullptr;            // GE mode (K1Params::ge_ids)
+    const double* ge_rowwit = nullptr;
 };
 
 size_t meta_bytes_for(int64_t n, int64_t npv, int64_t ctas) {
@@ -320,6 +323,8 @@ int k1_execute(Buffers& B, K1Launch& L, bool fast, cudaStream_t st, K1Run& run) 
     p.wit_in = nullptr;
     p.abort_flag = nullptr;
     p.pstep_offset = 0;
+    p.ge_ids = L.ge_ids;
+    p.ge_rowwit = L.ge_rowwit;
 
     CUDA_TRY(cudaEventRecord(B.ev0, st));
     cudaError_t e = k1_launch(p, fast, st);
@@ -359,7 +364,8 @@ int k1_execute(Buffers& B, K1Launch& L, bool fast, cudaStream_t st, K1Run& run) 
 // CTA groups with separate workspaces, exercising the multi-GPU push protocol).
 int k1_run_local(Buffers& B, const double* d_a, int64_t n, int64_t lda, bool fast, cudaStream_t st,
                  K1Run& run, const Blocks* groups, const std::vector<int32_t>* keep_rows, int64_t keep_cols,
-                 std::vector<double>* keep_out, std::vector<double>* keep_wit) {
+                 std::vector<double>* keep_out, std::vector<double>* keep_wit, int32_t* ge_ids = nullptr,
+                 const double* ge_rowwit = nullptr) {
     const int32_t P = groups ? (int32_t)groups->start.size() : 1;
     if (P > kMaxGroups) return fail(MCND_EINVAL, "at most %d CTA groups", kMaxGroups);
     const int64_t npv = std::max<int64_t>((int64_t)run.seq.size(), 1);
@@ -393,6 +399,8 @@ int k1_run_local(Buffers& B, const double* d_a, int64_t n, int64_t lda, bool fas
         for (int64_t r = 0; r < n; ++r) L.row_group[(size_t)r] = groups->group_of(r);
     L.d_meta = base + (size_t)P * GL.bytes;
     L.meta_bytes = mb;
+    L.ge_ids = ge_ids;
+    L.ge_rowwit = ge_rowwit;
     rc = k1_execute(B, L, fast, st, run);
     if (rc) return rc;
     if (keep_rows && keep_out) {
@@ -570,6 +578,80 @@ int serial_dev(const double* d_a, int64_t n, int64_t lda, const int64_t* seq_in,
     out->sign = sign_acc * (vf > 0 ? 1 : -1);
     out->log_abs = log_acc + std::log(std::fabs(vf));
     out->steps = n - 1;
+    return MCND_OK;
+}
+
+// ---- Gaussian elimination with row pivoting: logdet_lu (gauss.py:34-68) on the GPU ----
+// K1 in GE mode on A^T.  Column k of A is row k of A^T; gauss.py's pivot (max |a[r, k]| over
+// the unprocessed rows r, ties -> lowest r) is K1's argmax over that row with ties broken by
+// the original row id; its update a[r, j] -= (a[r, k] / piv) * a[p, j] is, transposed, K1's
+// b[j, c] -= b[j, l] * (b[k, c] / v) with the same three roundings (the product commutes).  So
+// the pivots are bitwise gauss.py's and so is log|det| (summed in pivot order); the sign is
+// prod sgn(piv) x parity(pivot rows) (gauss.py:16-31, 64-68).  Singular: an exactly zero
+// pivot, or |piv| <= 1e-12 x row_witness[pivot row] when the caller passes one (gauss.py:55-58).
+int ge_dev(const double* d_a, int64_t n, int64_t lda, const double* d_rowwit, uint32_t flags, cudaStream_t st,
+           mcnd_logdet* out, double* pivots_out, int32_t* rows_out, const double* h_rowwit = nullptr) {
+    clear_out(out);
+    int rc = check_shape(d_a, n, lda);
+    if (rc) return rc;
+    int code = MCND_OK;
+    Buffers* B = buffers_for_current(&code);
+    if (!B) return code;
+    // transposed matrix + row ids (+ the witness), in the library's GE scratch area
+    const size_t o_t = 0, o_ids = align_up((size_t)n * n * sizeof(double), 256);
+    const size_t o_w = o_ids + align_up((size_t)n * sizeof(int32_t), 256);
+    rc = ensure_dev(&B->dge, &B->dge_bytes, o_w + (size_t)n * sizeof(double));
+    if (rc) return rc;
+    char* base = (char*)B->dge;
+    double* at = (double*)(base + o_t);
+    int32_t* ids = (int32_t*)(base + o_ids);
+    if (h_rowwit) {
+        d_rowwit = (const double*)(base + o_w);
+        CUDA_TRY(cudaMemcpyAsync((void*)d_rowwit, h_rowwit, (size_t)n * sizeof(double), cudaMemcpyHostToDevice, st));
+    }
+    cudaError_t e = transpose_launch(d_a, n, lda, at, n, st);
+    if (e != cudaSuccess) return fail(MCND_ECUDA, "transpose: %s", cudaGetErrorString(e));
+    std::vector<int32_t> iota((size_t)n);
+    for (int64_t i = 0; i < n; ++i) iota[(size_t)i] = (int32_t)i;
+    CUDA_TRY(cudaMemcpyAsync(ids, iota.data(), (size_t)n * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+    K1Run run;
+    run.n = n;
+    run.seq = iota;
+    run.steps = n - 1;
+    rc = k1_run_local(*B, at, n, n, (flags & MCND_FLAG_FAST) != 0, st, run, nullptr, nullptr, 0, nullptr, nullptr,
+                      ids, d_rowwit);
+    if (rc) return rc;
+    out->device_ms = run.device_ms;
+    out->launches = 2;
+    // replay the column exchanges: position l at step t holds original row ids[l]
+    std::vector<int64_t> perm;
+    perm.reserve((size_t)n);
+    std::vector<int32_t> cur = iota;
+    const int64_t np = run.singular_at >= 0 ? run.singular_at + 1 : n;
+    for (int64_t t = 0; t < np; ++t) {
+        const int64_t m = n - t;
+        const int32_t lr = run.piv_col[(size_t)t];
+        const int32_t l = lr >= 0 ? lr : -lr - 2;  // a singular record keeps its position as -(l + 2)
+        const int32_t id = cur[(size_t)l];
+        if (pivots_out) pivots_out[t] = run.piv_val[(size_t)t];
+        if (rows_out) rows_out[t] = id;
+        if (lr >= 0) { perm.push_back(id); if (l != m - 1) cur[(size_t)l] = cur[(size_t)(m - 1)]; }
+    }
+    if (run.singular_at >= 0) {
+        out->sign = 0; out->singular = 1; out->log_abs = -INFINITY;
+        out->singular_step = run.singular_at; out->steps = run.singular_at;
+        return MCND_OK;
+    }
+    double log_acc = 0.0;
+    int signs = 1;
+    for (int64_t t = 0; t < n; ++t) {
+        const double v = run.piv_val[(size_t)t];
+        log_acc += std::log(std::fabs(v));
+        signs *= v > 0 ? 1 : -1;
+    }
+    out->sign = signs * permutation_parity(perm);
+    out->log_abs = log_acc;
+    out->steps = n;
     return MCND_OK;
 }
 
@@ -1972,6 +2054,33 @@ int mcnd_logdet_blocked(const double* h_a, int64_t n, int64_t lda, uint32_t flag
 
 int32_t mcnd_blocked_panel(void) { return kK2B; }
 
+int mcnd_logdet_lu_dev(const double* d_a, int64_t n, int64_t lda, const double* d_row_witness, uint32_t flags,
+                       void* stream, mcnd_logdet* out, double* pivots_out, int32_t* rows_out) {
+    if (!out) return fail(MCND_EINVAL, "null out");
+    clear_out(out);
+    if (int rc = check_shape(d_a, n, lda)) return rc;
+    int code = MCND_OK;
+    Buffers* B = buffers_for_current(&code);
+    if (!B) return code;
+    std::lock_guard<std::mutex> lk(B->mu);
+    return ge_dev(d_a, n, lda, d_row_witness, flags, (cudaStream_t)stream, out, pivots_out, rows_out);
+}
+
+int mcnd_logdet_lu(const double* h_a, int64_t n, int64_t lda, const double* h_row_witness, uint32_t flags,
+                   void* stream, mcnd_logdet* out, double* pivots_out, int32_t* rows_out) {
+    if (!out) return fail(MCND_EINVAL, "null out");
+    clear_out(out);
+    if (int rc = check_shape(h_a, n, lda)) return rc;
+    int code = MCND_OK;
+    Buffers* B = buffers_for_current(&code);
+    if (!B) return code;
+    std::lock_guard<std::mutex> lk(B->mu);
+    const double* d_a = nullptr;
+    int rc = stage_input(*B, h_a, n, n, lda, (cudaStream_t)stream, &d_a);
+    if (rc) return rc;
+    return ge_dev(d_a, n, n, nullptr, flags, (cudaStream_t)stream, out, pivots_out, rows_out, h_row_witness);
+}
+
 int mcnd_fold_mc_parallel(int64_t n, int32_t p, const double* piv_vals, const int32_t* piv_cols,
                           int64_t singular_at, const double* rem, const double* rem_wit, mcnd_logdet* out,
                           mcnd_comm_stats* stats, int64_t* payload_entries, int64_t* row_updates) {
@@ -2160,6 +2269,7 @@ void mcnd_release_workspace(void) {
         cudaSetDevice(b.device);
         if (b.dws) cudaFree(b.dws);
         if (b.din) cudaFree(b.din);
+        if (b.dge) cudaFree(b.dge);
         if (b.hpin) cudaFreeHost(b.hpin);
         if (b.ev0) cudaEventDestroy(b.ev0);
         if (b.ev1) cudaEventDestroy(b.ev1);

@@ -68,9 +68,18 @@ struct K1Params {
     K1Err* err;
     int32_t chunk;                   // staged pivot-row chunk (even, <= kK1MaxChunk)
     unsigned long long timeout_ns;
+    // Gaussian-elimination mode (logdet_lu, gauss.py:34-68, run on A^T: the pivot row of A^T
+    // is the elimination column of A, its argmax the row pivot): ge_ids[c] = original row id
+    // of A at column position c (kept current across the column exchanges by the publishers),
+    // ties -> lowest ORIGINAL id, singular iff the pivot is exactly 0 or
+    // |v| <= 1e-12 * ge_rowwit[id] (optional caller witness).  nullptr: condensation.
+    int32_t* ge_ids;
+    const double* ge_rowwit;
 };
 
 cudaError_t k1_launch(const K1Params& p, bool fast, cudaStream_t s);
+// out = a^T (n x n; row strides lda, ldo)
+cudaError_t transpose_launch(const double* a, int64_t n, int64_t lda, double* out, int64_t ldo, cudaStream_t s);
 size_t k1_smem_bytes(int chunk);
 
 // ---- K2: blocked rank-b condensation (k2_blocked.cu) ----

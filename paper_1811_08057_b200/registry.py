@@ -1,11 +1,10 @@
 """The reference's plugin seam: ALGORITHMS + run_algorithm (mcnd/bench.py:25, :50-65).
 
 ``run_algorithm(name, a, p) -> RunResult`` dispatches by string exactly like
-the reference so its bench/CLI layers can call the GPU path by name.  Only
-the condensation algorithms are on the GPU path; the Gaussian-elimination
-names (ge-serial, ge-parallel) are the paper's comparison baseline and are
-out of scope here -- asking for them raises ValueError with
-a pointer back to the reference package.
+the reference so its bench/CLI layers can call the GPU path by name: the
+condensation algorithms (mc-serial, mc-parallel, + mc-blocked) and the paper's
+Gaussian-elimination baseline (ge-serial = gauss.py:34-68 logdet_lu, ge-parallel =
+runtime.py:232-321), all on the GPU.
 """
 
 from __future__ import annotations
@@ -16,10 +15,10 @@ import time
 from dataclasses import dataclass
 
 from .condense import logdet_blocked, logdet_condensation
+from .gauss import ge_parallel, logdet_lu
 from .runtime import CommStats, RunResult, mc_parallel
 
-ALGORITHMS = ("mc-serial", "mc-parallel", "mc-blocked")
-REFERENCE_ONLY = ("ge-serial", "ge-parallel")
+ALGORITHMS = ("mc-serial", "mc-parallel", "ge-serial", "ge-parallel", "mc-blocked")
 
 
 def run_algorithm(algorithm: str, a, p: int, *, fast: bool = False) -> RunResult:
@@ -34,8 +33,12 @@ def run_algorithm(algorithm: str, a, p: int, *, fast: bool = False) -> RunResult
         t0 = time.perf_counter()
         ld = logdet_blocked(a, fast=fast)
         return RunResult(logdet=ld, stats=CommStats(), n_workers=1, total_seconds=time.perf_counter() - t0)
-    if algorithm in REFERENCE_ONLY:
-        raise ValueError(f"algorithm {algorithm!r} is not on the GPU condensation path; use mcnd for it")
+    if algorithm == "ge-parallel":
+        return ge_parallel(a, p, fast=fast)
+    if algorithm == "ge-serial":
+        t0 = time.perf_counter()
+        ld = logdet_lu(a, fast=fast)
+        return RunResult(logdet=ld, stats=CommStats(), n_workers=1, total_seconds=time.perf_counter() - t0)
     raise ValueError(f"unknown algorithm {algorithm!r}")
 
 
@@ -45,7 +48,7 @@ def run_algorithm(algorithm: str, a, p: int, *, fast: bool = False) -> RunResult
 # format_report (speedup T_s / T_p, bench.py:178-195) covers GPU runs unchanged.
 CSV_HEADER = ["algorithm", "n", "p", "run", "total_s", "scatter_s", "comm_s", "sign", "logabs"]
 GPU_ALGORITHMS = {"mc-gpu": "mc-serial", "mc-gpu-parallel": "mc-parallel", "mc-gpu-blocked": "mc-blocked",
-                  "ge-gpu": "ge-cusolver"}
+                  "ge-gpu": "ge-serial", "ge-gpu-parallel": "ge-parallel", "ge-cusolver": "ge-cusolver"}
 
 
 def _ge_cusolver(d):
@@ -103,7 +106,7 @@ def run_bench(sizes, workers, repeats: int = 5, kind: str = "uniform-random", se
             for run in range(repeats):
                 for alg in algorithms:
                     base = GPU_ALGORITHMS[alg]
-                    if base != "mc-parallel" and p != 1:
+                    if base not in ("mc-parallel", "ge-parallel") and p != 1:
                         continue
                     torch.cuda.synchronize()
                     t0 = time.perf_counter()

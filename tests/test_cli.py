@@ -59,8 +59,8 @@ def test_logdet_workers_and_reference_only_algorithms(tmp_path, capsys):
     mio.write_matrix(np.eye(3), p)
     rc, _, err = run(["logdet", str(p), "--workers", "0"], capsys)
     assert rc == 1 and "workers must be >= 1" in err
-    rc, _, err = run(["logdet", str(p), "--algorithm", "ge-serial"], capsys)
-    assert rc == 1 and "not on the GPU condensation path" in err
+    rc, _, err = run(["logdet", str(p), "--algorithm", "ge-bogus"], capsys)
+    assert rc == 1 and "invalid choice" in err
 
 
 def test_csv_matrix_round_trip_and_errors(tmp_path):
@@ -97,11 +97,11 @@ def test_logdet_cli_on_gpu(tmp_path, capsys):
     p = tmp_path / "m.mcnd"
     mio.write_matrix(a, p)
     ref = O.logdet_condensation(a)
-    for alg, workers in [("mc-serial", 1), ("mc-parallel", 4), ("mc-blocked", 1)]:
+    for alg, workers in [("mc-serial", 1), ("mc-parallel", 4), ("mc-blocked", 1), ("ge-serial", 1), ("ge-parallel", 3)]:
         rc, out, _ = run(["logdet", str(p), "--algorithm", alg, "--workers", str(workers)], capsys)
         assert rc == 0, out
         m = re.match(r"status=ok sign=([+-]1) logabs=(\S+) algorithm=(\S+) workers=(\d+) broadcasts=(\d+) "
-                     r"broadcast_bytes=(\d+) pivot_search_msgs=0 scatter_s=\S+ comm_s=\S+ total_s=\S+$", out.strip())
+                     r"broadcast_bytes=(\d+) pivot_search_msgs=(\d+) scatter_s=\S+ comm_s=\S+ total_s=\S+$", out.strip())
         assert m, out
         assert int(m.group(1)) == ref.sign and abs(float(m.group(2)) - ref.log_abs) <= 1e-8 * 40
         if alg == "mc-parallel":

@@ -526,3 +526,62 @@ def test_blocked_streamed_host_input_errors(mc):
     h[n - 5, 17] = 0.5
     h[n - 700, :] = 0.0
     assert mc.logdet_blocked(h) == mc.SINGULAR
+
+
+# ---------------------------------------------------------------- GE counterpart (f3)
+GE_SERIAL = [c for c in load_cases() if c["algo"] == "ge_serial"]
+GE_PARALLEL = [c for c in load_cases() if c["algo"] == "ge_parallel"]
+
+
+@pytest.mark.parametrize("case", GE_SERIAL, ids=[c["name"] for c in GE_SERIAL])
+def test_ge_logdet_lu_bitwise_vs_reference(mc, case):
+    """gauss.py:34-68 on the GPU (K1 in GE mode on A^T): sign, log|det| and every pivot
+    (row and value) bitwise the reference's, with and without the row witness."""
+    a = case_input(case)
+    wit = np.max(np.abs(a), axis=1) if case["witness"] else None
+    res, piv, rows, _ = mc.logdet_lu(a, wit, return_pivots=True)
+    sign, la = expect(case)
+    assert res.sign == sign
+    if case.get("blas") and digest(a) != case["input_digest"]:
+        assert abs(res.log_abs - la) <= tol(a.shape[0], la)
+        return
+    assert same(res.log_abs, la), (res.log_abs, la)
+    k = len(case["ge_pivots"])
+    assert [int(r) for r in rows[:k]] == [r for (r, _) in case["ge_pivots"]]
+    assert [float(v) for v in piv[:k]] == [float.fromhex(v) for (_, v) in case["ge_pivots"]]
+
+
+@pytest.mark.parametrize("case", GE_PARALLEL, ids=[c["name"] for c in GE_PARALLEL])
+def test_ge_parallel_bitwise_and_stats(mc, case):
+    """runtime.py:232-321: the cyclic GE's result (per-owner log sums) and its accounting."""
+    import torch
+
+    a = case_input(case)
+    for src in (a, torch.from_numpy(a).cuda()):
+        res = mc.ge_parallel(src, case["p"])
+        assert (res.logdet.sign, res.logdet.log_abs) == expect(case) or same(res.logdet.log_abs, expect(case)[1])
+        st = case["stats"]
+        assert res.stats.broadcasts == st["broadcasts"]
+        assert res.stats.broadcast_bytes == st["broadcast_bytes"]
+        assert res.stats.pivot_search_msgs == st["pivot_search_msgs"]
+        assert res.broadcast_payload_entries == st["broadcast_payload_entries"]
+        assert res.row_updates == st["row_updates"]
+        assert res.scalar_updates == st["scalar_updates"]
+
+
+def test_ge_edges_and_large(mc):
+    """Non-finite input, a device tensor with lda > n, and N = 4000 against the oracle."""
+    import torch
+
+    from oracle import mcnd_oracle as O
+
+    bad = np.eye(30)
+    bad[4, 2] = np.inf
+    with pytest.raises(ValueError, match="finite"):
+        mc.logdet_lu(bad)
+    a = np.random.default_rng(8).standard_normal((257, 257))
+    big = torch.zeros((300, 301), dtype=torch.float64, device="cuda")
+    big[:257, :257] = torch.from_numpy(a)
+    assert mc.logdet_lu(big[:257, :257]) == mc.logdet_lu(a) == O.logdet_lu(a)
+    b = np.random.default_rng(9).uniform(-1, 1, (4000, 4000))
+    assert mc.logdet_lu(b) == O.logdet_lu(b)

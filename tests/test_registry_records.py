@@ -47,9 +47,9 @@ def test_reference_report_reads_gpu_records(tmp_path):
 def test_run_bench_gpu():
     recs = R.run_bench([64, 200], [1, 2], repeats=2)
     algs = {r.algorithm for r in recs}
-    assert algs == {"mc-gpu", "mc-gpu-parallel", "mc-gpu-blocked", "ge-gpu"}
+    assert algs == {"mc-gpu", "mc-gpu-parallel", "mc-gpu-blocked", "ge-gpu", "ge-gpu-parallel", "ge-cusolver"}
     assert all(r.total_seconds > 0 and r.scatter_seconds > 0 for r in recs)
-    assert not any(r.algorithm != "mc-gpu-parallel" and r.p != 1 for r in recs)
+    assert not any(r.algorithm not in ("mc-gpu-parallel", "ge-gpu-parallel") and r.p != 1 for r in recs)
     serial = {(r.n, r.run_index): (r.sign, r.log_abs) for r in recs if r.algorithm == "mc-gpu"}
     for r in recs:
         s, l = serial[(r.n, r.run_index)]
