@@ -64,6 +64,8 @@ typedef struct mcnd_comm_stats {
     int64_t pivot_search_msgs;
     int64_t scalar_updates;
     int64_t aborted_step;    /* -1 if no abort */
+    double scatter_seconds;  /* rows distributed to the workers (+ the H2D copy for host input) */
+    double comm_seconds;     /* time in the pivot-row broadcasts (device, summed over steps)  */
 } mcnd_comm_stats;
 
 /* ---- serial condensation: replaces mcnd.logdet_condensation (condense.py:134) ----

@@ -34,7 +34,8 @@ class McndLogDet(ctypes.Structure):
 class McndCommStats(ctypes.Structure):
     _fields_ = [("broadcasts", ctypes.c_int64), ("broadcast_bytes", ctypes.c_int64),
                 ("pivot_search_msgs", ctypes.c_int64), ("scalar_updates", ctypes.c_int64),
-                ("aborted_step", ctypes.c_int64)]
+                ("aborted_step", ctypes.c_int64), ("scatter_seconds", ctypes.c_double),
+                ("comm_seconds", ctypes.c_double)]
 
 
 _lock = threading.Lock()

@@ -148,6 +148,7 @@ __device__ void publish(const K1Params& p, Smem& sm, int g, int row, int t, int 
     // condense.py:90; GE mode: gauss.py:55-58 (exact zero, or the caller's row witness)
     const bool singular = p.ge_ids ? (v == 0.0 || (p.ge_rowwit && fabs(v) <= kSingularRtol * p.ge_rowwit[p.ge_ids[l]]))
                                    : !(fabs(v) > kSingularRtol * wit);
+    const unsigned long long t_pub = threadIdx.x == 0 ? globaltimer() : 0ull;  // CommStats.comm_seconds
     const int wp = m_pub - 1;
     const bool sys = p.sys_scope != 0;
     double* own = p.ws[g] + (int64_t)row * p.ld;
@@ -174,6 +175,7 @@ __device__ void publish(const K1Params& p, Smem& sm, int g, int row, int t, int 
         // (ordered before it by the barrier), no separate fence needed
         if (sys) __threadfence_system();
         for (int h = 0; h < p.n_groups; ++h) st_release_flag(&p.rec[h][t].flag, p.epoch, sys);
+        atomicAdd(&p.err->comm_ns, globaltimer() - t_pub);
     }
 }
 
@@ -182,6 +184,7 @@ __global__ void __launch_bounds__(kThreads, 1) k1_condense(const K1Params p) {
     extern __shared__ __align__(16) double s_prow[];
     __shared__ Smem sm;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const unsigned long long t_k0 = globaltimer();
     const int gl = blockIdx.x / p.ctas_per_group;  // local group
     const int g = p.group0 + gl;                   // global group (worker / rank)
     double* const ws = p.ws[g];
@@ -245,6 +248,7 @@ __global__ void __launch_bounds__(kThreads, 1) k1_condense(const K1Params p) {
         if (__any_sync(kFull, bad) && lane == 0) atomicOr(&p.err->nonfinite, 1u);
     }
     __syncthreads();
+    if (tid == 0 && !p.in_place) atomicMax(&p.err->scatter_ns, globaltimer() - t_k0);  // CommStats.scatter_seconds
 
     // ---- pivot 0 (its row was just copied by this CTA)
     if (nr > 0 && sm.pstep[0] == 0) {

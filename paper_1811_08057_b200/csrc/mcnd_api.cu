@@ -71,6 +71,7 @@ struct Buffers {
     cudaStream_t crit = nullptr;                 // K2: the panel chain (highest priority)
     cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_c = nullptr;  // K2: stream joins
     cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+    cudaEvent_t ev_h0 = nullptr, ev_h1 = nullptr;  // timed: host-input staging (mc_parallel's scatter)
     cudaStream_t cpy = nullptr;                  // K2 host input: row chunks copied while the first pairs run
     std::mutex mu;                               // calls on this device are serialised; other devices run concurrently
     static constexpr int kMaxChunks = 32;
@@ -84,7 +85,8 @@ std::deque<Buffers> g_bufs;  // one per device; deque: element addresses are sta
 int init_buffers(Buffers& b, int dev) {
     b.device = dev;
     cudaDeviceGetAttribute(&b.sms, cudaDevAttrMultiProcessorCount, dev);
-    if (cudaEventCreate(&b.ev0) != cudaSuccess || cudaEventCreate(&b.ev1) != cudaSuccess)
+    if (cudaEventCreate(&b.ev0) != cudaSuccess || cudaEventCreate(&b.ev1) != cudaSuccess ||
+        cudaEventCreate(&b.ev_h0) != cudaSuccess || cudaEventCreate(&b.ev_h1) != cudaSuccess)
         return fail(MCND_ECUDA, "cudaEventCreate failed");
     int prio_lo = 0, prio_hi = 0;
     cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
@@ -187,6 +189,7 @@ struct K1Run {
     std::vector<int32_t> piv_col;
     int64_t singular_at = -1;       // pivot index with failed witness test
     double device_ms = 0.0;
+    double scatter_s = 0.0, comm_s = 0.0;  // in-kernel distribution / pivot-row publication time
 };
 
 // Per-group workspace layout: [matrix n x ld][records npv][row_wit n]
@@ -341,6 +344,8 @@ int k1_execute(Buffers& B, K1Launch& L, bool fast, cudaStream_t st, K1Run& run) 
     float ms = 0.f;
     cudaEventElapsedTime(&ms, B.ev0, B.ev1);
     run.device_ms = ms;
+    run.scatter_s = (double)h_err->scatter_ns * 1e-9;
+    run.comm_s = (double)h_err->comm_ns * 1e-9;
     if (h_err->nonfinite) return fail(MCND_EINVAL, "matrix entries must be finite (no NaN/Inf)");
     if (h_err->error) return fail(MCND_EDEVICE, "device timeout waiting for pivot %u", h_err->err_step);
     run.piv_val.resize((size_t)npiv);
@@ -755,8 +760,13 @@ int parallel_dev(const double* d_a, int64_t n, int64_t lda, int32_t p, uint32_t 
     out->device_ms = run.device_ms;
     out->launches = 1;
     if (owners_out) for (size_t t = 0; t < owner.size(); ++t) owners_out[t] = owner[t];
-    return fold_parallel(n, p, run.piv_val.data(), run.piv_col.data(), run.singular_at, rem.data(), rem_wit.data(),
-                         out, stats, payload_out, row_updates_out);
+    rc = fold_parallel(n, p, run.piv_val.data(), run.piv_col.data(), run.singular_at, rem.data(), rem_wit.data(),
+                       out, stats, payload_out, row_updates_out);
+    if (stats) {
+        stats->scatter_seconds = run.scatter_s;
+        stats->comm_seconds = run.comm_s;
+    }
+    return rc;
 }
 
 // Host-input staging: copy an n x n (lda) host matrix into a cached device buffer.
@@ -2017,10 +2027,16 @@ int mcnd_mc_parallel(const double* h_a, int64_t n, int64_t lda, int32_t p, uint3
     if (!B) return code;
     std::lock_guard<std::mutex> lk(B->mu);
     const double* d_a = nullptr;
+    CUDA_TRY(cudaEventRecord(B->ev_h0, (cudaStream_t)stream));
     rc = stage_input(*B, h_a, n, n, lda, (cudaStream_t)stream, &d_a);
     if (rc) return rc;
-    return parallel_dev(d_a, n, n, p, flags, (cudaStream_t)stream, out, stats, payload_entries, row_updates,
-                        owners_out);
+    CUDA_TRY(cudaEventRecord(B->ev_h1, (cudaStream_t)stream));
+    rc = parallel_dev(d_a, n, n, p, flags, (cudaStream_t)stream, out, stats, payload_entries, row_updates,
+                      owners_out);
+    float h2d_ms = 0.f;  // the matrix reaching the device is part of the scatter (runtime.py:138-143)
+    if (rc == MCND_OK && stats && cudaEventElapsedTime(&h2d_ms, B->ev_h0, B->ev_h1) == cudaSuccess)
+        stats->scatter_seconds += (double)h2d_ms * 1e-3;
+    return rc;
 }
 
 /* debug (not part of the ABI header): panel-launch spans of the calls since the last read */

@@ -27,6 +27,8 @@ struct K1Err {
     unsigned nonfinite; // nonzero: the input held NaN/Inf (-> ValueError)
     unsigned torn;      // panel records read torn (one word stale) and re-polled
     unsigned dbg[8];    // diagnostics of the first timeout (panel kernel)
+    unsigned long long scatter_ns;  // K1: rows distributed into the workspaces (slowest CTA's prologue)
+    unsigned long long comm_ns;     // K1: time in pivot-row publications (the broadcasts of runtime.py:185)
 };
 
 // Persistent, barrier-free condensation kernel parameters (k1_condense.cu).

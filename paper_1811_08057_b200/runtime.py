@@ -108,9 +108,12 @@ def mc_parallel(a, p: int | None = None, *, n_workers: int | None = None, fast: 
     _lib.check(rc)
     total = time.perf_counter() - t0
     n_payload = int(out.steps)
+    # scatter: the rows distributed into the workers' workspaces (+ the H2D copy for a host
+    # matrix); comm: the pivot-row broadcasts (in-kernel publication time, summed over steps)
     stats = CommStats(broadcasts=int(st.broadcasts), broadcast_bytes=int(st.broadcast_bytes),
-                      pivot_search_msgs=int(st.pivot_search_msgs), scatter_seconds=0.0,
-                      comm_seconds=0.0, compute_seconds=float(out.device_ms) / 1e3)
+                      pivot_search_msgs=int(st.pivot_search_msgs), scatter_seconds=float(st.scatter_seconds),
+                      comm_seconds=float(st.comm_seconds),
+                      compute_seconds=max(0.0, float(out.device_ms) / 1e3 - float(st.comm_seconds)))
     ld_res = SINGULAR if out.singular else LogDet(int(out.sign), float(out.log_abs))
     return RunResult(logdet=ld_res, stats=stats, n_workers=p, total_seconds=total,
                      broadcast_payload_entries=[int(x) for x in payload[:n_payload]],

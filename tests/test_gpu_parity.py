@@ -585,3 +585,20 @@ def test_ge_edges_and_large(mc):
     assert mc.logdet_lu(big[:257, :257]) == mc.logdet_lu(a) == O.logdet_lu(a)
     b = np.random.default_rng(9).uniform(-1, 1, (4000, 4000))
     assert mc.logdet_lu(b) == O.logdet_lu(b)
+
+
+def test_mc_parallel_comm_timings(mc):
+    """CommStats timings (runtime.py:47-54, 138-143, 85-89): scatter = the rows distributed
+    into the workers' workspaces (+ the H2D copy of a host matrix), comm = the pivot-row
+    broadcasts (device time in the publications); both measured, comm inside the call."""
+    import torch
+
+    a = np.random.default_rng(2).uniform(-1, 1, (2000, 2000))
+    for src in (a, torch.from_numpy(a).cuda()):
+        r = mc.mc_parallel(src, 4)
+        st = r.stats
+        assert st.scatter_seconds > 0 and st.comm_seconds > 0
+        assert st.comm_seconds < r.total_seconds and st.scatter_seconds < r.total_seconds
+    host = mc.mc_parallel(a, 4).stats.scatter_seconds
+    dev = mc.mc_parallel(torch.from_numpy(a).cuda(), 4).stats.scatter_seconds
+    assert host > dev  # the 32 MB H2D copy is part of the host call's scatter
