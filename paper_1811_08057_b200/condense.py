@@ -121,12 +121,56 @@ def logdet_condensation(a, pivot_sequence: Optional[Sequence[int]] = None, *, fa
 
 
 
-def logdet_blocked(a, *, fast: bool = False, return_pivots: bool = False):
+def _perm_parity(perm) -> int:
+    """Parity of a permutation (cycle decomposition, as gauss.py:16-31)."""
+    seen = np.zeros(len(perm), dtype=bool)
+    par = 1
+    for s in range(len(perm)):
+        if seen[s]:
+            continue
+        ln, j = 0, s
+        while not seen[j]:
+            seen[j] = True
+            j = int(perm[j])
+            ln += 1
+        if ln % 2 == 0:
+            par = -par
+    return par
+
+
+def logdet_blocked(a, pivot_sequence: Optional[Sequence[int]] = None, *, fast: bool = False,
+                   return_pivots: bool = False):
     """Blocked rank-64 condensation (K2, csrc/k2_blocked.cu): panels of 64 pivot
     rows chosen by the reference's rule, trailing update on FP64 tensor cores.
-    Same result type and pivot rule as logdet_condensation (top-to-bottom);
-    rounding differs from the reference, so parity is by tolerance.  Input
-    handling as logdet_condensation."""
+    Same result type and pivot rule as logdet_condensation; rounding differs from
+    the reference, so parity is by tolerance.  Input handling as
+    logdet_condensation.
+
+    ``pivot_sequence`` (condense.py:147-152): the rows are taken in that order.  The
+    blocked kernels always run top to bottom, so the rows are gathered into that order on
+    the device first (the condensation steps only see which row is the pivot, never where
+    it sits) and the sign picks up the permutation's parity: det(A) = sgn(P) det(PA).  A
+    sequence that names an inactive row, or is too short, goes to logdet_condensation,
+    which raises exactly when the reference would (or returns SINGULAR first)."""
+    if pivot_sequence is not None:
+        n = int(a.shape[0]) if len(getattr(a, "shape", ())) == 2 else None
+        seq = [int(x) for x in list(pivot_sequence)[: max((n or 1) - 1, 0)]]
+        ok = n is not None and len(seq) >= n - 1 and all(0 <= r < n for r in seq) and len(set(seq)) == len(seq)
+        if not ok:
+            return logdet_condensation(a, pivot_sequence, fast=fast, return_pivots=return_pivots)
+        rest = sorted(set(range(n)) - set(seq))
+        perm = np.array(seq + rest, dtype=np.int64)
+        if _is_torch_cuda(a):
+            import torch
+
+            pa = a.index_select(0, torch.as_tensor(perm, device=a.device))
+        else:
+            pa = np.ascontiguousarray(np.asarray(a, dtype=np.float64)[perm])
+        out = logdet_blocked(pa, fast=fast, return_pivots=return_pivots)
+        res = out[0] if return_pivots else out
+        if res.sign != 0:
+            res = LogDet(res.sign * _perm_parity(perm), res.log_abs)
+        return (res,) + tuple(out[1:]) if return_pivots else res
     lib = _lib.load()
     out = _lib.McndLogDet()
     flags = _lib.FLAG_FAST if fast else 0

@@ -602,3 +602,26 @@ def test_mc_parallel_comm_timings(mc):
     host = mc.mc_parallel(a, 4).stats.scatter_seconds
     dev = mc.mc_parallel(torch.from_numpy(a).cuda(), 4).stats.scatter_seconds
     assert host > dev  # the 32 MB H2D copy is part of the host call's scatter
+
+
+def test_blocked_pivot_sequence_vs_oracle(mc):
+    """logdet_blocked with a caller pivot order (condense.py:147-152): rows gathered into that
+    order on the device, sign corrected by the permutation parity; within tolerance of the
+    oracle run in the same order, invalid sequences behave like logdet_condensation."""
+    import torch
+
+    from oracle import mcnd_oracle as O
+
+    for n, seed in ((300, 1), (1100, 2)):
+        a = np.random.default_rng(seed).uniform(-1, 1, (n, n))
+        seq = list(np.random.default_rng(seed + 5).permutation(n))[: n - 1]
+        ref = O.logdet_condensation(a, seq)
+        for src in (a, torch.from_numpy(a).cuda()):
+            got, piv, cols, _ = mc.logdet_blocked(src, seq, return_pivots=True)
+            assert got.sign == ref.sign and abs(got.log_abs - ref.log_abs) <= tol(n, ref.log_abs)
+            assert np.mean(cols[: n - 1] == ref.cols[: n - 1]) > 0.99
+    a = np.random.default_rng(0).uniform(-1, 1, (6, 6))
+    with pytest.raises(ValueError, match="not active"):
+        mc.logdet_blocked(a, [0, 1, 1, 2, 3])
+    with pytest.raises(IndexError):
+        mc.logdet_blocked(a, [0, 1])
