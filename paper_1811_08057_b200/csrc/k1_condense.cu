@@ -61,6 +61,25 @@ __device__ __forceinline__ unsigned long long globaltimer() {
     return t;
 }
 
+
+// Race stress (test builds only: MCND_BUILD_DEFINES="MCND_JITTER=1"): pseudo-random sleeps of up
+// to ~2 us at the protocol's hand-off points, so a read that is not properly ordered after its
+// write would see stale data (wrong pivots) or time out.  The parity tests then run unchanged.
+#ifndef MCND_JITTER
+#define MCND_JITTER 0
+#endif
+__device__ __forceinline__ void jitter(unsigned salt) {
+#if MCND_JITTER
+    unsigned long long c;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
+    unsigned x = (unsigned)c * 2654435761u ^ (blockIdx.x * 40503u + threadIdx.x * 9176u + salt * 7919u);
+    x ^= x >> 15; x *= 2246822519u; x ^= x >> 13;
+    if ((x & 7u) == 0u) __nanosleep(x % 2048u);
+#else
+    (void)salt;
+#endif
+}
+
 #ifndef K1_POLL_SLEEP
 #define K1_POLL_SLEEP 32  // ns between flag polls
 #endif
@@ -152,6 +171,7 @@ __device__ void publish(const K1Params& p, Smem& sm, int g, int row, int t, int 
     const int wp = m_pub - 1;
     const bool sys = p.sys_scope != 0;
     double* own = p.ws[g] + (int64_t)row * p.ld;
+    jitter(5u);
     if (!singular && wp > 0) {
         const double ylast = own[wp];
         for (int c = threadIdx.x; c < wp; c += kThreads) {
@@ -174,6 +194,7 @@ __device__ void publish(const K1Params& p, Smem& sm, int g, int row, int t, int 
         // single GPU: the gpu-scope release is cumulative over the CTA's row stores
         // (ordered before it by the barrier), no separate fence needed
         if (sys) __threadfence_system();
+        jitter(6u);
         for (int h = 0; h < p.n_groups; ++h) st_release_flag(&p.rec[h][t].flag, p.epoch, sys);
         atomicAdd(&p.err->comm_ns, globaltimer() - t_pub);
     }
@@ -354,6 +375,7 @@ __global__ void __launch_bounds__(kThreads, 1) k1_condense(const K1Params p) {
             if (tid == 0) sm.wit[start] = (unsigned long long)__double_as_longlong(wit);
         }
 
+        jitter(7u);
         // ---- bulk update of my other live rows, chunk by chunk
         for (int c0 = 0; c0 < w; c0 += p.chunk) {
             const int cend = (c0 + p.chunk < w) ? c0 + p.chunk : w;

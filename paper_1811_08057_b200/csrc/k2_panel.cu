@@ -139,6 +139,25 @@ __device__ __forceinline__ unsigned long long abs_bits(double x) {
     return (unsigned long long)__double_as_longlong(x) & 0x7fffffffffffffffull;
 }
 
+
+// Race stress (test builds only: MCND_BUILD_DEFINES="MCND_JITTER=1"): pseudo-random sleeps of up
+// to ~2 us at the protocol's hand-off points, so a read that is not properly ordered after its
+// write would see stale data (wrong pivots) or time out.  The parity tests then run unchanged.
+#ifndef MCND_JITTER
+#define MCND_JITTER 0
+#endif
+__device__ __forceinline__ void jitter(unsigned salt) {
+#if MCND_JITTER
+    unsigned long long c;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
+    unsigned x = (unsigned)c * 2654435761u ^ (blockIdx.x * 40503u + threadIdx.x * 9176u + salt * 7919u);
+    x ^= x >> 15; x *= 2246822519u; x ^= x >> 13;
+    if ((x & 7u) == 0u) __nanosleep(x % 2048u);
+#else
+    (void)salt;
+#endif
+}
+
 // Span log of the panel launches (CTA 0: globaltimer at entry and exit), read by
 // mcnd_debug_kp_spans() for schedule analysis; two stores per panel.
 __device__ unsigned long long g_kp_span[4096][2];
@@ -350,6 +369,7 @@ __global__ void __launch_bounds__(kThreads, 1) kp_panel_kernel(const KPParams p)
 #pragma unroll
             for (int k = 0; k < kPer; ++k)
                 if (lane + 32 * k < G) need |= 1u << k;
+            jitter(3u);
             for (unsigned it = 0;; ++it) {
 #pragma unroll
                 for (int k = 0; k < kPer; ++k)
@@ -552,6 +572,7 @@ __global__ void __launch_bounds__(kThreads, 1) kp_panel_kernel(const KPParams p)
                     const double rm = fmax(fmax(s_rmax[s + 1], s_rmax2[s + 1]), m0);
                     s_rmax[s + 1] = rm;
                     // proposal of pivot s+1 goes out now; its column follows in D2
+                    jitter(1u);
                     put(WREC(s + 1, g), pack(rm, tag1, 0));
                     put(CAND(s + 1, g), pack_cand(v0, tag1, i0, rm));
                     KP_MARK(s, 6);
@@ -579,6 +600,7 @@ __global__ void __launch_bounds__(kThreads, 1) kp_panel_kernel(const KPParams p)
         KP_MARK(s, 2);
         if (last_step) break;
         const double* us = S + s * cw;
+        jitter(4u);
         const int pos = s_cpos;                                   // candidate column of pivot s+1
         const int pc = (pos != INT_MAX) ? pos - lo : -1;          // local
         const int lc = (ms - 2 >= lo && ms - 2 - lo < wn) ? ms - 2 - lo : -1;  // new last column, local
@@ -602,6 +624,7 @@ __global__ void __launch_bounds__(kThreads, 1) kp_panel_kernel(const KPParams p)
                 }
                 put(LAST(s + 1, r), pack(xl, tag1, 0));
             }
+            jitter(2u);
             put(COL(s + 1, g, r), pack(xc, tag1, 0));
             if (r > s + 1) s_rmax2[r] = fmax(s_rmax2[r], mx);
         } else {
