@@ -1035,14 +1035,12 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
         *cw_out = cw;
         return G;
     };
-    // ~176 columns per panel CTA (C3 sweep with the 4-warp GEMM: 128: 31.26, 160: 31.19, 176: 31.03,
-    // 184: 31.54, 192: 31.50, 224: 31.74 ms): the pivot latency is flat up to ~200 columns
-    // (`scripts/micro/kp_bench.cu`), and fewer panel CTAs leave more SMs to the
-    // overlapped trailing GEMM
-    const int64_t kp_cols = kKPCols;
+    // panel chunk width: kp_cols_for(m) (mcnd_internal.h: the sweeps behind 176 / 240 columns)
     const int64_t kp_maxg = std::min<int64_t>(B->sms, env_long("MCND_KP_MAXG", kKPMaxG));  // test hook: wide chunks
-    auto kp_ctas = [&](int64_t m) {  // ~kp_cols columns per CTA, at most 256 unless the SM count caps G
-        return std::min<int64_t>({kp_maxg, (int64_t)kKPMaxG, std::max<int64_t>((m + 255) / 256, m / kp_cols)});
+    auto kp_ctas = [&](int64_t m) {  // ~kp_cols_for(m) columns per CTA, at most 256 unless the SM count caps G
+        const int64_t cols = kp_cols_for(m);
+        const int64_t cap = std::max<int64_t>(256, cols);
+        return std::min<int64_t>({kp_maxg, (int64_t)kKPMaxG, std::max<int64_t>((m + cap - 1) / cap, m / cols)});
     };
     auto run_kp = [&](int64_t kb, K2Gather* gp, double* Wout) -> cudaError_t {
         const int64_t m = n - kb;
@@ -1464,9 +1462,9 @@ int mg_load(MgHandle* h, const double* src, int64_t lds, cudaStream_t st) {
 
 KPParams mg_kp(MgHandle* h, int64_t lr0, int64_t t, int64_t m, K2Gather* gp, double* W, int64_t ldw) {
     const int64_t b = kK2B;
-    const int64_t cols = kKPCols;
+    const int64_t cols = kp_cols_for(m), cap = std::max<int64_t>(256, cols);
     int64_t G = std::min<int64_t>({(int64_t)h->sms, env_long("MCND_KP_MAXG", kKPMaxG), (int64_t)kKPMaxG,
-                                   std::max<int64_t>((m + 255) / 256, m / cols)});
+                                   std::max<int64_t>((m + cap - 1) / cap, m / cols)});
     int64_t cw = 0;
     for (;; --G) {
         cw = (int64_t)align_up((size_t)((m + G - 1) / G), 2);

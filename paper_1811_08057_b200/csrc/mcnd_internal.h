@@ -148,6 +148,13 @@ constexpr size_t kLastBufBytes = (size_t)64 * 64 * 16 + (size_t)kPPBars * sizeof
 // 184: 31.54, 192: 31.50, 224: 31.74 ms): the pivot latency is flat up to ~200 columns and fewer
 // panel CTAs leave more SMs to the overlapped trailing GEMM
 constexpr int kKPCols = 176;
+// while the trailing GEMM bounds the pair (m above ~6000 at the panel's ~3.2 us per pivot), wider
+// chunks: fewer panel CTAs, more SMs for the overlapped GEMM (C3 sweep: 176 everywhere 30.77 ms;
+// 208 / 240 / 272 / 320 above 6000: 30.59 / 30.36 / 30.54 / 30.45; 240 above 4500 / 6500 / 7200:
+// 30.60 / 30.54 / 30.67)
+constexpr int kKPColsWide = 240;
+constexpr int kKPWideAbove = 6000;
+__host__ __device__ constexpr int kp_cols_for(long long m) { return m > kKPWideAbove ? kKPColsWide : kKPCols; }
 constexpr int kKPMaxCw = 380;  // columns per panel CTA (64 x 380 doubles = 190 KB of shared memory)
 cudaError_t kp_launch(const KPParams& p, cudaStream_t s);
 size_t kp_smem_bytes(int cw);
