@@ -176,13 +176,19 @@ int64_t mcnd_mg_gather_bytes(void);   /* size of the gather descriptor to broadc
  * rank 0 fills an id (mcnd_nccl_id_bytes() bytes) with mcnd_nccl_unique_id, the ranks share it
  * over any host transport, every rank calls mcnd_mg_attach (world 1 needs no id and no NCCL;
  * force_comm = 1 runs the broadcasts even then).  mcnd_mg_logdet takes this rank's block rows
- * (plan_blocks(n, world), DEVICE pointer, row stride lds) and returns the whole matrix's result
+ * (plan_blocks(n, world), DEVICE pointer, row stride lds; `tail` rows finished by K1, 0 = 64) and
+ * returns the whole matrix's result
  * on every rank (synchronous; device_ms = this rank's time from entry to the folded records).
  * Replaces mc_parallel's worker loop (runtime.py:153-204) for the blocked variant. */
 int32_t mcnd_nccl_id_bytes(void);
 int mcnd_nccl_unique_id(void* id_out);
 int mcnd_mg_attach(void* handle, int32_t world, int32_t rank, const void* nccl_id, int32_t force_comm);
-int mcnd_mg_logdet(void* handle, const double* d_rows, int64_t lds, void* stream, mcnd_logdet* out);
+int mcnd_mg_logdet(void* handle, const double* d_rows, int64_t lds, int64_t tail, void* stream, mcnd_logdet* out);
+/* Test transport: the same driver with its collectives done by host callbacks on pinned
+ * buffers (bcast(buf, bytes, root); allgather(send, recv = world x bytes, bytes)), e.g. over
+ * gloo for ranks that share one GPU.  Callbacks return 0 on success. */
+int mcnd_mg_attach_host(void* handle, int32_t world, int32_t rank, int (*bcast)(void*, int64_t, int32_t),
+                        int (*allgather)(const void*, void*, int64_t));
 /* Host only: the pair schedule (5 int64 per pair: owner, local row, first pivot, active width,
  * k_pos) of n rows over world ranks with a `tail`-row K1 finish; returns the pair count. */
 int64_t mcnd_mg_schedule(int64_t n, int32_t world, int64_t tail, int64_t* pairs_out, int64_t max_pairs);

@@ -38,6 +38,10 @@ class McndCommStats(ctypes.Structure):
                 ("comm_seconds", ctypes.c_double)]
 
 
+# host-transport callbacks of the native multi-GPU driver (mcnd_mg_attach_host)
+HOST_BCAST = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32)
+HOST_ALLGATHER = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64)
+
 _lock = threading.Lock()
 LAST_LAUNCHES = 0  # GPU kernels launched by the most recent single-matrix call (bench accounting)
 LAST_TORN_READS = 0  # panel records the most recent blocked call saw half-written (re-polled)
@@ -54,7 +58,7 @@ EXPORTS = (
     "mcnd_mg_create", "mcnd_mg_load", "mcnd_mg_pair", "mcnd_mg_trailing", "mcnd_mg_export", "mcnd_mg_tail",
     "mcnd_mg_records", "mcnd_mg_gather_bytes", "mcnd_mg_ld", "mcnd_mg_destroy",
     "mcnd_nccl_id_bytes", "mcnd_nccl_unique_id", "mcnd_mg_attach", "mcnd_mg_logdet", "mcnd_mg_schedule",
-    "mcnd_logdet_lu_dev", "mcnd_logdet_lu",
+    "mcnd_logdet_lu_dev", "mcnd_logdet_lu", "mcnd_mg_attach_host",
 )
 
 
@@ -127,7 +131,9 @@ def load(path: str | None = None):
         lib.mcnd_nccl_unique_id.restype = ctypes.c_int
         lib.mcnd_mg_attach.argtypes = [P, i32, i32, P, i32]
         lib.mcnd_mg_attach.restype = ctypes.c_int
-        lib.mcnd_mg_logdet.argtypes = [P, P, i64, P, LD]
+        lib.mcnd_mg_attach_host.argtypes = [P, i32, i32, HOST_BCAST, HOST_ALLGATHER]
+        lib.mcnd_mg_attach_host.restype = ctypes.c_int
+        lib.mcnd_mg_logdet.argtypes = [P, P, i64, i64, P, LD]
         lib.mcnd_mg_logdet.restype = ctypes.c_int
         lib.mcnd_mg_schedule.argtypes = [i64, i32, i64, P, i64]
         lib.mcnd_mg_schedule.restype = ctypes.c_int64

@@ -1349,6 +1349,12 @@ struct MgHandle {
     int32_t world = 1, rank = 0;
     ncclComm_t comm = nullptr;
     bool use_comm = false;                      // broadcasts even with one rank (test hook)
+    // host transport (tests: ranks sharing one GPU over gloo): the collectives go through
+    // these callbacks on pinned staging buffers instead of NCCL
+    int (*host_bcast)(void* buf, int64_t bytes, int32_t root) = nullptr;
+    int (*host_allgather)(const void* send, void* recv, int64_t bytes) = nullptr;
+    void* hs_send = nullptr; size_t hs_send_bytes = 0;
+    void* hs_recv = nullptr; size_t hs_recv_bytes = 0;
     cudaStream_t crit = nullptr, side = nullptr, cst = nullptr;
     cudaEvent_t ev_pair[2] = {}, ev_bc[2] = {}, ev_trc[2] = {}, ev_trs[2] = {}, ev_side = nullptr, ev_crit = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -1746,6 +1752,9 @@ void mg_release_native(MgHandle* h) {
     h->comm = nullptr;
     if (h->pmem) cudaFree(h->pmem);
     h->pmem = nullptr;
+    if (h->hs_send) cudaFreeHost(h->hs_send);
+    if (h->hs_recv) cudaFreeHost(h->hs_recv);
+    h->hs_send = h->hs_recv = nullptr;
     for (int i = 0; i < 2; ++i)
         for (cudaEvent_t ev : {h->ev_pair[i], h->ev_bc[i], h->ev_trc[i], h->ev_trs[i]}) if (ev) cudaEventDestroy(ev);
     for (cudaEvent_t ev : {h->ev_side, h->ev_crit, h->ev0, h->ev1}) if (ev) cudaEventDestroy(ev);
@@ -1753,12 +1762,12 @@ void mg_release_native(MgHandle* h) {
     h->crit = h->side = h->cst = nullptr;
 }
 
-int mg_logdet(MgHandle* h, const double* rows, int64_t lds, cudaStream_t cur, mcnd_logdet* out) {
+int mg_logdet(MgHandle* h, const double* rows, int64_t lds, int64_t tail_rows, cudaStream_t cur, mcnd_logdet* out) {
     clear_out(out);
     if (!h->crit) { int rc = mg_attach(h, 1, 0, nullptr, 0); if (rc) return rc; }
     const int64_t n = h->n, b = kK2B;
     const int32_t world = h->world, rank = h->rank;
-    const int64_t tail = std::max<int64_t>(2, env_long("MCND_K2_TAIL", 64));  // test hook, as blocked_dev
+    const int64_t tail = std::max<int64_t>(2, tail_rows > 0 ? tail_rows : 64);  // rows finished by K1
     const MgSchedule S = mg_schedule(n, world, tail);
     if (S.len[rank] != h->lr)
         return fail(MCND_EINVAL, "mg_logdet: rank %d holds %lld rows, the plan gives it %lld", rank, (long long)h->lr,
@@ -1790,6 +1799,42 @@ int mg_logdet(MgHandle* h, const double* rows, int64_t lds, cudaStream_t cur, mc
     K2Gather* gp[2] = {(K2Gather*)(pb + o_gp), (K2Gather*)(pb + o_gp) + 1};
     cudaStream_t crit = h->crit, side = h->side, cst = h->cst;
     const NcclApi& nc = mg_nccl();
+    const bool host_tx = h->host_bcast != nullptr;
+    // the collectives: NCCL on the library's communicator, or (tests) host callbacks
+    auto bcast = [&](void* d, size_t bytes, int32_t root, cudaStream_t s) -> int {
+        if (!host_tx) {
+            NCCL_TRY(nc.broadcast(d, d, bytes, ncclUint8, root, h->comm, s));
+            return MCND_OK;
+        }
+        int r = ensure_pinned(&h->hs_send, &h->hs_send_bytes, bytes);
+        if (r) return r;
+        CUDA_TRY(cudaMemcpyAsync(h->hs_send, d, bytes, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        if (h->host_bcast(h->hs_send, (int64_t)bytes, root)) return fail(MCND_ENCCL, "host broadcast failed");
+        CUDA_TRY(cudaMemcpyAsync(d, h->hs_send, bytes, cudaMemcpyHostToDevice, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        return MCND_OK;
+    };
+    auto allgather = [&](const void* d_send, void* d_recv, size_t bytes, cudaStream_t s) -> int {
+        if (!host_tx) {
+            NCCL_TRY(nc.allGather(d_send, d_recv, bytes, ncclUint8, h->comm, s));
+            return MCND_OK;
+        }
+        int r = ensure_pinned(&h->hs_send, &h->hs_send_bytes, bytes);
+        if (!r) r = ensure_pinned(&h->hs_recv, &h->hs_recv_bytes, bytes * (size_t)world);
+        if (r) return r;
+        CUDA_TRY(cudaMemcpyAsync(h->hs_send, d_send, bytes, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        if (h->host_allgather(h->hs_send, h->hs_recv, (int64_t)bytes)) return fail(MCND_ENCCL, "host all-gather failed");
+        CUDA_TRY(cudaMemcpyAsync(d_recv, h->hs_recv, bytes * (size_t)world, cudaMemcpyHostToDevice, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        return MCND_OK;
+    };
+    auto group = [&](bool start) -> int {
+        if (host_tx) return MCND_OK;
+        NCCL_TRY(start ? nc.groupStart() : nc.groupEnd());
+        return MCND_OK;
+    };
 
     CUDA_TRY(cudaEventRecord(h->ev0, cur));
     CUDA_TRY(cudaStreamWaitEvent(crit, h->ev0, 0));
@@ -1825,11 +1870,10 @@ int mg_logdet(MgHandle* h, const double* rows, int64_t lds, cudaStream_t cur, mc
                 CUDA_TRY(cudaStreamWaitEvent(cst, h->ev_trc[q & 1], 0));
                 CUDA_TRY(cudaStreamWaitEvent(cst, h->ev_trs[q & 1], 0));
             }
-            NCCL_TRY(nc.groupStart());
-            NCCL_TRY(nc.broadcast(W[q & 1], W[q & 1], (size_t)128 * ldw, ncclFloat64, P.o, h->comm, cst));
-            NCCL_TRY(nc.broadcast(Wp[q & 1], Wp[q & 1], (size_t)b * b, ncclFloat64, P.o, h->comm, cst));
-            NCCL_TRY(nc.broadcast(gp[q & 1], gp[q & 1], sizeof(K2Gather), ncclUint8, P.o, h->comm, cst));
-            NCCL_TRY(nc.groupEnd());
+            if ((rc = group(true)) || (rc = bcast(W[q & 1], (size_t)128 * ldw * sizeof(double), P.o, cst)) ||
+                (rc = bcast(Wp[q & 1], (size_t)b * b * sizeof(double), P.o, cst)) ||
+                (rc = bcast(gp[q & 1], sizeof(K2Gather), P.o, cst)) || (rc = group(false)))
+                return rc;
             CUDA_TRY(cudaEventRecord(h->ev_bc[q & 1], cst));
             CUDA_TRY(cudaStreamWaitEvent(crit, h->ev_bc[q & 1], 0));
             CUDA_TRY(cudaStreamWaitEvent(side, h->ev_bc[q & 1], 0));
@@ -1875,10 +1919,9 @@ int mg_logdet(MgHandle* h, const double* rows, int64_t lds, cudaStream_t cur, mc
     double* twit = (double*)(pb + o_twit);
     if (live[rank] > 0 && (rc = mg_export(h, top[rank], live[rank], mt, buf, ldr, wbuf, cur))) return rc;
     if (h->use_comm) {
-        NCCL_TRY(nc.groupStart());
-        NCCL_TRY(nc.allGather(buf, gbuf, (size_t)rmax * ldr, ncclFloat64, h->comm, cur));
-        NCCL_TRY(nc.allGather(wbuf, gwbuf, (size_t)rmax, ncclFloat64, h->comm, cur));
-        NCCL_TRY(nc.groupEnd());
+        if ((rc = group(true)) || (rc = allgather(buf, gbuf, (size_t)rmax * ldr * sizeof(double), cur)) ||
+            (rc = allgather(wbuf, gwbuf, (size_t)rmax * sizeof(double), cur)) || (rc = group(false)))
+            return rc;
     } else {
         gbuf = buf;
         gwbuf = wbuf;
@@ -1902,10 +1945,9 @@ int mg_logdet(MgHandle* h, const double* rows, int64_t lds, cudaStream_t cur, mc
     CUDA_TRY(cudaMemcpyAsync(errs, h->err, 3 * sizeof(uint32_t), cudaMemcpyDeviceToDevice, cur));
     CUDA_TRY(cudaMemcpyAsync(errs + 3, epoch_h, sizeof(uint32_t), cudaMemcpyHostToDevice, cur));
     if (h->use_comm) {
-        NCCL_TRY(nc.groupStart());
-        NCCL_TRY(nc.allGather(h->recs, grec, (size_t)n * sizeof(PivRec), ncclUint8, h->comm, cur));
-        NCCL_TRY(nc.allGather(errs, gerr, 16, ncclUint8, h->comm, cur));
-        NCCL_TRY(nc.groupEnd());
+        if ((rc = group(true)) || (rc = allgather(h->recs, grec, (size_t)n * sizeof(PivRec), cur)) ||
+            (rc = allgather(errs, gerr, 16, cur)) || (rc = group(false)))
+            return rc;
     } else {
         grec = h->recs;
         gerr = errs;
@@ -2345,9 +2387,23 @@ int mcnd_mg_attach(void* handle, int32_t world, int32_t rank, const void* nccl_i
     if (!handle) return fail(MCND_EINVAL, "null handle");
     return mg_attach((MgHandle*)handle, world, rank, nccl_id, force_comm);
 }
-int mcnd_mg_logdet(void* handle, const double* d_rows, int64_t lds, void* stream, mcnd_logdet* out) {
+int mcnd_mg_attach_host(void* handle, int32_t world, int32_t rank, int (*bcast)(void*, int64_t, int32_t),
+                        int (*allgather)(const void*, void*, int64_t)) {
+    if (!handle || !bcast || !allgather) return fail(MCND_EINVAL, "null handle / callback");
+    if (world < 1 || rank < 0 || rank >= world) return fail(MCND_EINVAL, "mg_attach_host: bad rank %d of %d", rank, world);
+    int rc = mg_attach((MgHandle*)handle, 1, 0, nullptr, 0);  // the streams and events, no NCCL
+    if (rc) return rc;
+    auto* h = (MgHandle*)handle;
+    h->world = world;
+    h->rank = rank;
+    h->use_comm = true;
+    h->host_bcast = bcast;
+    h->host_allgather = allgather;
+    return MCND_OK;
+}
+int mcnd_mg_logdet(void* handle, const double* d_rows, int64_t lds, int64_t tail, void* stream, mcnd_logdet* out) {
     if (!handle || !out) return fail(MCND_EINVAL, "null handle/out");
-    return mg_logdet((MgHandle*)handle, d_rows, lds, (cudaStream_t)stream, out);
+    return mg_logdet((MgHandle*)handle, d_rows, lds, tail, (cudaStream_t)stream, out);
 }
 int64_t mcnd_mg_schedule(int64_t n, int32_t world, int64_t tail, int64_t* pairs_out, int64_t max_pairs) {
     if (n < 1 || world < 1 || world > n) return -1;

@@ -220,7 +220,30 @@ class BlockedGroup:
         # communicator) whenever the group is NCCL or a single rank; the Python loop below stays
         # for gloo groups (host-staged broadcasts: the CPU / shared-GPU tests)
         self.native = (self.nccl or self.world == 1) if native is None else bool(native)
-        if self.native:
+        if self.native and not self.nccl and self.world > 1:
+            # gloo group (tests: ranks sharing one GPU): the native driver with host collectives
+            import torch as _t
+
+            def _bcast(ptr, nbytes, root):
+                try:
+                    t = _t.frombuffer((ctypes.c_ubyte * nbytes).from_address(ptr), dtype=_t.uint8)
+                    dist.broadcast(t, root, group=self.group)
+                    return 0
+                except Exception:  # pragma: no cover
+                    return 1
+
+            def _allgather(send, recv, nbytes):
+                try:
+                    s = _t.frombuffer((ctypes.c_ubyte * nbytes).from_address(send), dtype=_t.uint8)
+                    r = _t.frombuffer((ctypes.c_ubyte * (nbytes * self.world)).from_address(recv), dtype=_t.uint8)
+                    dist.all_gather(list(r.view(self.world, nbytes).unbind(0)), s, group=self.group)
+                    return 0
+                except Exception:  # pragma: no cover
+                    return 1
+
+            self._cbs = (_lib.HOST_BCAST(_bcast), _lib.HOST_ALLGATHER(_allgather))  # kept alive
+            _lib.check(lib.mcnd_mg_attach_host(h, self.world, self.rank, *self._cbs))
+        elif self.native:
             idb = int(lib.mcnd_nccl_id_bytes())
             uid = bytes(idb)
             need = self.world > 1 or self.force_comm
@@ -268,8 +291,8 @@ class BlockedGroup:
             rows = rows.to(torch.float64).contiguous()
         if self.native:
             out = _lib.McndLogDet()
-            _lib.check(lib.mcnd_mg_logdet(h, rows.data_ptr(), rows.stride(0), torch.cuda.current_stream().cuda_stream,
-                                          ctypes.byref(out)))
+            _lib.check(lib.mcnd_mg_logdet(h, rows.data_ptr(), rows.stride(0), self.tail,
+                                          torch.cuda.current_stream().cuda_stream, ctypes.byref(out)))
             self.last_device_ms = float(out.device_ms)
             self.last_launches = int(out.launches)
             return SINGULAR if out.singular else LogDet(int(out.sign), float(out.log_abs))

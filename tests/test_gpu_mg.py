@@ -48,13 +48,18 @@ def _worker(rank, world, port, n, seed, tail, out_path):
     from paper_1811_08057_b200 import dist as D
 
     a = np.random.default_rng(seed).uniform(-1, 1, (n, n))
-    g = D.BlockedGroup(n, tail=tail)
+    g = D.BlockedGroup(n, tail=tail)  # the Python loop (host-staged broadcasts)
     s, ln = g.plan.assignments[rank]
     res = g.logdet(torch.from_numpy(np.ascontiguousarray(a[s:s + ln])).cuda())
     res2 = g.logdet(torch.from_numpy(np.ascontiguousarray(a[s:s + ln])).cuda())  # reuse of the handle
     g.close()
+    # the native per-rank driver (mcnd_mg_logdet) with its collectives over gloo: the same
+    # kernels in the same order on every rank -> the same result to the last bit
+    gn = D.BlockedGroup(n, tail=tail, native=True)
+    res3 = gn.logdet(torch.from_numpy(np.ascontiguousarray(a[s:s + ln])).cuda())
+    gn.close()
     if rank == 0:
-        np.save(out_path, np.array([res.sign, res.log_abs, res2.sign, res2.log_abs]))
+        np.save(out_path, np.array([res.sign, res.log_abs, res2.sign, res2.log_abs, res3.sign, res3.log_abs]))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -87,18 +92,19 @@ def test_mg_world1_vs_oracle(mc, n, tail):
     assert abs(got.log_abs - ref.log_abs) <= tol(n, ref.log_abs)
 
 
-@pytest.mark.parametrize("n,tail", [(700, 2), (1500, 256)])
-def test_mg_world2_gloo_vs_oracle(mc, tmp_path, n, tail):
+@pytest.mark.parametrize("n,tail,world", [(700, 2, 2), (1500, 256, 2), (2000, 64, 3)])
+def test_mg_world2_gloo_vs_oracle(mc, tmp_path, n, tail, world):
     import torch.multiprocessing as tmp
 
     out = str(tmp_path / "res.npy")
-    tmp.start_processes(_worker, args=(2, _port(), n, 7, tail, out), nprocs=2, join=True, start_method="spawn")
+    tmp.start_processes(_worker, args=(world, _port(), n, 7, tail, out), nprocs=world, join=True, start_method="spawn")
     r = np.load(out)
     a = np.random.default_rng(7).uniform(-1, 1, (n, n))
-    ref = _oracle(a, 2, tail)
+    ref = _oracle(a, world, tail)
     assert int(r[0]) == ref.sign and int(r[2]) == ref.sign
     assert abs(r[1] - ref.log_abs) <= tol(n, ref.log_abs)
     assert r[1] == r[3]  # deterministic across calls
+    assert int(r[4]) == ref.sign and r[5] == r[1]  # native driver == Python loop, bitwise
 
 
 def test_mg_singular_and_nonfinite(mc):
