@@ -1042,20 +1042,26 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
         const int64_t cap = std::max<int64_t>(256, cols);
         return std::min<int64_t>({kp_maxg, (int64_t)kKPMaxG, std::max<int64_t>((m + cap - 1) / cap, m / cols)});
     };
+    // the parameters of the panel at kb; its column chunks split the active width `m_split`
+    // (the pair's first panel's: the second panel runs on the same CTAs and chunks)
+    auto kp_at = [&](int64_t kb, K2Gather* gp, double* Wout, int64_t m_split) -> KPParams {
+        KPParams q = kp;
+        int64_t cw = 0;
+        const int64_t G = split(m_split, kp_ctas(m_split), &cw);
+        q.row0 = (int32_t)kb;
+        q.m = (int32_t)(n - kb);
+        q.G = (int32_t)G;
+        q.cw = (int32_t)cw;
+        q.rec = recs + kb;
+        q.pan = gp;
+        q.W = Wout;
+        q.tag0 = kp_tag0(kb);  // slots cleared per call
+        return q;
+    };
     auto run_kp = [&](int64_t kb, K2Gather* gp, double* Wout) -> cudaError_t {
-        const int64_t m = n - kb;
-        int64_t cw = 0, G = 0;
-        G = split(m, kp_ctas(m), &cw);
-        if (kp_smem_bytes((int)cw) > 190 * 1024) return cudaErrorInvalidValue;
-        kp.row0 = (int32_t)kb;
-        kp.m = (int32_t)m;
-        kp.G = (int32_t)G;
-        kp.cw = (int32_t)cw;
-        kp.rec = recs + kb;
-        kp.pan = gp;
-        kp.W = Wout;
-        kp.tag0 = (uint32_t)(kb + 1);  // global step + 1: unique within the call (slots cleared per call)
-        return kp_launch(kp, st);
+        const KPParams q = kp_at(kb, gp, Wout, n - kb);
+        if (kp_smem_bytes(q.cw) > 190 * 1024) return cudaErrorInvalidValue;
+        return kp_launch(q, st);
     };
     // Panels go in pairs: panel k, then its update of panel k+1's 64 rows, panel
     // k+1, and ONE rank-128 trailing update (half the C traffic of two rank-64
@@ -1137,17 +1143,20 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
         };
         const int64_t cov_end = cr[cov_q + 1];  // rows past it are not resident yet
         if (k + 1 < n_panels) {
-            e = run_kp(kb, gp0, Wq);
-            mark("kp1");
-            // the second panel kernel applies the first panel to its own rows in its prologue
-            // and runs the pair prep (spread over its CTAs around one grid barrier)
-            kp.r1_g0 = gp0; kp.r1_W = Wq; kp.r1_ldw = ld;
-            kp.pp_g0 = gp0; kp.pp_W = Wq; kp.pp_ldw = ld; kp.pp_Wp = Wp; kp.pp_gpair = gpair; kp.pp_m = (int32_t)m;
-            kp.pp_bar = reinterpret_cast<unsigned*>(kp.lastbuf + 64 * 64) + kb / (2 * b);
-            if (e == cudaSuccess) e = run_kp(kb + b, gp1, Wq + b * ld);
-            kp.pp_g0 = nullptr;
-            kp.r1_g0 = nullptr;
-            mark("kp2");
+            // both panels of the pair in ONE launch on the same CTAs: the second applies the
+            // first's update to its own rows in its prologue and runs the pair prep (spread over
+            // its CTAs around one grid barrier)
+            {
+                const KPParams q0 = kp_at(kb, gp0, Wq, m);
+                KPParams q1 = kp_at(kb + b, gp1, Wq + b * ld, m);
+                unsigned* const bars = reinterpret_cast<unsigned*>(kp.lastbuf + 64 * 64);
+                q1.r1_g0 = gp0; q1.r1_W = Wq; q1.r1_ldw = ld;
+                q1.pp_g0 = gp0; q1.pp_W = Wq; q1.pp_ldw = ld; q1.pp_Wp = Wp; q1.pp_gpair = gpair; q1.pp_m = (int32_t)m;
+                q1.pp_bar = bars + kb / (2 * b);
+                q1.half_bar = bars + kPPBars + kb / (2 * b);
+                e = kp_smem_bytes(q0.cw) > 190 * 1024 ? cudaErrorInvalidValue : kp_launch(q0, st, &q1);
+            }
+            mark("kp_pair");
             if (e == cudaSuccess) e = join_rows();  // the critical rows final for the previous pair
             mark("join");
             const int32_t nr = (int32_t)(n - kb - 2 * b);
@@ -1208,7 +1217,7 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
                 side_pending = (e == cudaSuccess);
                 n_launch += 3;
             }
-            n_launch += 4;  // 2 panels, gather + L correction, the critical update
+            n_launch += 3;  // the panel pair, gather + L correction, the critical update
             if (streamed) done_pairs.push_back({kb, m, par});
             k += 2;
             par = (par + 1) % kRing;
@@ -1466,8 +1475,12 @@ int mg_load(MgHandle* h, const double* src, int64_t lds, cudaStream_t st) {
     return MCND_OK;
 }
 
-KPParams mg_kp(MgHandle* h, int64_t lr0, int64_t t, int64_t m, K2Gather* gp, double* W, int64_t ldw) {
+// m_split: the active width the column chunks split (the pair's first panel's for both)
+KPParams mg_kp(MgHandle* h, int64_t lr0, int64_t t, int64_t m, K2Gather* gp, double* W, int64_t ldw,
+               int64_t m_split = -1) {
     const int64_t b = kK2B;
+    const int64_t m_act = m;
+    if (m_split > 0) m = m_split;
     const int64_t cols = kp_cols_for(m), cap = std::max<int64_t>(256, cols);
     int64_t G = std::min<int64_t>({(int64_t)h->sms, env_long("MCND_KP_MAXG", kKPMaxG), (int64_t)kKPMaxG,
                                    std::max<int64_t>((m + cap - 1) / cap, m / cols)});
@@ -1480,13 +1493,13 @@ KPParams mg_kp(MgHandle* h, int64_t lr0, int64_t t, int64_t m, K2Gather* gp, dou
     kp.ws = h->ws;
     kp.ld = h->ld;
     kp.row0 = (int32_t)lr0;
-    kp.m = (int32_t)m;
+    kp.m = (int32_t)m_act;
     kp.G = (int32_t)G;
     kp.cw = (int32_t)cw;
     kp.wit = h->wit;
     kp.rec = h->recs + t;
     kp.epoch = h->epoch;
-    kp.tag0 = (uint32_t)(t + 1);  // slots cleared by mg_load
+    kp.tag0 = kp_tag0(t);  // slots cleared by mg_load
     kp.W = W;
     kp.ldw = ldw;
     kp.pan = gp;
@@ -1514,15 +1527,26 @@ int mg_pair(MgHandle* h, int64_t lr0, int64_t t, int64_t m, double* W, int64_t l
                     (long long)t);
     K2Gather* gp0 = h->gp;
     K2Gather* gp1 = h->gp + 1;
-    KPParams kp = mg_kp(h, lr0, t, m, gp0, W, ldw);
-    cudaError_t e = kp_launch(kp, st);
-    if (e == cudaSuccess) {
-        KPParams kp1 = mg_kp(h, lr0 + b, t + b, m - b, gp1, W + b * ldw, ldw);
+    const KPParams kp = mg_kp(h, lr0, t, m, gp0, W, ldw);
+    cudaError_t e = cudaSuccess;
+    const int64_t pair = t / (2 * b);
+    unsigned* const bars = reinterpret_cast<unsigned*>(h->lastb + 64 * 64);
+    if (pair < kPPBars) {
+        // both panels in one launch on the same CTAs and column chunks (as blocked_dev)
+        KPParams kp1 = mg_kp(h, lr0 + b, t + b, m - b, gp1, W + b * ldw, ldw, m);
         kp1.r1_g0 = gp0; kp1.r1_W = W; kp1.r1_ldw = ldw;  // + the first panel's update of these rows
         kp1.pp_g0 = gp0; kp1.pp_W = W; kp1.pp_ldw = ldw; kp1.pp_Wp = Wp; kp1.pp_gpair = gpair; kp1.pp_m = (int32_t)m;
-        kp1.pp_bar = (t / (2 * b) < kPPBars)
-                         ? reinterpret_cast<unsigned*>(h->lastb + 64 * 64) + t / (2 * b) : nullptr;
-        e = kp_launch(kp1, st);  // + the pair prep in its CTA 0
+        kp1.pp_bar = bars + pair;
+        kp1.half_bar = bars + kPPBars + pair;
+        e = kp_launch(kp, st, &kp1);
+    } else {
+        e = kp_launch(kp, st);
+        if (e == cudaSuccess) {
+            KPParams kp1 = mg_kp(h, lr0 + b, t + b, m - b, gp1, W + b * ldw, ldw);
+            kp1.r1_g0 = gp0; kp1.r1_W = W; kp1.r1_ldw = ldw;
+            kp1.pp_g0 = gp0; kp1.pp_W = W; kp1.pp_ldw = ldw; kp1.pp_Wp = Wp; kp1.pp_gpair = gpair; kp1.pp_m = (int32_t)m;
+            e = kp_launch(kp1, st);  // + the pair prep in its CTA 0 (no barrier counter left)
+        }
     }
     if (e != cudaSuccess) return fail(MCND_ECUDA, "mg_pair: %s", cudaGetErrorString(e));
     return MCND_OK;
@@ -1849,7 +1873,7 @@ int mg_logdet(MgHandle* h, const double* rows, int64_t lds, int64_t tail_rows, c
         int r = mg_pair(h, P.lr0, P.t, P.m, W[q & 1], ldw_of(P.m), Wp[q & 1], gp[q & 1], crit);
         if (r) return r;
         CUDA_TRY(cudaEventRecord(h->ev_pair[q & 1], crit));
-        nl += 2;
+        nl += (P.t / (2 * kK2B) < kPPBars) ? 1 : 2;  // one launch for both panels (mg_pair)
         return MCND_OK;
     };
     auto trailing = [&](int64_t r0, int64_t nrows, size_t q, bool on_side) -> int {

@@ -139,11 +139,16 @@ struct KPParams {
     // in slices, the composite descriptor in CTA 0) around one grid barrier on this
     // counter (zeroed per call, one per pair); nullptr: CTA 0 does all of it
     unsigned* pp_bar;
+    // second half of a two-panel launch: the grid barrier between the panels (zeroed per call)
+    unsigned* half_bar;
 };
 constexpr int kKPMaxG = 160;
 // lastbuf allocation: the LAST records [64][64], then the pair-prep barrier counters
+// 16-bit record tags: step t's tag, wrapped so tag0 .. tag0 + 64 stays below 0xffff and never 0
+// (a slot read in one panel was last written by the panel before it, 64 steps back)
+inline uint32_t kp_tag0(int64_t t) { return (uint32_t)(t % 65472) + 1u; }
 constexpr int kPPBars = 1024;  // pairs per call (n <= 131072)
-constexpr size_t kLastBufBytes = (size_t)64 * 64 * 16 + (size_t)kPPBars * sizeof(unsigned);
+constexpr size_t kLastBufBytes = (size_t)64 * 64 * 16 + (size_t)2 * kPPBars * sizeof(unsigned);  // + pp / half barriers
 // ~176 columns per panel CTA (C3 sweep with the 4-warp GEMM: 128: 31.26, 160: 31.19, 176: 31.03,
 // 184: 31.54, 192: 31.50, 224: 31.74 ms): the pivot latency is flat up to ~200 columns and fewer
 // panel CTAs leave more SMs to the overlapped trailing GEMM
@@ -156,7 +161,8 @@ constexpr int kKPColsWide = 240;
 constexpr int kKPWideAbove = 6000;
 __host__ __device__ constexpr int kp_cols_for(long long m) { return m > kKPWideAbove ? kKPColsWide : kKPCols; }
 constexpr int kKPMaxCw = 380;  // columns per panel CTA (64 x 380 doubles = 190 KB of shared memory)
-cudaError_t kp_launch(const KPParams& p, cudaStream_t s);
+// second != nullptr: one launch runs p then *second (the pair's second panel, same G / cw)
+cudaError_t kp_launch(const KPParams& p, cudaStream_t s, const KPParams* second = nullptr);
 size_t kp_smem_bytes(int cw);
 // debug: (entry, exit) globaltimer of the panel launches since the last call; returns the count
 int kp_debug_spans(unsigned long long* out, int max_spans);
