@@ -338,7 +338,10 @@ __global__ void __launch_bounds__(64 * (BNT / 32) * SUB, 2 / SUB) k2_gemm_ms_ker
 constexpr int W4_THREADS = 128;
 // WN = warps in N: 2 -> 64 x 128 tiles, 128 threads (the trailing update); 1 -> 64 x 64 tiles,
 // 64 threads (the short critical-path update: twice the CTAs)
-template <int K, int S, int WN = 2, int BK = MS_BK>
+// U: stages per iteration of the (not unrolled) stage loop -- 2 in the persistent grid (the
+// compiler keeps the accumulators in place across the pair: 28.15 -> 28.67 TF at n = 16384,
+// scripts/micro/gemm_w5.cu), 1 for one tile per CTA (2 is 0.5 % slower there)
+template <int K, int S, int WN = 2, int BK = MS_BK, int U = 1>
 __global__ void __launch_bounds__(64 * WN, 2) k2_gemm_w4_kernel(double* __restrict__ ws, int64_t ld, int32_t rbase,
                                                                     int32_t M, int32_t N2, const double* __restrict__ L,
                                                                     int64_t ldl, const double* __restrict__ W, int64_t ldw,
@@ -449,7 +452,7 @@ __global__ void __launch_bounds__(64 * WN, 2) k2_gemm_w4_kernel(double* __restri
     double rmx[MI] = {0.0, 0.0, 0.0, 0.0};
     int c_slot = 0;
     for (;;) {
-#pragma unroll 1
+#pragma unroll U
         for (int ks = 0; ks < KS; ++ks) {
             if (ks == KS / 2 && t + 1 < t_end) {
                 const int tn = t + 1;
@@ -559,12 +562,13 @@ cudaError_t k2_gemm(double* ws, int64_t ld, int32_t rbase, int32_t M, int32_t N2
     if (!attr_done[dev]) {
         if ((e = cudaFuncSetAttribute(k2_gemm_w4_kernel<64, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm4)) != cudaSuccess ||
             (e = cudaFuncSetAttribute(k2_gemm_w4_kernel<128, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm4)) != cudaSuccess ||
+            (e = cudaFuncSetAttribute(k2_gemm_w4_kernel<128, 3, 2, MS_BK, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm4)) != cudaSuccess ||
             (e = cudaFuncSetAttribute(k2_gemm_ms_kernel<128, 1, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smn)) != cudaSuccess)
             return e;
         attr_done[dev] = true;
     }
     auto* w = reinterpret_cast<unsigned long long*>(row_wit);
-    if (sm_budget >= 0 && M <= 2 * BM && K == 128) {
+    if (sm_budget == 0 && M <= 2 * BM && K == 128) {
         // a short critical-path update (the next pair's 128 rows): 64 x 64 tiles, twice the
         // CTAs of the 64 x 128 kernel, so more SMs share it (measured faster than the 4-warp
         // kernel with 64-wide tiles: 24.6 vs 25.1 us at m = 8000, and inside C3/C5)
@@ -581,7 +585,8 @@ cudaError_t k2_gemm(double* ws, int64_t ld, int32_t rbase, int32_t M, int32_t N2
     const bool one_tile = sm_budget < 0 && tiles <= 40 * 2 * (int64_t)sms;
     const int g4 = (int)(one_tile ? tiles : std::min<int64_t>(tiles, 2 * (int64_t)sms));
     if (K == 64) k2_gemm_w4_kernel<64, 3><<<g4, W4_THREADS, sm4, s>>>(ws, ld, rbase, M, N2, L, ldl, W, ldw, w, abort);
-    else k2_gemm_w4_kernel<128, 3><<<g4, W4_THREADS, sm4, s>>>(ws, ld, rbase, M, N2, L, ldl, W, ldw, w, abort);
+    else if (one_tile) k2_gemm_w4_kernel<128, 3><<<g4, W4_THREADS, sm4, s>>>(ws, ld, rbase, M, N2, L, ldl, W, ldw, w, abort);
+    else k2_gemm_w4_kernel<128, 3, 2, MS_BK, 2><<<g4, W4_THREADS, sm4, s>>>(ws, ld, rbase, M, N2, L, ldl, W, ldw, w, abort);
     return cudaGetLastError();
 }
 

@@ -1060,7 +1060,7 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
     };
     auto run_kp = [&](int64_t kb, K2Gather* gp, double* Wout) -> cudaError_t {
         const KPParams q = kp_at(kb, gp, Wout, n - kb);
-        if (kp_smem_bytes(q.cw) > 190 * 1024) return cudaErrorInvalidValue;
+        if (q.cw > kKPMaxCw) return cudaErrorInvalidValue;
         return kp_launch(q, st);
     };
     // Panels go in pairs: panel k, then its update of panel k+1's 64 rows, panel
@@ -1097,7 +1097,7 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
     int64_t n_launch = 1;  // kernels launched by this call (K1 init so far)
     // debug timeline (MCND_DEBUG_TIMELINE=1): an event after every critical-stream step,
     // per-label device time printed to stderr at the end of the call
-    const bool dbg_tl = env_long("MCND_DEBUG_TIMELINE", 0) != 0;
+    const long dbg_tl = env_long("MCND_DEBUG_TIMELINE", 0);  // 2: every step
     std::vector<std::pair<const char*, cudaEvent_t>> tl;
     auto mark = [&](const char* label) {
         if (!dbg_tl) return;
@@ -1154,7 +1154,7 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
                 q1.pp_g0 = gp0; q1.pp_W = Wq; q1.pp_ldw = ld; q1.pp_Wp = Wp; q1.pp_gpair = gpair; q1.pp_m = (int32_t)m;
                 q1.pp_bar = bars + kb / (2 * b);
                 q1.half_bar = bars + kPPBars + kb / (2 * b);
-                e = kp_smem_bytes(q0.cw) > 190 * 1024 ? cudaErrorInvalidValue : kp_launch(q0, st, &q1);
+                e = kp_launch(q0, st, &q1);  // (checks the chunk width)
             }
             mark("kp_pair");
             if (e == cudaSuccess) e = join_rows();  // the critical rows final for the previous pair
@@ -1259,6 +1259,7 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
             auto& a = acc[tl[i].first];
             a.first += ms;
             a.second += 1;
+            if (dbg_tl > 1) std::fprintf(stderr, "mcnd step %4zu %-12s %8.1f us\n", i, tl[i].first, 1e3 * ms);
         }
         for (auto& kv : acc)
             std::fprintf(stderr, "mcnd timeline %-10s %8.3f ms  (%d x %.1f us)\n", kv.first.c_str(), kv.second.first,
@@ -1383,6 +1384,11 @@ int mg_create(int64_t n, int64_t lr, MgHandle** out) {
     const int64_t b = kK2B, lrr = std::max<int64_t>(lr, 1);
     h->g0 = std::max<int64_t>(1, std::min<int64_t>(h->sms, lrr));
     if ((lrr + h->g0 - 1) / h->g0 > kK1MaxRowsPerCta) { delete h; return fail(MCND_EINVAL, "mg_create: %lld rows too many", (long long)lr); }
+    if (n > (int64_t)kKPMaxCw * std::min<int64_t>(h->sms, kKPMaxG)) {  // the owner's panel spans all n columns
+        delete h;
+        return fail(MCND_EINVAL, "mg_create: n=%lld too large for the panel kernel (at most %d columns per SM)",
+                    (long long)n, kKPMaxCw);
+    }
     size_t off = 0;
     auto take = [&](size_t by) { size_t o = off; off = align_up(off + by, 256); return o; };
     const size_t o_ws = take((size_t)lrr * h->ld * sizeof(double));

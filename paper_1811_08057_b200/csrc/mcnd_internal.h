@@ -144,9 +144,6 @@ struct KPParams {
 };
 constexpr int kKPMaxG = 160;
 // lastbuf allocation: the LAST records [64][64], then the pair-prep barrier counters
-// 16-bit record tags: step t's tag, wrapped so tag0 .. tag0 + 64 stays below 0xffff and never 0
-// (a slot read in one panel was last written by the panel before it, 64 steps back)
-inline uint32_t kp_tag0(int64_t t) { return (uint32_t)(t % 65472) + 1u; }
 constexpr int kPPBars = 1024;  // pairs per call (n <= 131072)
 constexpr size_t kLastBufBytes = (size_t)64 * 64 * 16 + (size_t)2 * kPPBars * sizeof(unsigned);  // + pp / half barriers
 // ~176 columns per panel CTA (C3 sweep with the 4-warp GEMM: 128: 31.26, 160: 31.19, 176: 31.03,
@@ -159,8 +156,20 @@ constexpr int kKPCols = 176;
 // 30.60 / 30.54 / 30.67)
 constexpr int kKPColsWide = 240;
 constexpr int kKPWideAbove = 6000;
-__host__ __device__ constexpr int kp_cols_for(long long m) { return m > kKPWideAbove ? kKPColsWide : kKPCols; }
-constexpr int kKPMaxCw = 380;  // columns per panel CTA (64 x 380 doubles = 190 KB of shared memory)
+// far above (C5, m up to 32768): 300 columns -- 110 CTAs instead of 136 at m = 32768, the rest of
+// the SMs for the GEMM (C5 sweep: 240 / 280 / 300 / 320 / 368 above 12000: 0.915 / - / 0.904 / 0.923
+// / 0.921 s; 300 above 9000 / 16000: 0.905 / 0.904 s)
+constexpr int kKPColsXL = 300;
+constexpr int kKPXLAbove = 12000;
+__host__ __device__ constexpr int kp_cols_for(long long m) {
+    return m > kKPXLAbove ? kKPColsXL : m > kKPWideAbove ? kKPColsWide : kKPCols;
+}
+// columns per panel CTA: 64 x 368 doubles = 184 KB of dynamic shared memory, + the kernel's 42 KB
+// static, inside the 227 KB a CTA may have (n up to 368 x 148 = 54464 on one B200)
+constexpr int kKPMaxCw = 368;
+// 16-bit record tags: step t's tag t + 1, unique within a call (n <= kKPMaxCw * kKPMaxG)
+static_assert((long long)kKPMaxCw * kKPMaxG + 64 < 0xffff, "panel record tags are 16-bit");
+inline uint32_t kp_tag0(int64_t t) { return (uint32_t)t + 1u; }
 // second != nullptr: one launch runs p then *second (the pair's second panel, same G / cw)
 cudaError_t kp_launch(const KPParams& p, cudaStream_t s, const KPParams* second = nullptr);
 size_t kp_smem_bytes(int cw);

@@ -446,6 +446,31 @@ def test_blocked_c5_32768_vs_cusolver(mc):
     assert abs(got.log_abs - float(l_ref)) <= tol(32768, float(l_ref)), (got.log_abs, float(l_ref))
 
 
+def test_blocked_max_size_vs_cusolver(mc):
+    """The largest N the one-GPU blocked path takes -- 368 panel columns per SM, the panel's 64
+    rows in shared memory (N = 54464 on 148 SMs, 24 GB) -- vs cuSOLVER LU slogdet; one more
+    row is refused with ValueError before any work."""
+    import torch
+
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    n = 368 * min(sms, 160)
+    g = torch.Generator(device="cuda").manual_seed(n)
+    a = torch.rand((n + 1, n + 1), dtype=torch.float64, device="cuda", generator=g) * 2 - 1
+    try:
+        with pytest.raises(ValueError, match="too large"):
+            mc.logdet_blocked(a)
+        v = a[:n, :n]
+        s_ref, l_ref = torch.linalg.slogdet(v)
+        torch.cuda.empty_cache()
+        got = mc.logdet_blocked(v)
+    finally:
+        del a
+        mc._lib.load().mcnd_release_workspace()
+        torch.cuda.empty_cache()
+    assert got.sign == int(s_ref.item())
+    assert abs(got.log_abs - float(l_ref)) <= tol(n, float(l_ref)), (got.log_abs, float(l_ref))
+
+
 def test_batched_nonfinite_detected_on_device(mc):
     import torch
 
