@@ -71,7 +71,8 @@ __global__ void k2_gather_fix_kernel(double* __restrict__ ws, int64_t ld, int32_
 constexpr int kGLThreads = 256;
 __global__ void __launch_bounds__(kGLThreads) k2_gather_lcorr_kernel(double* __restrict__ ws, int64_t ld, int32_t rbase,
                                                                      int32_t nrows, const K2Gather* __restrict__ gp,
-                                                                     double* __restrict__ L, const double* __restrict__ Wp,
+                                                                     double* __restrict__ L, int64_t ldl,
+                                                                     const double* __restrict__ Wp,
                                                                      const unsigned* __restrict__ abort) {
     __shared__ double sWp[64 * 64];
     if (*(volatile const unsigned*)abort) return;
@@ -135,7 +136,7 @@ __global__ void __launch_bounds__(kGLThreads) k2_gather_lcorr_kernel(double* __r
         }
         const double n10 = (a10 + b10) + (c10 + d10), n11 = (a11 + b11) + (c11 + d11);
         if (i + stride < nrows) gather(i + stride);  // the next row's loads overlap the stores below
-        double* Lr = L + (int64_t)i * 128;
+        double* Lr = L + (int64_t)i * ldl;
         Lr[lane] = n00;
         Lr[lane + 32] = n01;
         Lr[lane + 64] = n10;
@@ -341,12 +342,14 @@ constexpr int W4_THREADS = 128;
 // U: stages per iteration of the (not unrolled) stage loop -- 2 in the persistent grid (the
 // compiler keeps the accumulators in place across the pair: 28.15 -> 28.67 TF at n = 16384,
 // scripts/micro/gemm_w5.cu), 1 for one tile per CTA (2 is 0.5 % slower there)
+// K = 256 (a group of two pairs): W rows 0..127 from W, rows 128..255 from W1 (same ldw).
 template <int K, int S, int WN = 2, int BK = MS_BK, int U = 1>
 __global__ void __launch_bounds__(64 * WN, 2) k2_gemm_w4_kernel(double* __restrict__ ws, int64_t ld, int32_t rbase,
                                                                     int32_t M, int32_t N2, const double* __restrict__ L,
                                                                     int64_t ldl, const double* __restrict__ W, int64_t ldw,
                                                                     unsigned long long* __restrict__ wit,
-                                                                    const unsigned* __restrict__ abort) {
+                                                                    const unsigned* __restrict__ abort,
+                                                                    const double* __restrict__ W1 = nullptr) {
     constexpr int KS = K / BK, LDA = BK + 4;
     constexpr int MI = 4, NJ = 8;  // warp tile 32 x 64
     constexpr int NTH = 64 * WN, BNW = 64 * WN, LDW = BNW + 4, STG = BM * LDA + BK * LDW;
@@ -369,6 +372,7 @@ __global__ void __launch_bounds__(64 * WN, 2) k2_gemm_w4_kernel(double* __restri
     int l_t = t_begin, l_ks = 0, l_slot = 0;
     const double* l_src = nullptr;  // L + row(u = 0) * ldl + kk + ca
     const double* w_src = nullptr;  // W + (kk + kb) * ldw + col
+    const double* w_src1 = nullptr; // W1 + (kk - 128 + kb) * ldw + col (K = 256)
     unsigned l_ok = 0;              // bit u: row u in range; bit 4: column chunk in range
     auto l_tile = [&]() {
         const int row0 = (l_t / ntn) * BM, col0 = (l_t % ntn) * BNW;
@@ -379,6 +383,7 @@ __global__ void __launch_bounds__(64 * WN, 2) k2_gemm_w4_kernel(double* __restri
         l_ok |= (unsigned)okc << 16;
         l_src = L + (int64_t)(row0 + ra) * ldl + ca;
         w_src = W + (int64_t)kb * ldw + (okc ? col0 + cb : 0);
+        if constexpr (K > 128) w_src1 = W1 + (int64_t)kb * ldw + (okc ? col0 + cb : 0);
     };
     auto load_next = [&]() {  // one stage -> slot l_slot, then advance
         if (l_t < t_end) {
@@ -391,7 +396,7 @@ __global__ void __launch_bounds__(64 * WN, 2) k2_gemm_w4_kernel(double* __restri
                 cp_async16_zf(ls + (ra + (NTH / (BK / 2)) * u) * LDA + ca, ok ? l_src + (int64_t)((NTH / (BK / 2)) * u) * ldl + kk : L, ok);
             }
             const bool okc = (l_ok >> 16) & 1u;
-            const double* wsrc = w_src + (int64_t)kk * ldw;
+            const double* wsrc = (K > 128 && kk >= 128) ? w_src1 + (int64_t)(kk - 128) * ldw : w_src + (int64_t)kk * ldw;
 #pragma unroll
             for (int u = 0; u < WR; ++u) cp_async16_zf(wsm + (kb + 2 * u) * LDW + cb, wsrc + (int64_t)(2 * u) * ldw, okc);
             if (++l_ks == KS) {
@@ -520,7 +525,44 @@ __global__ void __launch_bounds__(64 * WN, 2) k2_gemm_w4_kernel(double* __restri
     asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
+// ---- a group of two pairs (a, b = a + 1) applied to the rows past b's next pair as ONE
+// rank-256 update (the GEMM at K = 256 runs ~9 % faster than two K = 128 updates: per-tile
+// C traffic and pipeline fill are amortised over twice the k-steps).  With the rows still in
+// the state before a (a's column moves applied by a's gather), b's multipliers need a's update
+// of b's pivot columns:  NL_b = lcorr_b(-(x + NL_a W_a[:, P_b])) = lcorr_b(-x) + NL_a Wx,
+// Wx = lcorr_b applied to the columns of -W_a[:, P_b] (built here, 128 x 128), and W_a's
+// columns take b's column moves (fixed in place once every per-pair user of W_a is done).
+__global__ void k2_group_wx_kernel(const double* __restrict__ Wa, int64_t ldw, const K2Gather* __restrict__ gb,
+                                   const double* __restrict__ Wpb, double* __restrict__ Wx, const unsigned* __restrict__ abort) {
+    __shared__ double t[128];
+    if (*(volatile const unsigned*)abort) return;  // a singular panel left no descriptor
+    const int j = blockIdx.x, k = threadIdx.x;
+    t[k] = -Wa[(int64_t)j * ldw + gb->P[k]];
+    __syncthreads();
+    double v = t[k];
+    if (k >= 64)
+        for (int i = 0; i < 64; ++i) v = fma(t[i], Wpb[i * 64 + (k - 64)], v);
+    Wx[j * 128 + k] = v;
+}
+
+__global__ void k2_group_wfix_kernel(double* __restrict__ Wa, int64_t ldw, const K2Gather* __restrict__ gb,
+                                     const unsigned* __restrict__ abort) {
+    if (*(volatile const unsigned*)abort) return;
+    const int j = blockIdx.x, k = threadIdx.x;
+    if (k < gb->n_moved) {  // sources (dropped columns) and destinations are disjoint
+        double* const row = Wa + (int64_t)j * ldw;
+        row[gb->moved_c[k]] = row[gb->moved_src[k]];
+    }
+}
+
 }  // namespace
+
+cudaError_t k2_group_prep(double* Wa, int64_t ldw, const K2Gather* gb, const double* Wpb, double* Wx,
+                          const unsigned* abort, cudaStream_t s) {
+    k2_group_wx_kernel<<<128, 128, 0, s>>>(Wa, ldw, gb, Wpb, Wx, abort);
+    k2_group_wfix_kernel<<<128, 128, 0, s>>>(Wa, ldw, gb, abort);
+    return cudaGetLastError();
+}
 
 cudaError_t k2_gather_fix(double* ws, int64_t ld, int32_t rbase, int32_t nrows, int32_t K, const K2Gather* gp,
                           double* L, const unsigned* abort, cudaStream_t s) {
@@ -533,23 +575,23 @@ cudaError_t k2_gather_fix(double* ws, int64_t ld, int32_t rbase, int32_t nrows, 
 }
 
 cudaError_t k2_gather_lcorr(double* ws, int64_t ld, int32_t rbase, int32_t nrows, const K2Gather* gp, double* L,
-                            const double* Wp, const unsigned* abort, cudaStream_t s) {
+                            const double* Wp, const unsigned* abort, cudaStream_t s, int64_t ldl) {
     if (nrows <= 0) return cudaSuccess;
     int dev = 0;
     cudaGetDevice(&dev);
     const int sms = device_sms(dev);
     const int per = kGLThreads / 32;
     const int grid = (int)std::min<int64_t>(((int64_t)nrows + per - 1) / per, 4 * (int64_t)sms);
-    k2_gather_lcorr_kernel<<<grid, kGLThreads, 0, s>>>(ws, ld, rbase, nrows, gp, L, Wp, abort);
+    k2_gather_lcorr_kernel<<<grid, kGLThreads, 0, s>>>(ws, ld, rbase, nrows, gp, L, ldl, Wp, abort);
     return cudaGetLastError();
 }
 
 
 cudaError_t k2_gemm(double* ws, int64_t ld, int32_t rbase, int32_t M, int32_t N2, int32_t K, const double* L,
                     int64_t ldl, const double* W, int64_t ldw, double* row_wit, const unsigned* abort, cudaStream_t s,
-                    int sm_budget) {
+                    int sm_budget, const double* W1) {
     if (M <= 0 || N2 <= 0) return cudaSuccess;
-    if (K != 64 && K != 128) return cudaErrorInvalidValue;
+    if (K != 64 && K != 128 && !(K == 256 && W1)) return cudaErrorInvalidValue;
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
@@ -563,6 +605,8 @@ cudaError_t k2_gemm(double* ws, int64_t ld, int32_t rbase, int32_t M, int32_t N2
         if ((e = cudaFuncSetAttribute(k2_gemm_w4_kernel<64, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm4)) != cudaSuccess ||
             (e = cudaFuncSetAttribute(k2_gemm_w4_kernel<128, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm4)) != cudaSuccess ||
             (e = cudaFuncSetAttribute(k2_gemm_w4_kernel<128, 3, 2, MS_BK, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm4)) != cudaSuccess ||
+            (e = cudaFuncSetAttribute(k2_gemm_w4_kernel<256, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm4)) != cudaSuccess ||
+            (e = cudaFuncSetAttribute(k2_gemm_w4_kernel<256, 3, 2, MS_BK, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm4)) != cudaSuccess ||
             (e = cudaFuncSetAttribute(k2_gemm_ms_kernel<128, 1, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smn)) != cudaSuccess)
             return e;
         attr_done[dev] = true;
@@ -582,9 +626,12 @@ cudaError_t k2_gemm(double* ws, int64_t ld, int32_t rbase, int32_t M, int32_t N2
     // and a persistent grid (no per-CTA pipeline fill) is faster.  Critical-stream updates
     // (sm_budget >= 0) always run persistent.
     const int64_t tiles = (int64_t)((N2 + BN - 1) / BN) * ((M + BM - 1) / BM);
-    const bool one_tile = sm_budget < 0 && tiles <= 40 * 2 * (int64_t)sms;
+    const bool one_tile = sm_budget < 0 && tiles * K <= 40 * 2 * (int64_t)sms * 128;
     const int g4 = (int)(one_tile ? tiles : std::min<int64_t>(tiles, 2 * (int64_t)sms));
-    if (K == 64) k2_gemm_w4_kernel<64, 3><<<g4, W4_THREADS, sm4, s>>>(ws, ld, rbase, M, N2, L, ldl, W, ldw, w, abort);
+    if (K == 256) {
+        if (one_tile) k2_gemm_w4_kernel<256, 3><<<g4, W4_THREADS, sm4, s>>>(ws, ld, rbase, M, N2, L, ldl, W, ldw, w, abort, W1);
+        else k2_gemm_w4_kernel<256, 3, 2, MS_BK, 2><<<g4, W4_THREADS, sm4, s>>>(ws, ld, rbase, M, N2, L, ldl, W, ldw, w, abort, W1);
+    } else if (K == 64) k2_gemm_w4_kernel<64, 3><<<g4, W4_THREADS, sm4, s>>>(ws, ld, rbase, M, N2, L, ldl, W, ldw, w, abort);
     else if (one_tile) k2_gemm_w4_kernel<128, 3><<<g4, W4_THREADS, sm4, s>>>(ws, ld, rbase, M, N2, L, ldl, W, ldw, w, abort);
     else k2_gemm_w4_kernel<128, 3, 2, MS_BK, 2><<<g4, W4_THREADS, sm4, s>>>(ws, ld, rbase, M, N2, L, ldl, W, ldw, w, abort);
     return cudaGetLastError();

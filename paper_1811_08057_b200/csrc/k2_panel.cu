@@ -167,11 +167,13 @@ __device__ unsigned g_kp_span_n;
 #define KP_TRACE 0  // microbenchmark knob: record per-step phase timestamps of CTA 0
 #endif
 #if KP_TRACE
-__device__ unsigned long long g_kp_trace[64][12];
+__device__ unsigned long long g_kp_trace[64][16];
 __device__ unsigned long long g_kp_gt[64][kKPMaxG][4];  // per CTA (globaltimer): poll done, fetch done, published
 #define KP_GT(s, k) do { if (threadIdx.x == 0) g_kp_gt[s][blockIdx.x][k] = globaltimer(); } while (0)
 #define KP_MARK(s, k) do { if (blockIdx.x == 0 && threadIdx.x == 0) g_kp_trace[s][k] = clock64(); } while (0)
+#define KP_MARKT(s, k, t) do { if (blockIdx.x == 0 && threadIdx.x == (t)) g_kp_trace[s][k] = clock64(); } while (0)
 #else
+#define KP_MARKT(s, k, t) do { } while (0)
 #define KP_MARK(s, k) do { } while (0)
 #define KP_GT(s, k) do { } while (0)
 #endif
@@ -711,6 +713,9 @@ __global__ void __launch_bounds__(kThreads, 1) kp_panel_kernel(const KPParams p0
                 }
             }
             KP_MARK(s, 4);
+            KP_MARKT(s, 12, 64);   // E done, warp 2
+            KP_MARKT(s, 13, 480);  // E done, warp 15
+            KP_MARKT(s, 14, 32);   // D2 done, warp 1
         }
         __syncthreads();
 

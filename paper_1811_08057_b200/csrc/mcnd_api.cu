@@ -841,7 +841,18 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
     int n_chunks = 1;
     std::vector<int64_t> cr{0, n};  // chunk row boundaries
     std::vector<int> cov_of;        // per pair: last chunk covered by its side update
-    int ring = 3;
+    // groups of two pairs: the rows past the second pair's next pair take both pairs' update as
+    // ONE rank-256 GEMM (k2_group_prep, k2_gemm K = 256), only while the trailing GEMM bounds
+    // the pairs by far -- a group halves the time the side stream has for a pair's bulk rows:
+    // C5 0.895 -> 0.853 s with groups above 12000 (8000 / 16000 / 20000: 0.851 / 0.853 / 0.858),
+    // C3 30.5 -> 31.4 ms with groups everywhere.  Test hook MCND_K2_GROUP_ABOVE: the active width
+    // above which a pair may start a group (0: always).
+    const int64_t group_above = env_long("MCND_K2_GROUP_ABOVE", kK2GroupAbove);
+    const bool groups = n - 4 * b > group_above;
+    // pair slots (L, W, Wp, descriptor): a side update may read slot q while pairs q+1, q+2
+    // factor (depth-2 look-ahead); a group's update reads the slots of both its pairs while
+    // the next two factor
+    int ring = groups ? 4 : 3;
     const bool overlap = env_long("MCND_K2_OVERLAP", 1) != 0;  // test hook: 0 = serial schedule (same arithmetic)
     if (h_src && overlap && n_panels >= 8) {
         cudaPointerAttributes pa{};
@@ -874,7 +885,7 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
                 tq += std::max(t_pan, 2.0 * (double)nr * (double)(m - 2 * b) * 128.0 / 26e12) + 60e-6;
             }
             if (cov != n_chunks - 1) { n_chunks = 1; cr.assign({0, n}); cov_of.clear(); }
-            else ring = std::max(3, q_last + 3);
+            else ring = std::max(ring, q_last + 3);
         }
     }
     const bool streamed = n_chunks > 1;
@@ -902,6 +913,10 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
     const size_t o_W = take((size_t)kRing * 2 * b * ld * sizeof(double));
     const size_t o_pan = take((2 + kRing) * sizeof(K2Gather));           // gp0, gp1, gpair ring
     const size_t o_Wp = take((size_t)kRing * b * b * sizeof(double));
+    // groups: [NL_a | NL_b] of every row (absolute row index, side stream only) and each group's Wx
+    const int64_t n_groups = groups ? n_panels / 4 + 1 : 0;
+    const size_t o_Lc = take(groups ? (size_t)n * 4 * b * sizeof(double) : 0);
+    const size_t o_Wx = take((size_t)n_groups * 2 * b * 2 * b * sizeof(double));
     const size_t o_cand = take((size_t)64 * kKPMaxG * sizeof(ulonglong2));
     const size_t o_wrec = take((size_t)64 * kKPMaxG * sizeof(ulonglong2));
     const size_t o_colb = take((size_t)64 * kKPMaxG * 64 * sizeof(ulonglong2));
@@ -967,6 +982,8 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
     K2Gather* gp1 = gp0 + 1;
     K2Gather* const gpair2 = gp0 + 2;  // ring, like L and W
     double* const Wp2 = (double*)(base + o_Wp);
+    double* const Lc = (double*)(base + o_Lc);
+    double* const Wx2 = (double*)(base + o_Wx);
     K1Err* err = (K1Err*)(base + o_ctl);
     unsigned* abort = (unsigned*)(base + o_ctl + sizeof(K1Err));
     const uint32_t epoch = ++B->epoch;
@@ -1091,10 +1108,33 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
     };
     int64_t k = 0;
     int par = 0;  // ring slot
-    struct PairSlot { int64_t kb, m; int par; };
-    std::vector<PairSlot> done_pairs;  // streamed input: the pairs a late chunk catches up on
-    int cov_prev = 0;
     int64_t n_launch = 1;  // kernels launched by this call (K1 init so far)
+    // a finished unit a late chunk of streamed input catches up on: one pair (par2 < 0) or a
+    // group of two (slots par, par2; kb, m of its first pair; its Wx)
+    struct PairSlot { int64_t kb, m; int par, par2; const double* wx; };
+    std::vector<PairSlot> done_pairs;
+    // a group's update of absolute rows [r0, r0 + rows): the two gathers (each with its pair's
+    // column moves and L correction) into Lc, NL_b += NL_a Wx, then the rank-256 update
+    auto group_update = [&](const PairSlot& G, int64_t r0, int64_t rows, cudaStream_t ss, int sm_budget) -> cudaError_t {
+        if (rows <= 0) return cudaSuccess;
+        double* const Lr = Lc + r0 * 4 * b;
+        cudaError_t ee = k2_gather_lcorr(ws, ld, (int32_t)r0, (int32_t)rows, gpair2 + G.par, Lr, Wp2 + (size_t)G.par * b * b,
+                                         abort, ss, 4 * b);
+        if (ee == cudaSuccess)
+            ee = k2_gather_lcorr(ws, ld, (int32_t)r0, (int32_t)rows, gpair2 + G.par2, Lr + 2 * b,
+                                 Wp2 + (size_t)G.par2 * b * b, abort, ss, 4 * b);
+        if (ee == cudaSuccess)
+            ee = k2_gemm(Lr + 2 * b, 4 * b, 0, (int32_t)rows, (int32_t)(2 * b), 128, Lr, 4 * b, G.wx, 2 * b, nullptr, abort, ss,
+                         sm_budget);
+        if (ee == cudaSuccess)
+            ee = k2_gemm(ws, ld, (int32_t)r0, (int32_t)rows, (int32_t)(G.m - 4 * b), 256, Lr, 4 * b,
+                         Wb + (size_t)G.par * 2 * b * ld, ld, wit, abort, ss, sm_budget, Wb + (size_t)G.par2 * 2 * b * ld);
+        n_launch += 4;
+        return ee;
+    };
+    bool grp_open = false;  // the previous pair started a group
+    PairSlot grp{};
+    int cov_prev = 0;
     // debug timeline (MCND_DEBUG_TIMELINE=1): an event after every critical-stream step,
     // per-label device time printed to stderr at the end of the call
     const long dbg_tl = env_long("MCND_DEBUG_TIMELINE", 0);  // 2: every step
@@ -1128,6 +1168,10 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
                 ++n_launch;
                 for (const PairSlot& ps : done_pairs) {
                     if (ee != cudaSuccess) break;
+                    if (ps.par2 >= 0) {
+                        ee = group_update(ps, cr[c], cr[c + 1] - cr[c], side, -1);
+                        continue;
+                    }
                     const int64_t r0 = cr[c] - (ps.kb + 2 * b);  // rows relative to that pair's trailing block
                     double* const Lp = Lb + (size_t)ps.par * std::max<int64_t>(n, 1) * 2 * b + r0 * 2 * b;
                     ee = k2_gather_lcorr(ws, ld, (int32_t)cr[c], (int32_t)(cr[c + 1] - cr[c]), gpair2 + ps.par, Lp,
@@ -1160,14 +1204,23 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
             if (e == cudaSuccess) e = join_rows();  // the critical rows final for the previous pair
             mark("join");
             const int32_t nr = (int32_t)(n - kb - 2 * b);
-            // rows the next unit factors: a pair (128), a last single panel (64), or the tail (all)
-            const int64_t k2 = k + 2;
-            // (serial schedule, MCND_K2_OVERLAP=0: everything on the critical stream)
-            int64_t ahead = (k2 + 1 < n_panels) ? 2 * b : (k2 < n_panels ? b : nr);
-            if (!overlap) ahead = nr;
+            // rows the next unit factors (a pair: 128, a last single panel: 64, or the tail: all)
+            // and, when the next unit is a pair, the rows of the unit after it
+            const int64_t k2 = k + 2, k4 = k + 4;
+            const int64_t unit1 = (k2 + 1 < n_panels) ? 2 * b : (k2 < n_panels ? b : nr);
+            const int64_t unit2 = (k2 + 1 < n_panels) ? ((k4 + 1 < n_panels) ? 2 * b : (k4 < n_panels ? b : nr - unit1)) : 0;
+            // groups: this pair (a) starts one when the next unit is a pair (b) and rows are left
+            // past b's next unit; those rows take a and b together at b (group_update)
+            const bool g_end = grp_open;
+            const bool g_start = groups && !g_end && m > group_above && k + 3 < n_panels && unit1 + unit2 < nr;
+            // rows this pair updates on its own; the rest is deferred (g_start) or the group's (g_end)
+            const int64_t own = g_start ? unit1 + unit2 : (g_end ? unit1 : nr);
+            // (serial schedule, MCND_K2_OVERLAP=0: everything on the critical stream, same arithmetic)
+            const int64_t ahead = overlap ? unit1 : own;
             // gather + L correction + trailing update of `rows` rows starting at row offset r0
             // (relative to the pair's trailing block) on stream `ss`
             auto trailing = [&](int64_t r0, int64_t rows, cudaStream_t ss, int sm_budget) -> cudaError_t {
+                if (rows <= 0) return cudaSuccess;
                 double* const Lr = Lq + r0 * 2 * b;
                 // gather + NL[:, 64:128] += NL[:, 0:64] * (-Wp) in one pass, then the DMMA update
                 cudaError_t ee = k2_gather_lcorr(ws, ld, (int32_t)(kb + 2 * b + r0), (int32_t)rows, gpair, Lr, Wp, abort, ss);
@@ -1176,12 +1229,23 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
                     ee = k2_gemm(ws, ld, (int32_t)(kb + 2 * b + r0), (int32_t)rows, (int32_t)(m - 2 * b), 128, Lr, 2 * b,
                                  Wq, ld, wit, abort, ss, sm_budget);
                 if (ss == st) mark("trailing");
+                n_launch += 2;
                 return ee;
             };
-            // side stream: W, Wp and the gather descriptor are final once pair prep is done;
-            // started only after the critical rows' update, so the side kernels do not take
-            // the SMs the critical ones need (C3 33.8 -> 33.2 ms)
-            if (streamed && cov_q > cov_prev && ahead >= nr) {  // no side work: new rows caught up first
+            PairSlot gq{};
+            if (g_end) {
+                gq = grp;
+                gq.par2 = par;
+            }
+            // the group's preparation (Wx from W_a, then b's column moves into W_a): after every
+            // per-pair use of W_a (the critical rows of a and its part A precede it in stream order)
+            auto group_prep = [&](cudaStream_t ss) -> cudaError_t {
+                n_launch += 2;
+                return k2_group_prep(Wb + (size_t)gq.par * 2 * b * ld, ld, gpair, Wp, const_cast<double*>(gq.wx), abort, ss);
+            };
+            const int64_t r_end = std::min<int64_t>(nr, cov_end - (kb + 2 * b));  // resident rows
+            if (streamed && cov_q > cov_prev && ahead >= nr) {
+                // no side work: new rows caught up first
                 if (e == cudaSuccess) e = cudaEventRecord(B->ev_a, st);
                 if (e == cudaSuccess) e = cudaStreamWaitEvent(side, B->ev_a, 0);
                 if (e == cudaSuccess) e = catch_up();
@@ -1189,36 +1253,46 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
                 side_pending = (e == cudaSuccess);
                 if (e == cudaSuccess) e = join_side();
             }
-            if (e == cudaSuccess) e = trailing(0, ahead, st, 0);  // the critical rows first
-            if (e == cudaSuccess && ahead < nr) e = cudaEventRecord(B->ev_a, st);
-            if (e == cudaSuccess && ahead < nr) {
-                e = cudaStreamWaitEvent(side, B->ev_a, 0);
-                // part A: the rows of the unit after next (a pair: 128, a single panel: 64, else
-                // everything left) when the next unit is a pair; the next pair waits for it alone
-                const int64_t k4 = k2 + 2;
-                const int64_t ahead2 = (k2 + 1 < n_panels)
-                                           ? ((k4 + 1 < n_panels) ? 2 * b : (k4 < n_panels ? b : nr - ahead))
-                                           : 0;
-                if (ahead2 > 0 && ahead2 < nr - ahead) {
+            // the critical rows first (serial: every row this pair updates on its own)
+            if (e == cudaSuccess) e = trailing(0, ahead, st, 0);
+            if (!overlap) {
+                if (g_end && e == cudaSuccess) e = group_prep(st);
+                if (g_end && e == cudaSuccess) e = group_update(gq, kb + 2 * b + own, nr - own, st, 0);
+            } else if (ahead < nr) {
+                // side stream: W, Wp and the gather descriptor are final once the pair prep is done;
+                // started only after the critical rows' update, so the side kernels do not take the
+                // SMs the critical ones need
+                if (e == cudaSuccess) e = cudaEventRecord(B->ev_a, st);
+                if (e == cudaSuccess) e = cudaStreamWaitEvent(side, B->ev_a, 0);
+                if (g_end && e == cudaSuccess) e = group_prep(side);
+                // part A: the rows of the unit after next, when the next unit is a pair; the next
+                // pair waits for it alone.  Part B: the rest (deferred when this pair starts a group)
+                const int64_t a_rows = unit2 < nr - unit1 ? unit2 : 0;
+                if (a_rows > 0) {
                     // (defensive: part A's rows not resident yet -> catch up first)
-                    if (e == cudaSuccess && streamed && kb + 2 * b + ahead + ahead2 > cr[cov_prev + 1]) e = catch_up();
-                    if (e == cudaSuccess) e = trailing(ahead, ahead2, side, -1);
+                    if (e == cudaSuccess && streamed && kb + 2 * b + unit1 + a_rows > cr[cov_prev + 1]) e = catch_up();
+                    if (e == cudaSuccess)
+                        e = g_end ? group_update(gq, kb + 2 * b + unit1, a_rows, side, -1) : trailing(unit1, a_rows, side, -1);
                     if (e == cudaSuccess) e = cudaEventRecord(B->ev_c, side);
                     sideA_pending = (e == cudaSuccess);
-                    if (e == cudaSuccess && streamed) e = catch_up();
-                    const int64_t rows_b = std::min<int64_t>(nr, cov_end - (kb + 2 * b)) - ahead - ahead2;
-                    if (e == cudaSuccess && rows_b > 0) e = trailing(ahead + ahead2, rows_b, side, -1);
-                    n_launch += 2;
-                } else {
-                    if (e == cudaSuccess && streamed) e = catch_up();
-                    if (e == cudaSuccess) e = trailing(ahead, std::min<int64_t>(nr, cov_end - (kb + 2 * b)) - ahead, side, -1);
+                }
+                if (e == cudaSuccess && streamed) e = catch_up();
+                if (!g_start) {
+                    const int64_t r_b = unit1 + a_rows;
+                    if (e == cudaSuccess)
+                        e = g_end ? group_update(gq, kb + 2 * b + r_b, r_end - r_b, side, -1) : trailing(r_b, r_end - r_b, side, -1);
                 }
                 if (e == cudaSuccess) e = cudaEventRecord(B->ev_b, side);
                 side_pending = (e == cudaSuccess);
-                n_launch += 3;
             }
-            n_launch += 3;  // the panel pair, gather + L correction, the critical update
-            if (streamed) done_pairs.push_back({kb, m, par});
+            ++n_launch;  // the panel pair
+            if (g_start) {
+                grp = PairSlot{kb, m, par, -1, Wx2 + (size_t)(k / 4) * 4 * b * b};
+                grp_open = true;
+            } else {
+                grp_open = false;
+                if (streamed) done_pairs.push_back(g_end ? gq : PairSlot{kb, m, par, -1, nullptr});
+            }
             k += 2;
             par = (par + 1) % kRing;
         } else {

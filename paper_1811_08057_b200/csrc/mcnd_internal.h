@@ -86,6 +86,7 @@ size_t k1_smem_bytes(int chunk);
 
 // ---- K2: blocked rank-b condensation (k2_blocked.cu) ----
 constexpr int kK2B = 64;  // panel height b (rank of the trailing update)
+constexpr long kK2GroupAbove = 12000;  // pairs grouped into rank-256 updates above this active width
 // Gather descriptor of a trailing update: the K multiplier columns P (positions
 // in the layout the trailing rows are in) and the final columns whose source
 // column moved (composition of the column exchanges of condense.py:104-107).
@@ -183,7 +184,11 @@ cudaError_t k2_gather_fix(double* ws, int64_t ld, int32_t rbase, int32_t nrows, 
                           double* L, const unsigned* abort, cudaStream_t s);
 // Pair gather (K = 128) fused with the L correction NL[:, 64:128] += NL[:, 0:64] * Wp.
 cudaError_t k2_gather_lcorr(double* ws, int64_t ld, int32_t rbase, int32_t nrows, const K2Gather* gp, double* L,
-                            const double* Wp, const unsigned* abort, cudaStream_t s);
+                            const double* Wp, const unsigned* abort, cudaStream_t s, int64_t ldl = 128);
+// a group of two pairs (a, b): Wx = lcorr_b(-W_a[:, P_b]) (128 x 128), then b's column moves
+// applied to W_a in place (k2_blocked.cu)
+cudaError_t k2_group_prep(double* Wa, int64_t ldw, const K2Gather* gb, const double* Wpb, double* Wx,
+                          const unsigned* abort, cudaStream_t s);
 
 // C[M x N2] (rows rbase.. of ws) += NL[M x K] W[K x N2], K in {64, 128}; NL (= -L, as written by
 // k2_gather_fix) row stride ldl;
@@ -191,7 +196,7 @@ cudaError_t k2_gather_lcorr(double* ws, int64_t ld, int32_t rbase, int32_t nrows
 // sm_budget > 0: at most that many SMs, one "fat" CTA each (the rest stay free).
 cudaError_t k2_gemm(double* ws, int64_t ld, int32_t rbase, int32_t M, int32_t N2, int32_t K, const double* L,
                     int64_t ldl, const double* W, int64_t ldw, double* row_wit, const unsigned* abort, cudaStream_t s,
-                    int sm_budget = 0);
+                    int sm_budget = 0, const double* W1 = nullptr);
 
 // nonfinite (nullable, device): set to nonzero if any input entry is NaN/Inf.
 cudaError_t k3_launch(const double* a, int64_t batch, int64_t n, int64_t stride, bool fast,

@@ -41,7 +41,7 @@ int main(int argc, char** argv) {
 #ifdef KP_OLD
     p.wrec = wrec;
 #else
-    p.lastc = wrec;
+    p.wrec = wrec;
 #endif
     p.err = err; p.timeout_ns = 5000000000ull;
     if (r1) {  // second panel of a pair: the r1 prologue (rank-64 update of the rows)
@@ -84,7 +84,7 @@ int main(int argc, char** argv) {
         printf("W checksum %016llx pivots %016llx piv0 %.17g l0 %d\n", hsum, psum, rr[0].v, rr[0].l);
     }
 #if KP_TRACE
-    unsigned long long tr[64][12];
+    unsigned long long tr[64][16];
     cudaMemcpyFromSymbol(tr, g_kp_trace, sizeof(tr));
     double p8 = 0, p9 = 0, p1 = 0, p3 = 0, p5 = 0, p6 = 0, p2 = 0, p4 = 0, tot = 0;
     for (int s = 1; s < 62; ++s) {
@@ -94,6 +94,15 @@ int main(int argc, char** argv) {
     }
     printf("per step (cycles, CTA 0): poll %.0f reduce %.0f ->sync %.0f D1loop %.0f D1red %.0f combine+put %.0f ->sync %.0f D2/E %.0f | total %.0f\n",
            p8 / 61, p9 / 61, p1 / 61, p3 / 61, p5 / 61, p6 / 61, p2 / 61, p4 / 61, tot / 61);
+    {
+        double e2 = 0, e15 = 0, d2w1 = 0, w0bar = 0;
+        for (int s = 1; s < 62; ++s) {
+            e2 += (double)(tr[s][12] - tr[s][2]); e15 += (double)(tr[s][13] - tr[s][2]); d2w1 += (double)(tr[s][14] - tr[s][2]);
+            w0bar += (double)(tr[s + 1][10] - tr[s][2]);
+        }
+        printf("  from E start (cycles): E done warp 2 %.0f, warp 15 %.0f, D2 done warp 1 %.0f, warp 0 at the barrier %.0f\n",
+               e2 / 61, e15 / 61, d2w1 / 61, w0bar / 61);
+    }
     printf("  prologue %llu cycles, loop %llu, W %llu\n", tr[0][9] - tr[0][8], tr[0][10] - tr[0][9], tr[0][11] - tr[0][10]);
     {   // cross-CTA view (globaltimer ns): per step, the last publish -> each CTA's poll completion
         static unsigned long long gt[64][kKPMaxG][4];

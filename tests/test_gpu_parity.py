@@ -353,14 +353,22 @@ def test_large_n_chunked_vs_cusolver(mc):
 
 
 # ---------------------------------------------------------------- K2 blocked
+# MCND_K2_GROUP_ABOVE=0: pairs grouped into rank-256 updates at every size (by default only
+# above an active width of 12000, i.e. C5), so the group path is exercised at small N
+GROUPS = [None, 0]
+
+
+@pytest.mark.parametrize("grp", GROUPS)
 @pytest.mark.parametrize("tail", [2, 100, 1024])
-def test_blocked_vs_oracle(mc, env_knob, tail):
+def test_blocked_vs_oracle(mc, env_knob, tail, grp):
     """Blocked rank-64 condensation: sign exact, log|det| within tolerance, and
     (well-conditioned inputs) the same pivot columns as the reference."""
     from oracle import mcnd_oracle as O
     from paper_1811_08057_b200 import matrix as M
 
     env_knob("MCND_K2_TAIL", tail)
+    if grp is not None:
+        env_knob("MCND_K2_GROUP_ABOVE", grp)
     cases = [np.random.default_rng(1).uniform(-1, 1, (300, 300)),
              np.random.default_rng(2).standard_normal((257, 257)),
              M.config_spd(320, 3),
@@ -393,8 +401,9 @@ def test_blocked_wide_panel_chunks(mc, env_knob, maxg):
     assert got[0].sign == o.sign and abs(got[0].log_abs - o.log_abs) <= tol(2000, o.log_abs)
 
 
+@pytest.mark.parametrize("grp", GROUPS)
 @pytest.mark.parametrize("n", [4000, 8000])
-def test_blocked_lookahead_identical(mc, env_knob, n):
+def test_blocked_lookahead_identical(mc, env_knob, n, grp):
     """The look-ahead schedule (trailing update split over two streams, side GEMM
     concurrent with the next panels) performs exactly the serial schedule's
     arithmetic: identical pivots, repeatedly (catches timing-dependent races
@@ -403,6 +412,8 @@ def test_blocked_lookahead_identical(mc, env_knob, n):
     from paper_1811_08057_b200 import matrix as M
 
     a = torch.from_numpy(M.config_uniform(n, 3)).cuda()
+    if grp is not None:
+        env_knob("MCND_K2_GROUP_ABOVE", grp)
     env_knob("MCND_K2_OVERLAP", 0)
     ref = mc.logdet_blocked(a, return_pivots=True)
     env_knob("MCND_K2_OVERLAP", 1)
@@ -499,12 +510,15 @@ def test_blocked_odd_sizes_vs_cusolver(mc, n):
     assert abs(got.log_abs - float(l_ref)) <= tol(n, float(l_ref))
 
 
+@pytest.mark.parametrize("grp", GROUPS)
 @pytest.mark.parametrize("dup_row", [5, 1500, 2990])
-def test_blocked_singular_mid_panel_and_tail(mc, dup_row):
+def test_blocked_singular_mid_panel_and_tail(mc, env_knob, dup_row, grp):
     """A row duplicated at a position handled by a panel early, mid-matrix, or in the
     K1 tail: SINGULAR (condense.py:90 / 153-158), every later launch aborted, no hang;
     the same handle (workspace) then serves a regular matrix."""
     n = 3000
+    if grp is not None:
+        env_knob("MCND_K2_GROUP_ABOVE", grp)
     a = np.random.default_rng(dup_row).uniform(-1, 1, (n, n))
     a[dup_row] = a[dup_row // 2]
     assert mc.logdet_blocked(a) == mc.SINGULAR
@@ -515,8 +529,8 @@ def test_blocked_singular_mid_panel_and_tail(mc, dup_row):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("n", [1500, 4000, 8000])
-def test_blocked_streamed_host_input_identical(mc, n):
+@pytest.mark.parametrize("n,grp", [(1500, None), (4000, None), (8000, None), (4000, 0), (8000, 0)])
+def test_blocked_streamed_host_input_identical(mc, env_knob, n, grp):
     """A pinned host matrix is streamed in row chunks while the first pairs run (late
     chunks caught up on the side stream, csrc/mcnd_api.cu blocked_dev): bitwise the
     result and pivots of the resident-matrix call; a pageable host matrix (one copy,
@@ -524,6 +538,8 @@ def test_blocked_streamed_host_input_identical(mc, n):
     import torch
     from paper_1811_08057_b200 import matrix as M
 
+    if grp is not None:
+        env_knob("MCND_K2_GROUP_ABOVE", grp)
     host = M.config_uniform(n, 3)
     ref = mc.logdet_blocked(torch.from_numpy(host).cuda(), return_pivots=True)
     pinned = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
