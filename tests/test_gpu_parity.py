@@ -645,7 +645,8 @@ def test_mc_parallel_comm_timings(mc):
     assert host > dev  # the 32 MB H2D copy is part of the host call's scatter
 
 
-def test_blocked_pivot_sequence_vs_oracle(mc):
+@pytest.mark.parametrize("grp", GROUPS)
+def test_blocked_pivot_sequence_vs_oracle(mc, env_knob, grp):
     """logdet_blocked with a caller pivot order (condense.py:147-152): rows gathered into that
     order on the device, sign corrected by the permutation parity; within tolerance of the
     oracle run in the same order, invalid sequences behave like logdet_condensation."""
@@ -653,6 +654,8 @@ def test_blocked_pivot_sequence_vs_oracle(mc):
 
     from oracle import mcnd_oracle as O
 
+    if grp is not None:
+        env_knob("MCND_K2_GROUP_ABOVE", grp)
     for n, seed in ((300, 1), (1100, 2)):
         a = np.random.default_rng(seed).uniform(-1, 1, (n, n))
         seq = list(np.random.default_rng(seed + 5).permutation(n))[: n - 1]
