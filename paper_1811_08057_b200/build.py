@@ -10,8 +10,8 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libmcnd_b200.so")
-SOURCES = ["k1_condense.cu", "k2_blocked.cu", "k2_panel.cu", "k3_batched.cu", "mcnd_api.cu"]
-HEADERS = ["mcnd_internal.h"]
+SOURCES = ["k1_condense.cu", "k2_blocked.cu", "k2_panel.cu", "k2_cpanel.cu", "k3_batched.cu", "mcnd_api.cu"]
+HEADERS = ["mcnd_internal.h", "k2_pair_prep.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

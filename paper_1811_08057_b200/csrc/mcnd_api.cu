@@ -59,6 +59,22 @@ long env_long(const char* name, long dflt) {
     return std::strtol(v, nullptr, 10);
 }
 
+// One panel (second == nullptr) or both panels of a pair in one launch: the cluster-resident
+// kernel (k2_cpanel.cu) while the panel fits one thread-block cluster (active width <= 16 x 352
+// columns), the column-distributed kernel (k2_panel.cu) above.  Test hooks: MCND_KC=0 keeps the
+// column-distributed kernel everywhere, MCND_KC_MAXM lowers the cluster kernel's range.
+cudaError_t panel_launch(KPParams q0, cudaStream_t st, KPParams* q1) {
+    int cw = 0;
+    const int C = (env_long("MCND_KC", 1) != 0 && q0.m <= env_long("MCND_KC_MAXM", 1L << 30)) ? kc_plan(q0.m, &cw) : 0;
+    if (C > 0) {
+        q0.G = C; q0.cw = cw;
+        if (q1) { q1->G = C; q1->cw = cw; }
+        return kc_launch(q0, st, q1);
+    }
+    if (q0.cw > kKPMaxCw) return cudaErrorInvalidValue;
+    return kp_launch(q0, st, q1);
+}
+
 // ---- cached device/pinned buffers (one set per device; calls are serialised) ----
 struct Buffers {
     int device = -1;
@@ -1076,9 +1092,7 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
         return q;
     };
     auto run_kp = [&](int64_t kb, K2Gather* gp, double* Wout) -> cudaError_t {
-        const KPParams q = kp_at(kb, gp, Wout, n - kb);
-        if (q.cw > kKPMaxCw) return cudaErrorInvalidValue;
-        return kp_launch(q, st);
+        return panel_launch(kp_at(kb, gp, Wout, n - kb), st, nullptr);
     };
     // Panels go in pairs: panel k, then its update of panel k+1's 64 rows, panel
     // k+1, and ONE rank-128 trailing update (half the C traffic of two rank-64
@@ -1198,7 +1212,7 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
                 q1.pp_g0 = gp0; q1.pp_W = Wq; q1.pp_ldw = ld; q1.pp_Wp = Wp; q1.pp_gpair = gpair; q1.pp_m = (int32_t)m;
                 q1.pp_bar = bars + kb / (2 * b);
                 q1.half_bar = bars + kPPBars + kb / (2 * b);
-                e = kp_launch(q0, st, &q1);  // (checks the chunk width)
+                e = panel_launch(q0, st, &q1);  // (checks the chunk width)
             }
             mark("kp_pair");
             if (e == cudaSuccess) e = join_rows();  // the critical rows final for the previous pair
@@ -1618,7 +1632,7 @@ int mg_pair(MgHandle* h, int64_t lr0, int64_t t, int64_t m, double* W, int64_t l
         kp1.pp_g0 = gp0; kp1.pp_W = W; kp1.pp_ldw = ldw; kp1.pp_Wp = Wp; kp1.pp_gpair = gpair; kp1.pp_m = (int32_t)m;
         kp1.pp_bar = bars + pair;
         kp1.half_bar = bars + kPPBars + pair;
-        e = kp_launch(kp, st, &kp1);
+        e = panel_launch(kp, st, &kp1);
     } else {
         e = kp_launch(kp, st);
         if (e == cudaSuccess) {

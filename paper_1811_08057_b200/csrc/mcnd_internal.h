@@ -174,6 +174,16 @@ inline uint32_t kp_tag0(int64_t t) { return (uint32_t)t + 1u; }
 // second != nullptr: one launch runs p then *second (the pair's second panel, same G / cw)
 cudaError_t kp_launch(const KPParams& p, cudaStream_t s, const KPParams* second = nullptr);
 size_t kp_smem_bytes(int cw);
+// Cluster-resident panel kernel (k2_cpanel.cu): the 64 x m panel in the shared memory of ONE
+// thread-block cluster (G = cluster size <= 16 CTAs, cw columns each), pivots exchanged over
+// distributed shared memory in micro-panels of 8 rows.  Same parameters and outputs as kp_launch
+// (cand / wrec / lastbuf unused, colbuf is a small scratch).
+constexpr int kKCMaxC = 16;
+constexpr int kKCMaxCw = 352;  // 64 x 352 doubles = 176 KB dynamic + 48 KB static shared memory
+// cluster size for active width m and its chunk width; 0: m is outside the cluster kernel's range
+int kc_plan(int64_t m, int* cw_out);
+cudaError_t kc_launch(const KPParams& p, cudaStream_t s, const KPParams* second = nullptr);
+size_t kc_smem_bytes(int cw);
 // debug: (entry, exit) globaltimer of the panel launches since the last call; returns the count
 int kp_debug_spans(unsigned long long* out, int max_spans);
 
