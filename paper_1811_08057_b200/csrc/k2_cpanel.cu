@@ -56,6 +56,11 @@ __device__ unsigned long long g_kc_tb[8][8];
 #define KC_MARKB(j, k) do { } while (0)
 #endif
 
+// Span log of the panels (CTA 0: globaltimer at the start and end of every panel), read by
+// mcnd_debug_kp_spans() together with the column-distributed kernel's
+__device__ unsigned long long g_kc_span[4096][2];
+__device__ unsigned g_kc_span_n;
+
 __device__ __forceinline__ unsigned long long globaltimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -65,18 +70,6 @@ __device__ __forceinline__ unsigned long long abs_bits(double x) {
     return (unsigned long long)__double_as_longlong(x) & 0x7fffffffffffffffull;
 }
 __device__ __forceinline__ unsigned hi_abs(double x) { return (unsigned)(abs_bits(x) >> 32); }
-
-// x / v correctly rounded from r = RN(1/v) (Markstein; see k2_panel.cu)
-__device__ __forceinline__ double div_rn_rcp(double x, double v, double r) {
-    const unsigned ex = (unsigned)(((unsigned long long)__double_as_longlong(x) >> 52) & 0x7ffu);
-    const unsigned ev = (unsigned)(((unsigned long long)__double_as_longlong(v) >> 52) & 0x7ffu);
-    if (ex - 523u < 1000u && ev - 523u < 1000u) {
-        const double q0 = __dmul_rn(x, r);
-        const double e = __fma_rn(-q0, v, x);
-        return __fma_rn(e, r, q0);
-    }
-    return __ddiv_rn(x, v);
-}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ uint32_t mapa(uint32_t addr, uint32_t cta) {
@@ -183,10 +176,10 @@ struct KCChain {
 };
 
 // One micro-panel (rows r0 .. r0+7 of the panel) on the 4 chain warps: thread t owns the columns
-// t, t + 128, ... (NC of them) of the chunk, their 8 entries in registers.  At exit the rows'
+// NC t .. NC t + NC - 1 of the chunk, their 8 entries in registers.  At exit the rows'
 // slots in the chunk hold W8 = T8^{-1} U8 (the micro-panel's rows of W).
 // One micro-panel (rows r0 .. r0+7 of the panel) on the 4 chain warps: thread t owns the columns
-// t, t + 128, ... (NC of them) of the chunk, their 8 entries in registers.  At exit the rows'
+// NC t .. NC t + NC - 1 of the chunk, their 8 entries in registers.  At exit the rows'
 // slots in the chunk hold W8 = T8^{-1} U8 (the micro-panel's rows of W).  Roles besides the
 // common path: warp 0 sends the CTA's record, warp 1 keeps T8, warp 2 runs the witness test and
 // writes the pivot records.
@@ -200,10 +193,12 @@ __device__ __forceinline__ void kc_chain(KCSmem& sm, double* __restrict__ S, con
     bool own[NC];
 #pragma unroll
     for (int u = 0; u < NC; ++u) {
-        own[u] = t + kChainThreads * u < cc.wc;
-        col[u] = lo + t + kChainThreads * u;
+        // NC CONSECUTIVE columns per thread: lane order = column order, so "ties -> lowest column"
+        // is "lowest lane" at every level of the argmax (no conditional tie-break code)
+        own[u] = NC * t + u < cc.wc;
+        col[u] = lo + NC * t + u;
 #pragma unroll
-        for (int i = 0; i < kR; ++i) x[u][i] = own[u] ? S[(r0 + i) * cw + t + kChainThreads * u] : 0.0;
+        for (int i = 0; i < kR; ++i) x[u][i] = own[u] ? S[(r0 + i) * cw + NC * t + u] : 0.0;
     }
     // a row's state at its micro-panel start joins its witness (with its state at the panel load;
     // the states in between are not tracked: witnesses only matter near singularity)
@@ -237,20 +232,16 @@ __device__ __forceinline__ void kc_chain(KCSmem& sm, double* __restrict__ S, con
         }
         const bool has = bc != INT_MAX;
         KC_MARK(s, 13);
+        // exact 64-bit argmax, branch-free: redux on the high words, on the low words among the top,
+        // ballot; the lowest lane of the ballot is the lowest column
         const unsigned bh = has ? (unsigned)(bits >> 32) : 0u, bl = (unsigned)bits;
         const unsigned mh = __reduce_max_sync(kFull, bh);
-        unsigned ball = __ballot_sync(kFull, has && bh == mh);
-        if (__popc(ball) > 1) {
-            const bool c1 = has && bh == mh;
-            const unsigned ml = __reduce_max_sync(kFull, c1 ? bl : 0u);
-            const bool c2 = c1 && bl == ml;
-            const unsigned cm = __reduce_min_sync(kFull, c2 ? (unsigned)bc : 0xffffffffu);
-            ball = __ballot_sync(kFull, c2 && (unsigned)bc == cm);
-        }
+        const unsigned ml = __reduce_max_sync(kFull, (has && bh == mh) ? bl : 0u);
+        const unsigned ball = __ballot_sync(kFull, has && bh == mh && bl == ml);
         KC_MARK(s, 14);
         {
-            // the winner lane (lane 0 when the warp has no active column: bc = INT_MAX there or its
-            // record is invalid) publishes {|candidate|, column} and the column's 8 entries
+            // the winner lane publishes {|candidate|, column} and the column's 8 entries (a warp
+            // without active columns: an invalid record from lane 0)
             const int wl = ball ? (int)(__ffs(ball) - 1) : 0;
             if (lane == wl) {
                 const uint32_t aw = sb + KC_OFF(wrec) + warp * 16, ax = sb + KC_OFF(wx) + warp * (kR * 8);
@@ -262,13 +253,16 @@ __device__ __forceinline__ void kc_chain(KCSmem& sm, double* __restrict__ S, con
                         for (int k = 0; k < kR; k += 2) sts_v2(ax + k * 8, d2u(x[u][k]), d2u(x[u][k + 1]));
                     }
             }
-        }
+            // the owner of the last active column publishes it
+            if (ms - 1 - lo >= NC * t && ms - 1 - lo < NC * t + NC) {
 #pragma unroll
-        for (int u = 0; u < NC; ++u)
-            if (own[u] && col[u] == ms - 1) {
+                for (int u = 0; u < NC; ++u)
+                    if (own[u] && col[u] == ms - 1) {
 #pragma unroll
-                for (int k = 0; k < kR; k += 2) sts_v2(sb + KC_OFF(xl) + k * 8, d2u(x[u][k]), d2u(x[u][k + 1]));
+                        for (int k = 0; k < kR; k += 2) sts_v2(sb + KC_OFF(xl) + k * 8, d2u(x[u][k]), d2u(x[u][k + 1]));
+                    }
             }
+        }
         KC_MARK(s, 15);
         asm volatile("bar.sync 1, %0;" ::"n"(kChainThreads) : "memory");
         KC_MARK(s, 1);
@@ -280,17 +274,12 @@ __device__ __forceinline__ void kc_chain(KCSmem& sm, double* __restrict__ S, con
             const unsigned wh = (unsigned)(rw.x >> 32), wlo = (unsigned)rw.x;
             const bool wok = (unsigned)rw.y != 0x7fffffffu;
             const unsigned wmh = __reduce_max_sync(kFull, wok ? wh : 0u);
-            unsigned wbal = __ballot_sync(kFull, wok && wh == wmh);
-            if (__popc(wbal) > 1) {
-                const bool c1 = wok && wh == wmh;
-                const unsigned wml = __reduce_max_sync(kFull, c1 ? wlo : 0u);
-                const bool c2 = c1 && wlo == wml;
-                const unsigned cm = __reduce_min_sync(kFull, c2 ? (unsigned)rw.y : 0xffffffffu);
-                wbal = __ballot_sync(kFull, c2 && (unsigned)rw.y == cm);
-            }
+            const unsigned wml = __reduce_max_sync(kFull, (wok && wh == wmh) ? wlo : 0u);
+            const unsigned wbal = __ballot_sync(kFull, wok && wh == wmh && wlo == wml);
             const int ww = wbal ? (int)(__ffs(wbal) - 1) : 0;
-            const unsigned long long b0 = __shfl_sync(kFull, rw.x, ww);
-            const int c0 = (int)__shfl_sync(kFull, (unsigned)rw.y, ww);
+            const ulonglong2 rbest = lds_v2(sb + KC_OFF(wrec) + ww * 16);
+            const unsigned long long b0 = rbest.x;
+            const int c0 = (int)(unsigned)rbest.y;
             KC_MARK(s, 8);
             if (cc.dst < C) {
                 // words: 0 value, 1 col | maxhi << 32, 2..9 the column's 8 entries
@@ -361,18 +350,16 @@ __device__ __forceinline__ void kc_chain(KCSmem& sm, double* __restrict__ S, con
             const unsigned long long b = r.x & 0x7fffffffffffffffull;
             const unsigned h2 = ok ? (unsigned)(b >> 32) : 0u, l2 = (unsigned)b;
             const unsigned mh2 = __reduce_max_sync(kFull, h2);
-            unsigned bal2 = __ballot_sync(kFull, ok && h2 == mh2);
-            if (__popc(bal2) > 1) {
-                const unsigned ml2 = __reduce_max_sync(kFull, (ok && h2 == mh2) ? l2 : 0u);
-                bal2 = __ballot_sync(kFull, ok && h2 == mh2 && l2 == ml2);
-            }
+            const unsigned ml2 = __reduce_max_sync(kFull, (ok && h2 == mh2) ? l2 : 0u);
+            const unsigned bal2 = __ballot_sync(kFull, ok && h2 == mh2 && l2 == ml2);
             const int gw = bal2 ? (int)(__ffs(bal2) - 1) : 0;
             KC_MARK(s, 12);
-            v = __shfl_sync(kFull, vl, gw);
-            l = __shfl_sync(kFull, c, gw);
-            rcp = __shfl_sync(kFull, rl, gw);
-            hi1 = hl ? (unsigned)(r.y >> 32) : 0u;
             arec = arcv + gw * (kRecWords * 8);
+            const ulonglong2 rbest = lds_v2(arec);
+            rcp = __shfl_sync(kFull, rl, gw);
+            v = u2d(rbest.x);
+            l = (int)(unsigned)rbest.y;
+            hi1 = hl ? (unsigned)(r.y >> 32) : 0u;
         }
         KC_MARK(s, 4);
         // the multipliers of rows > i (the winner column's entries), the last column if I take it
@@ -404,22 +391,46 @@ __device__ __forceinline__ void kc_chain(KCSmem& sm, double* __restrict__ S, con
             }
             dead = dead || singular;
         }
-        // ---- the step in registers: column exchange, row i scaled, rows > i updated
+        // ---- the step in registers: column exchange, row i scaled, rows > i updated.  Dropped and
+        //      foreign columns are computed along (their values are never used): no per-column
+        //      branches; one branch picks the division: x / v correctly rounded from rcp = RN(1/v)
+        //      (Markstein: q0 = RN(x rcp), e = x - q0 v exact, q = RN(q0 + e rcp); operands in
+        //      [2^-500, 2^500), as k2_panel.cu) when every live operand of the thread is in range,
+        //      IEEE division otherwise
+        if (l != ms - 1 && l - lo >= NC * t && l - lo < NC * t + NC) {
 #pragma unroll
-        for (int u = 0; u < NC; ++u) {
-            if (col[u] == l && l != ms - 1 && own[u]) {
+            for (int u = 0; u < NC; ++u)
+                if (col[u] == l) {
 #pragma unroll
-                for (int k = 0; k < kR; k += 2) {
-                    const ulonglong2 q2 = lds_v2(sb + KC_OFF(rxl) + par * (kR * 8) + k * 8);
-                    x[u][k] = u2d(q2.x);
-                    x[u][k + 1] = u2d(q2.y);
+                    for (int k = 0; k < kR; k += 2) {
+                        const ulonglong2 q2 = lds_v2(sb + KC_OFF(rxl) + par * (kR * 8) + k * 8);
+                        x[u][k] = u2d(q2.x);
+                        x[u][k + 1] = u2d(q2.y);
+                    }
                 }
-            }
-            if (own[u] && col[u] < ms - 1) {
-                const double q = div_rn_rcp(x[u][i], v, rcp);
-                x[u][i] = q;
+        }
+        {
+            bool inr = ((unsigned)((d2u(v) >> 52) & 0x7ffu) - 523u) < 1000u;
 #pragma unroll
-                for (int k = i + 1; k < kR; ++k) x[u][k] = __dsub_rn(x[u][k], __dmul_rn(u2d(mu[k]), q));
+            for (int u = 0; u < NC; ++u)  // (a dropped or foreign column never forces the slow path)
+                inr = inr && (!(own[u] && col[u] < ms - 1) || (((unsigned)((d2u(x[u][i]) >> 52) & 0x7ffu) - 523u) < 1000u));
+            double q[NC];
+            if (inr) {
+#pragma unroll
+                for (int u = 0; u < NC; ++u) {
+                    const double q0 = __dmul_rn(x[u][i], rcp);
+                    const double e = __fma_rn(-q0, v, x[u][i]);
+                    q[u] = __fma_rn(e, rcp, q0);
+                }
+            } else {
+#pragma unroll
+                for (int u = 0; u < NC; ++u) q[u] = __ddiv_rn(x[u][i], v);
+            }
+#pragma unroll
+            for (int u = 0; u < NC; ++u) {
+                x[u][i] = q[u];
+#pragma unroll
+                for (int k = i + 1; k < kR; ++k) x[u][k] = __dsub_rn(x[u][k], __dmul_rn(u2d(mu[k]), q[u]));
             }
         }
         KC_MARK(s, 5);
@@ -439,7 +450,7 @@ __device__ __forceinline__ void kc_chain(KCSmem& sm, double* __restrict__ S, con
         }
         if (own[u]) {
 #pragma unroll
-            for (int a = 0; a < kR; ++a) S[(r0 + a) * cw + t + kChainThreads * u] = w[a];
+            for (int a = 0; a < kR; ++a) S[(r0 + a) * cw + NC * t + u] = w[a];
         }
     }
 }
@@ -492,6 +503,11 @@ __global__ void __launch_bounds__(kThreads, 1) kc_panel_kernel(const KPParams p0
         const int lo = g * cw;
         const int wc = max(0, min(cw, m - lo));  // my columns at panel start
         if (*(volatile const unsigned*)p.abort) break;  // uniform: set only by earlier launches
+        unsigned span_slot = 0;
+        if (g == 0 && tid == 0) {
+            span_slot = atomicAdd(&g_kc_span_n, 1u) & 4095u;
+            g_kc_span[span_slot][0] = globaltimer();
+        }
         double* const gcol = reinterpret_cast<double*>(p.colbuf);        // [8][64] multiplier columns
         double* const gmov = gcol + kR * kB;                             // [8][64] moved columns
 
@@ -760,6 +776,7 @@ __global__ void __launch_bounds__(kThreads, 1) kc_panel_kernel(const KPParams p0
                 }
             }
         }
+        if (g == 0 && tid == 0) g_kc_span[span_slot][1] = globaltimer();
         __threadfence();
         __syncthreads();  // S / sm.l reads done before the next half reloads them
     }
@@ -775,6 +792,16 @@ void kc_debug_trace(unsigned long long* steps, unsigned long long* bounds) {
     cudaMemcpyFromSymbol(bounds, g_kc_tb, sizeof(g_kc_tb));
 }
 #endif
+
+int kc_debug_spans(unsigned long long* out, int max_spans) {
+    unsigned n = 0;
+    if (cudaMemcpyFromSymbol(&n, g_kc_span_n, sizeof(n)) != cudaSuccess) return -1;
+    const int k = (int)std::min<unsigned>(std::min<unsigned>(n, 4096u), (unsigned)max_spans);
+    if (k > 0 && cudaMemcpyFromSymbol(out, g_kc_span, (size_t)k * 2 * sizeof(unsigned long long)) != cudaSuccess) return -1;
+    const unsigned zero = 0;
+    cudaMemcpyToSymbol(g_kc_span_n, &zero, sizeof(zero));
+    return k;
+}
 
 size_t kc_smem_bytes(int cw) { return (size_t)kB * cw * sizeof(double); }
 

@@ -2198,7 +2198,18 @@ int mcnd_mc_parallel(const double* h_a, int64_t n, int64_t lda, int32_t p, uint3
 }
 
 /* debug (not part of the ABI header): panel-launch spans of the calls since the last read */
-int mcnd_debug_kp_spans(unsigned long long* out, int max_spans) { return mcnd::kp_debug_spans(out, max_spans); }
+int mcnd_debug_kp_spans(unsigned long long* out, int max_spans) {
+    // both panel kernels' spans, in time order
+    const int a = mcnd::kp_debug_spans(out, max_spans);
+    if (a < 0) return a;
+    const int b = mcnd::kc_debug_spans(out + 2 * (size_t)a, max_spans - a);
+    if (b < 0) return b;
+    std::vector<std::pair<unsigned long long, unsigned long long>> v((size_t)(a + b));
+    for (int i = 0; i < a + b; ++i) v[(size_t)i] = {out[2 * i], out[2 * i + 1]};
+    std::sort(v.begin(), v.end());
+    for (int i = 0; i < a + b; ++i) { out[2 * i] = v[(size_t)i].first; out[2 * i + 1] = v[(size_t)i].second; }
+    return a + b;
+}
 
 int mcnd_logdet_blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, void* stream,
                             mcnd_logdet* out, double* pivots_out, int32_t* cols_out) {

@@ -184,6 +184,7 @@ constexpr int kKCMaxCw = 352;  // 64 x 352 doubles = 176 KB dynamic + 48 KB stat
 int kc_plan(int64_t m, int* cw_out);
 cudaError_t kc_launch(const KPParams& p, cudaStream_t s, const KPParams* second = nullptr);
 size_t kc_smem_bytes(int cw);
+int kc_debug_spans(unsigned long long* out, int max_spans);
 // debug: (entry, exit) globaltimer of the panel launches since the last call; returns the count
 int kp_debug_spans(unsigned long long* out, int max_spans);
 
