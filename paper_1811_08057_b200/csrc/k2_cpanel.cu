@@ -71,6 +71,24 @@ __device__ __forceinline__ unsigned long long abs_bits(double x) {
 }
 __device__ __forceinline__ unsigned hi_abs(double x) { return (unsigned)(abs_bits(x) >> 32); }
 
+// Race stress (test builds only: MCND_BUILD_DEFINES="MCND_JITTER=1", scripts/race_stress.sh):
+// pseudo-random sleeps of up to ~2 us at the hand-off points, so a read that is not properly
+// ordered after its write sees stale data (wrong pivots) or times out
+#ifndef MCND_JITTER
+#define MCND_JITTER 0
+#endif
+__device__ __forceinline__ void jitter(unsigned salt) {
+#if MCND_JITTER
+    unsigned long long c;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
+    unsigned x = (unsigned)c * 2654435761u ^ (blockIdx.x * 40503u + (threadIdx.x >> 5) * 9176u + salt * 7919u);
+    x ^= x >> 15; x *= 2246822519u; x ^= x >> 13;
+    if ((x & 7u) == 0u) __nanosleep(x % 2048u);
+#else
+    (void)salt;
+#endif
+}
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ uint32_t mapa(uint32_t addr, uint32_t cta) {
     uint32_t r;
@@ -239,6 +257,7 @@ __device__ __forceinline__ void kc_chain(KCSmem& sm, double* __restrict__ S, con
         const unsigned ml = __reduce_max_sync(kFull, (has && bh == mh) ? bl : 0u);
         const unsigned ball = __ballot_sync(kFull, has && bh == mh && bl == ml);
         KC_MARK(s, 14);
+        jitter(1u);
         {
             // the winner lane publishes {|candidate|, column} and the column's 8 entries (a warp
             // without active columns: an invalid record from lane 0)
@@ -281,6 +300,7 @@ __device__ __forceinline__ void kc_chain(KCSmem& sm, double* __restrict__ S, con
             const unsigned long long b0 = rbest.x;
             const int c0 = (int)(unsigned)rbest.y;
             KC_MARK(s, 8);
+            jitter(2u);
             if (cc.dst < C) {
                 // words: 0 value, 1 col | maxhi << 32, 2..9 the column's 8 entries
                 const uint32_t bb = cc.r_bar + par * 8;
@@ -311,6 +331,7 @@ __device__ __forceinline__ void kc_chain(KCSmem& sm, double* __restrict__ S, con
         }
         KC_MARK(s, 2);
         // ---- every record of pivot s has arrived
+        jitter(3u);
 #ifndef KC_WAIT_W0
 #define KC_WAIT_W0 0
 #endif
@@ -362,6 +383,7 @@ __device__ __forceinline__ void kc_chain(KCSmem& sm, double* __restrict__ S, con
             hi1 = hl ? (unsigned)(r.y >> 32) : 0u;
         }
         KC_MARK(s, 4);
+        jitter(4u);
         // the multipliers of rows > i (the winner column's entries), the last column if I take it
         unsigned long long mu[kR];
 #pragma unroll
@@ -670,6 +692,7 @@ __global__ void __launch_bounds__(kThreads, 1) kc_panel_kernel(const KPParams p0
             if (sm.bail) goto finish;
             // ---- boundary: the 8 multiplier columns and the moved columns of the other 56 rows
             //      cross the cluster through L2 around one cluster barrier
+            jitter(5u);
             for (int e = tid; e < kR * kB; e += kThreads) {
                 const int k = e >> 6, r = e & 63;
                 if (r < r0 || r >= r0 + kR) {
@@ -683,6 +706,7 @@ __global__ void __launch_bounds__(kThreads, 1) kc_panel_kernel(const KPParams p0
             }
             cluster_sync_all();
             KC_MARKB(j, 2);
+            jitter(6u);
             for (int e = tid; e < kR * kB; e += kThreads) {
                 const int k = e >> 6, r = e & 63;
                 if (r < r0 || r >= r0 + kR) {

@@ -62,11 +62,17 @@ long env_long(const char* name, long dflt) {
 // One panel (second == nullptr) or both panels of a pair in one launch: the cluster-resident
 // kernel (k2_cpanel.cu) while the panel fits one thread-block cluster (active width <= 16 x 352
 // columns), the column-distributed kernel (k2_panel.cu) above.  Test hooks: MCND_KC=0 keeps the
-// column-distributed kernel everywhere, MCND_KC_MAXM lowers the cluster kernel's range.
+// column-distributed kernel everywhere, MCND_KC_MAXM lowers the cluster kernel's range, MCND_KC_C
+// caps the cluster size.
 cudaError_t panel_launch(KPParams q0, cudaStream_t st, KPParams* q1) {
     int cw = 0;
-    const int C = (env_long("MCND_KC", 1) != 0 && q0.m <= env_long("MCND_KC_MAXM", 1L << 30)) ? kc_plan(q0.m, &cw) : 0;
+    int C = (env_long("MCND_KC", 1) != 0 && q0.m <= env_long("MCND_KC_MAXM", 1L << 30)) ? kc_plan(q0.m, &cw) : 0;
     if (C > 0) {
+        const long fc = env_long("MCND_KC_C", 0);  // test hook: a smaller cluster (wider chunks, more columns per thread)
+        if (fc > 0 && fc < C && (q0.m + fc - 1) / fc <= kKCMaxCw - 31) {
+            C = (int)fc;
+            cw = (int)(((q0.m + fc - 1) / fc + 31) / 32 * 32);
+        }
         q0.G = C; q0.cw = cw;
         if (q1) { q1->G = C; q1->cw = cw; }
         return kc_launch(q0, st, q1);

@@ -358,15 +358,33 @@ def test_large_n_chunked_vs_cusolver(mc):
 GROUPS = [None, 0]
 
 
+# The panel factorisation has two kernels: the cluster-resident one (k2_cpanel.cu, active widths
+# <= 5632: every small-N test runs it by default) and the column-distributed one (k2_panel.cu,
+# above).  MCND_KC=0 keeps the column-distributed kernel at every size; MCND_KC_C caps the cluster
+# size (wider chunks: 2 or 3 columns per chain thread at small N).
+PANEL_KERNELS = [None, "column", "cluster2", "cluster4"]
+
+
+def _panel_kernel(env_knob, pk):
+    if pk == "column":
+        env_knob("MCND_KC", 0)
+    elif pk == "cluster2":
+        env_knob("MCND_KC_C", 2)
+    elif pk == "cluster4":
+        env_knob("MCND_KC_C", 4)
+
+
+@pytest.mark.parametrize("pk", PANEL_KERNELS)
 @pytest.mark.parametrize("grp", GROUPS)
 @pytest.mark.parametrize("tail", [2, 100, 1024])
-def test_blocked_vs_oracle(mc, env_knob, tail, grp):
+def test_blocked_vs_oracle(mc, env_knob, tail, grp, pk):
     """Blocked rank-64 condensation: sign exact, log|det| within tolerance, and
     (well-conditioned inputs) the same pivot columns as the reference."""
     from oracle import mcnd_oracle as O
     from paper_1811_08057_b200 import matrix as M
 
     env_knob("MCND_K2_TAIL", tail)
+    _panel_kernel(env_knob, pk)
     if grp is not None:
         env_knob("MCND_K2_GROUP_ABOVE", grp)
     cases = [np.random.default_rng(1).uniform(-1, 1, (300, 300)),
@@ -423,8 +441,45 @@ def test_blocked_lookahead_identical(mc, env_knob, n, grp):
         assert np.array_equal(got[1], ref[1]) and np.array_equal(got[2], ref[2])
 
 
-def test_blocked_singular_and_edges(mc, env_knob):
+@pytest.mark.parametrize("n", [300, 700, 1100, 2500])
+def test_blocked_panel_kernels_agree(mc, env_knob, n):
+    """The cluster-resident and the column-distributed panel kernels apply the same pivot
+    rule (condense.py:82-92) with different arithmetic for the panel's trailing rows (W form
+    per micro-panel vs rank-1 updates): the same pivot columns, pivots and log|det| to
+    rounding, for dense, SPD and tie-rich (entries +-1: the lowest column must win every
+    tie, at the lane, warp, CTA and cluster level) inputs; the tie-rich pivots against the
+    oracle's."""
+    from oracle import mcnd_oracle as O
+    from paper_1811_08057_b200 import matrix as M
+
+    rng = np.random.default_rng(n)
+    cases = [rng.uniform(-1, 1, (n, n)), M.config_spd(n, 7)]
+    if n <= 700:
+        cases.append(np.sign(rng.standard_normal((n, n))) + 3.0 * np.eye(n))
+    for a in cases:
+        res = {}
+        for pk in ("cluster", "column", "cluster2", "cluster4"):
+            _panel_kernel(env_knob, pk)
+            res[pk] = mc.logdet_blocked(a, return_pivots=True)
+            env_knob("MCND_KC", 1)
+            env_knob("MCND_KC_C", 0)
+        ref = res["column"]
+        for pk in ("cluster", "cluster2", "cluster4"):
+            got = res[pk]
+            assert got[0].sign == ref[0].sign
+            assert abs(got[0].log_abs - ref[0].log_abs) <= 1e-10 * max(1.0, abs(ref[0].log_abs)), (pk, got[0], ref[0])
+            assert np.array_equal(got[2], ref[2]), pk
+            assert np.allclose(got[1], ref[1], rtol=1e-9, atol=1e-13)
+    if n <= 700:
+        o = O.logdet_condensation(cases[-1])
+        assert res["cluster"][0].sign == o.sign
+        assert np.mean(res["cluster"][2] == o.cols) > 0.99
+
+
+@pytest.mark.parametrize("pk", [None, "column"])
+def test_blocked_singular_and_edges(mc, env_knob, pk):
     env_knob("MCND_K2_TAIL", 2)
+    _panel_kernel(env_knob, pk)
     from paper_1811_08057_b200 import matrix as M
 
     for n in (1, 2, 3, 65, 66, 130):
@@ -510,15 +565,18 @@ def test_blocked_odd_sizes_vs_cusolver(mc, n):
     assert abs(got.log_abs - float(l_ref)) <= tol(n, float(l_ref))
 
 
+@pytest.mark.parametrize("pk", [None, "column", "cluster4"])
 @pytest.mark.parametrize("grp", GROUPS)
 @pytest.mark.parametrize("dup_row", [5, 1500, 2990])
-def test_blocked_singular_mid_panel_and_tail(mc, env_knob, dup_row, grp):
+def test_blocked_singular_mid_panel_and_tail(mc, env_knob, dup_row, grp, pk):
     """A row duplicated at a position handled by a panel early, mid-matrix, or in the
     K1 tail: SINGULAR (condense.py:90 / 153-158), every later launch aborted, no hang;
     the same handle (workspace) then serves a regular matrix."""
-    n = 3000
+    n = 3000 if pk != "cluster4" else 1300
+    _panel_kernel(env_knob, pk)
     if grp is not None:
         env_knob("MCND_K2_GROUP_ABOVE", grp)
+    dup_row = min(dup_row, n - 10)
     a = np.random.default_rng(dup_row).uniform(-1, 1, (n, n))
     a[dup_row] = a[dup_row // 2]
     assert mc.logdet_blocked(a) == mc.SINGULAR
