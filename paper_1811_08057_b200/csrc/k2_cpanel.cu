@@ -31,7 +31,6 @@
 #include <climits>
 #include <cstddef>
 #include "mcnd_internal.h"
-#include "k2_pair_prep.cuh"
 
 namespace mcnd {
 namespace {
@@ -49,11 +48,14 @@ constexpr int kRecWords = 10;    // {value, col | maxhi << 32, the candidate col
 #if KC_TRACE
 __device__ unsigned long long g_kc_trace[64][16];  // per step: phase timestamps of CTA 0 thread 0
 __device__ unsigned long long g_kc_tb[8][8];
+__device__ unsigned long long g_kc_th[2][16];
+#define KC_MARKH(h, k) do { if (blockIdx.x == 0 && threadIdx.x == 0) g_kc_th[h][k] = clock64(); } while (0)
 #define KC_MARK(s, k) do { if (blockIdx.x == 0 && threadIdx.x == 0) g_kc_trace[s][k] = clock64(); } while (0)
 #define KC_MARKB(j, k) do { if (blockIdx.x == 0 && threadIdx.x == 0) g_kc_tb[j][k] = clock64(); } while (0)
 #else
 #define KC_MARK(s, k) do { } while (0)
 #define KC_MARKB(j, k) do { } while (0)
+#define KC_MARKH(h, k) do { } while (0)
 #endif
 
 // Span log of the panels (CTA 0: globaltimer at the start and end of every panel), read by
@@ -160,7 +162,7 @@ __device__ __forceinline__ unsigned long long d2u(double x) { return (unsigned l
 __device__ __forceinline__ double u2d(unsigned long long x) { return __longlong_as_double((long long)x); }
 
 struct KCSmem {
-    double NL[kB][kB + 1];                       // r1 prologue staging (-A[rows, P0])
+    double NL[kB][kB + 4];                       // r1 prologue staging (-A[rows, P0]); +4: conflict-free A fragments
     unsigned long long rcv[2][16][kRecWords];    // per step parity: one record per CTA
     unsigned long long rxl[2][kR];               // per step parity: the last active column's 8 entries
     unsigned long long bar[2];                   // mbarriers (step parity)
@@ -174,8 +176,9 @@ struct KCSmem {
     int l[kB];
     int P8[kR], mc[kR], ms[kR];
     int bail;
-    PairPrepSmem pp;
-    int P1[kB];
+    K2Gather d0, d1;                             // the pair's first descriptor, this panel's
+    K2Gather gp;                                 // the pair's composite descriptor
+    int cnt[4];
 };
 
 constexpr int kChainWarps = 4;
@@ -477,6 +480,12 @@ __device__ __forceinline__ void kc_chain(KCSmem& sm, double* __restrict__ S, con
     }
 }
 
+__device__ __forceinline__ void kc_copy_desc(K2Gather* dst, const K2Gather* src, int tid) {
+    constexpr int kWords = (int)(sizeof(K2Gather) / sizeof(int32_t));
+    for (int i = tid; i < kWords; i += kThreads)
+        reinterpret_cast<int32_t*>(dst)[i] = reinterpret_cast<const int32_t*>(src)[i];
+}
+
 // Rank-8 update of the four rows rb .. rb+3 of the chunk by the micro-panel at rows r0 .. r0+7
 // (whose slots hold W8): row <- row - L[row, 0:8] W8, columns c0, c0 + cstep, ... < wa.
 __device__ __forceinline__ void kc_update4(double* __restrict__ S, const KCSmem& sm, const int cw, const int r0,
@@ -533,6 +542,7 @@ __global__ void __launch_bounds__(kThreads, 1) kc_panel_kernel(const KPParams p0
         double* const gcol = reinterpret_cast<double*>(p.colbuf);        // [8][64] multiplier columns
         double* const gmov = gcol + kR * kB;                             // [8][64] moved columns
 
+        KC_MARKH(half, 0);
         // ---- load my chunk of the 64 panel rows
         for (int r = warp; r < kB; r += kWarps) {
             const double* src = p.ws + (int64_t)(p.row0 + r) * p.ld + lo;
@@ -550,31 +560,70 @@ __global__ void __launch_bounds__(kThreads, 1) kc_panel_kernel(const KPParams p0
             sm.wit0[tid] = p.wit[p.row0 + tid];
             sm.rmaxhi[tid] = 0u;
         }
-        if (g == 0 && tid == 0) p.pan->n_moved = 0;
         __syncthreads();
+        KC_MARKH(half, 1);
         if (half > 0) cluster_sync_all();  // the first panel's W and descriptor are complete
+        KC_MARKH(half, 2);
         if (p.r1_g0) {
             // ---- the pair's first panel applied to these rows: NL = -A[rows, P0], the moved
             //      columns, then S += NL * W0 on the FP64 tensor cores, k ascending (the trailing
             //      GEMM's arithmetic; same code as k2_panel.cu)
-            const K2Gather* g0 = p.r1_g0;
-            for (int e = tid; e < kB * kB; e += kThreads) {
-                const int r = e >> 6, k = e & 63;
-                sm.NL[r][k] = -__ldcg(p.ws + (int64_t)(p.row0 + r) * p.ld + __ldcg(&g0->P[k]));
+            // (the first panel's descriptor is in shared memory: kept from the first half of this
+            //  launch, or staged here; every gather below then has all its loads in flight)
+            if (half == 0) {
+                for (int i = tid; i < (int)(sizeof(K2Gather) / sizeof(int32_t)); i += kThreads)
+                    reinterpret_cast<int32_t*>(&sm.d0)[i] = __ldcg(reinterpret_cast<const int32_t*>(p.r1_g0) + i);
+                __syncthreads();
             }
-            const int nm = __ldcg(&g0->n_moved);
-            for (int e = tid; e < kB * nm; e += kThreads) {
-                const int r = e / nm, j = e - r * nm;
-                const int c = __ldcg(&g0->moved_c[j]);
-                if (c >= lo && c < lo + wc)
-                    S[r * cw + (c - lo)] = __ldcg(p.ws + (int64_t)(p.row0 + r) * p.ld + __ldcg(&g0->moved_src[j]));
+            const K2Gather& g0 = sm.d0;
+            const double* const rows = p.ws + (int64_t)p.row0 * p.ld;
+            for (int e0 = tid; e0 < kB * kB; e0 += 6 * kThreads) {
+                double v[6];
+#pragma unroll
+                for (int u = 0; u < 6; ++u) {
+                    const int e = e0 + u * kThreads;
+                    v[u] = (e < kB * kB) ? __ldcg(rows + (int64_t)(e >> 6) * p.ld + g0.P[e & 63]) : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < 6; ++u) {
+                    const int e = e0 + u * kThreads;
+                    if (e < kB * kB) sm.NL[e >> 6][e & 63] = -v[u];
+                }
+            }
+            const int nm = g0.n_moved;
+            for (int e0 = tid; e0 < kB * nm; e0 += 4 * kThreads) {
+                double v[4];
+                int at[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int e = e0 + u * kThreads;
+                    at[u] = -1;
+                    v[u] = 0.0;
+                    if (e < kB * nm) {
+                        const int r = e / nm, j = e - r * nm;
+                        const int c = g0.moved_c[j];
+                        if (c >= lo && c < lo + wc) {
+                            at[u] = r * cw + (c - lo);
+                            v[u] = __ldcg(rows + (int64_t)r * p.ld + g0.moved_src[j]);
+                        }
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (at[u] >= 0) S[at[u]] = v[u];
             }
             __syncthreads();
+            KC_MARKH(half, 3);
+            // S += NL * W0 on the FP64 tensor cores (mma.sync.m8n8k4.f64), k ascending (the trailing
+            // GEMM's arithmetic): warp w owns the 8-column tiles w, w + 12, ... two at a time for all
+            // 64 rows (one A fragment feeds both), W0 k-steps in a register ring; a missing second
+            // tile is skipped
             const double* W0 = p.r1_W + lo;
             const int gq = lane >> 2, qq = lane & 3;
             const int ntiles = (wc + 7) >> 3;
             for (int tp = warp; tp < ntiles; tp += 2 * kWarps) {
                 const int tl[2] = {tp, tp + kWarps};
+                const bool two = tl[1] < ntiles;  // warp-uniform
                 double acc[8][2][2];
 #pragma unroll
                 for (int i = 0; i < 8; ++i)
@@ -601,10 +650,11 @@ __global__ void __launch_bounds__(kThreads, 1) kc_panel_kernel(const KPParams p0
 #pragma unroll
                         for (int i = 0; i < 8; ++i) {
                             const double av = sm.NL[8 * i + gq][k + qq];
-#pragma unroll
-                            for (int t = 0; t < 2; ++t)
+                            asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                                : "+d"(acc[i][0][0]), "+d"(acc[i][0][1]) : "d"(av), "d"(bq[s4][0]));
+                            if (two)
                                 asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-                                    : "+d"(acc[i][t][0]), "+d"(acc[i][t][1]) : "d"(av), "d"(bq[s4][t]));
+                                    : "+d"(acc[i][1][0]), "+d"(acc[i][1][1]) : "d"(av), "d"(bq[s4][1]));
                         }
                         if (k + 4 * kPF < kB) {
 #pragma unroll
@@ -627,6 +677,7 @@ __global__ void __launch_bounds__(kThreads, 1) kc_panel_kernel(const KPParams p0
             }
             __syncthreads();
         }
+        KC_MARKH(half, 4);
         // ---- running row maxima of my chunk (high words: an upper bound within 2^-20)
         for (int r = warp; r < kB; r += kWarps) {
             unsigned h = 0u;
@@ -736,6 +787,7 @@ __global__ void __launch_bounds__(kThreads, 1) kc_panel_kernel(const KPParams p0
             KC_MARKB(j, 4);
         }
 
+        KC_MARKH(half, 5);
         // ---- the chunk holds W in the final layout: out (columns < m - 64)
         {
             const int wf = max(0, min(wc, m - kB - lo));
@@ -748,58 +800,137 @@ __global__ void __launch_bounds__(kThreads, 1) kc_panel_kernel(const KPParams p0
                 }
             }
         }
-        // ---- panel-start column of each pivot and the moved final columns (CTA 0)
-        if (g == 0 && tid < kB) {
-            const int s = tid;
-            int pos = sm.l[s];
-            for (int j = s - 1; j >= 0; --j) pos = (pos == sm.l[j]) ? (m - j - 1) : pos;
-            p.pan->P[s] = pos;
-            p.pan->l[s] = sm.l[s];
-            const int c = sm.l[s];
-            bool first = c < m - kB;
-            for (int t = 0; t < s && first; ++t) first = (sm.l[t] != c);
-            if (first) {
-                int q = c;
-                for (int t = kB - 1; t >= 0; --t) q = (q == sm.l[t]) ? (m - t - 1) : q;
-                if (q != c) {
-                    const int k = atomicAdd(&p.pan->n_moved, 1);
-                    p.pan->moved_c[k] = c;
-                    p.pan->moved_src[k] = q;
-                }
-            }
-        }
-        if (p.pp_g0) {
-            // pair prep spread over the cluster (as k2_panel.cu, cluster barriers for its grid barrier)
+        KC_MARKH(half, 6);
+        // ---- the panel's gather descriptor: panel-start column of each pivot and the final columns
+        //      whose content moved (the composition of the 64 exchanges), by every CTA in shared
+        //      memory (the pair prep below needs it everywhere); CTA 0 publishes it
+        {
+            K2Gather& d1 = sm.d1;
+            int c = 0, q = 0, pre = 0;
+            bool flag = false;
             if (tid < kB) {
-                int pos = sm.l[tid];
-                for (int j = tid - 1; j >= 0; --j) pos = (pos == sm.l[j]) ? (m - j - 1) : pos;
-                sm.P1[tid] = pos;
+                const int s = tid;
+                c = sm.l[s];
+                int pos = c;
+                q = c;
+                bool first = c < m - kB;
+#pragma unroll 8
+                for (int j = kB - 1; j >= 0; --j) {
+                    const int lj = sm.l[j];
+                    q = (q == lj) ? (m - j - 1) : q;
+                    if (j < s) {
+                        pos = (pos == lj) ? (m - j - 1) : pos;
+                        first = first && (lj != c);
+                    }
+                }
+                d1.P[s] = pos;
+                d1.l[s] = c;
+                flag = first && q != c;
+                const unsigned ball = __ballot_sync(kFull, flag);
+                pre = __popc(ball & ((1u << lane) - 1u));
+                if (lane == 0) sm.cnt[warp] = __popc(ball);
             }
             __syncthreads();
+            if (tid < kB && flag) {
+                const int k = pre + (warp ? sm.cnt[0] : 0);
+                d1.moved_c[k] = c;
+                d1.moved_src[k] = q;
+            }
+            if (tid == 0) d1.n_moved = sm.cnt[0] + sm.cnt[1];
+            __syncthreads();
+            if (g == 0) kc_copy_desc(p.pan, &d1, tid);
+        }
+        if (p.pp_g0) {
+            // ---- pair prep spread over the cluster: (a) a slice of Wp[s][s'] = -W_k[s][P1[s']];
+            //      the pair's composite descriptor (every CTA in shared memory, CTA 0 publishes it;
+            //      one thread per entry, deterministic order); one cluster barrier (every Wp read
+            //      of W_k done); (b) a slice of W_k's moved columns
+            const K2Gather& d0 = sm.d0;
+            const K2Gather& d1 = sm.d1;
+            if (half == 0) {  // (a second panel launched on its own: the first descriptor from memory)
+                for (int i = tid; i < (int)(sizeof(K2Gather) / sizeof(int32_t)); i += kThreads)
+                    reinterpret_cast<int32_t*>(&sm.d0)[i] = __ldcg(reinterpret_cast<const int32_t*>(p.pp_g0) + i);
+                __syncthreads();
+            }
             {
                 const int e0 = (int)((int64_t)kB * kB * g / C), e1 = (int)((int64_t)kB * kB * (g + 1) / C);
                 for (int e = e0 + tid; e < e1; e += kThreads) {
                     const int sr = e / kB, sp = e % kB;
-                    p.pp_Wp[e] = -__ldcg(p.pp_W + (int64_t)sr * p.pp_ldw + sm.P1[sp]);
+                    p.pp_Wp[e] = -__ldcg(p.pp_W + (int64_t)sr * p.pp_ldw + d1.P[sp]);
                 }
             }
+            KC_MARKH(half, 7);
             if (g == 0) {
+                // (the chunk is dead after the W output: it holds two direct-address maps, final
+                //  column -> source column of each panel, so every lookup is one load)
+                const int wf = p.pp_m - 2 * kB;
+                int* const map0 = reinterpret_cast<int*>(S);   // panel k   : width pp_m
+                int* const map1 = map0 + p.pp_m;               // panel k+1 : width pp_m - 64
+                for (int i = tid; i < 2 * p.pp_m; i += kThreads) map0[i] = -1;
                 __syncthreads();
-                pair_prep_desc<kThreads>(p.pp_g0, p.pan, p.pp_m, p.pp_gpair, sm.pp, tid);
+                if (tid < d0.n_moved) map0[d0.moved_c[tid]] = d0.moved_src[tid];
+                if (tid >= 2 * kB && tid - 2 * kB < d1.n_moved) map1[d1.moved_c[tid - 2 * kB]] = d1.moved_src[tid - 2 * kB];
+                __syncthreads();
+                auto pi0 = [&](int x) { const int r = map0[x]; return r < 0 ? x : r; };
+                auto pi1 = [&](int x) { const int r = map1[x]; return r < 0 ? x : r; };
+                if (tid < kB) {
+                    sm.gp.P[tid] = d0.P[tid];
+                    sm.gp.P[kB + tid] = pi0(d1.P[tid]);
+                    sm.gp.l[tid] = d1.l[tid];
+                }
+                // candidate moved columns: targets of either panel inside the final width (the
+                // first panel's only when the second does not also move them)
+                int c = 0, src = 0, pre = 0;
+                bool flag = false;
+                if (tid < 2 * kB) {
+                    const int n1 = d1.n_moved, n0 = d0.n_moved;
+                    bool valid = false;
+                    if (tid < n1) {
+                        c = d1.moved_c[tid];
+                        valid = c < wf;
+                    } else if (tid - n1 < n0) {
+                        c = d0.moved_c[tid - n1];
+                        valid = c < wf && map1[c] < 0;
+                    }
+                    if (valid) {
+                        src = pi0(pi1(c));
+                        flag = src != c;
+                    }
+                    const unsigned ball = __ballot_sync(kFull, flag);
+                    pre = __popc(ball & ((1u << lane) - 1u));
+                    if (lane == 0) sm.cnt[warp] = __popc(ball);
+                }
+                __syncthreads();
+                if (tid < 2 * kB && flag) {
+                    int k = pre;
+                    for (int w = 0; w < warp; ++w) k += sm.cnt[w];
+                    sm.gp.moved_c[k] = c;
+                    sm.gp.moved_src[k] = src;
+                }
+                if (tid == 0) sm.gp.n_moved = sm.cnt[0] + sm.cnt[1] + sm.cnt[2] + sm.cnt[3];
+                __syncthreads();
+                kc_copy_desc(p.pp_gpair, &sm.gp, tid);
             }
+            KC_MARKH(half, 8);
             __threadfence();
             cluster_sync_all();
+            KC_MARKH(half, 9);
             {
-                const int nm1 = __ldcg(&p.pan->n_moved), wf2 = p.pp_m - 2 * kB;
+                const int nm1 = d1.n_moved, wf2 = p.pp_m - 2 * kB;
                 const int tot = kB * nm1;
                 const int e0 = (int)((int64_t)tot * g / C), e1 = (int)((int64_t)tot * (g + 1) / C);
                 for (int e = e0 + tid; e < e1; e += kThreads) {
                     const int sr = e / nm1, k = e % nm1;
-                    const int c = __ldcg(&p.pan->moved_c[k]);
-                    if (c < wf2) p.pp_W[(int64_t)sr * p.pp_ldw + c] = __ldcg(p.pp_W + (int64_t)sr * p.pp_ldw + __ldcg(&p.pan->moved_src[k]));
+                    const int c = d1.moved_c[k];
+                    if (c < wf2) p.pp_W[(int64_t)sr * p.pp_ldw + c] = __ldcg(p.pp_W + (int64_t)sr * p.pp_ldw + d1.moved_src[k]);
                 }
             }
         }
+        if (half + 1 < halves) {  // the second panel's prologue and pair prep read this descriptor
+            __syncthreads();
+            kc_copy_desc(&sm.d0, &sm.d1, tid);
+        }
+        KC_MARKH(half, 10);
         if (g == 0 && tid == 0) g_kc_span[span_slot][1] = globaltimer();
         __threadfence();
         __syncthreads();  // S / sm.l reads done before the next half reloads them
@@ -815,6 +946,7 @@ void kc_debug_trace(unsigned long long* steps, unsigned long long* bounds) {
     cudaMemcpyFromSymbol(steps, g_kc_trace, sizeof(g_kc_trace));
     cudaMemcpyFromSymbol(bounds, g_kc_tb, sizeof(g_kc_tb));
 }
+void kc_debug_trace_halves(unsigned long long* halves) { cudaMemcpyFromSymbol(halves, g_kc_th, sizeof(g_kc_th)); }
 #endif
 
 int kc_debug_spans(unsigned long long* out, int max_spans) {

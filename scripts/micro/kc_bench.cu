@@ -14,7 +14,7 @@
 #include "mcnd_internal.h"
 using namespace mcnd;
 #if KC_TRACE
-namespace mcnd { void kc_debug_trace(unsigned long long*, unsigned long long*); }
+namespace mcnd { void kc_debug_trace(unsigned long long*, unsigned long long*); void kc_debug_trace_halves(unsigned long long*); }
 #endif
 
 struct Out {
@@ -162,6 +162,17 @@ int main(int argc, char** argv) {
             double dd[13] = {0}; int cn = 0;
             for (int s = 0; s < 64; ++s) { if ((s & 7) == 7) continue; for (int k = 0; k < 13; ++k) dd[k] += (double)(tr[s][seq[k + 1]] - tr[s][seq[k]]); ++cn; }
             for (int k = 0; k < 13; ++k) printf("    %-28s %.0f\n", nm[k], dd[k] / cn);
+        }
+        {
+            static unsigned long long th[2][16];
+            kc_debug_trace_halves(&th[0][0]);
+            const char* hn[] = {"load rows", "half barrier", "r1 gather", "r1 DMMA", "row maxima + micro-panels", "W out", "descriptor", "pair prep Wp",
+                                "pair desc (CTA 0)", "cluster barrier", "W_k moved columns"};
+            for (int h = 0; h < (pair ? 2 : 1); ++h) {
+                printf("  half %d (cycles):", h);
+                for (int k = 0; k < 10; ++k) if (th[h][k + 1] >= th[h][k] && th[h][k]) printf(" %s %llu,", hn[k], th[h][k + 1] - th[h][k]);
+                printf(" total %llu\n", th[h][10] - th[h][0]);
+            }
         }
         for (int j = 0; j < 8; ++j)
             printf("  micro-panel %d: chain %llu, W8+lists %llu, publish+cluster barrier %llu, read+write-back %llu, update %llu\n", j,

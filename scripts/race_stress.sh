@@ -11,7 +11,7 @@ out=${1:-gpurun_out/r2_race_stress.log}
 MCND_BUILD_DEFINES="MCND_JITTER=1" python -c "from paper_1811_08057_b200.build import build; build(force=True)"
 echo "NANOSLEEP instructions, jitter build: $(cuobjdump -sass paper_1811_08057_b200/lib/libmcnd_b200.so | grep -c NANOSLEEP)" > "$out.sass"
 python -m pytest tests/test_gpu_parity.py tests/test_gpu_mg.py -m gpu -q -p no:cacheprovider \
-  -k "serial_bitwise or mc_parallel_bitwise or emulated_ranks or kernel_shapes or blocked_lookahead or blocked_c3 or blocked_vs_oracle or singular or native_driver or ge_logdet" \
+  -k "serial_bitwise or mc_parallel_bitwise or emulated_ranks or kernel_shapes or blocked_lookahead or blocked_c3 or blocked_vs_oracle or panel_kernels_agree or singular or native_driver or ge_logdet" \
   > "$out" 2>&1
 rc=$?
 echo "jitter build exit $rc" >> "$out"
