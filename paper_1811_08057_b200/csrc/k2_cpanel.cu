@@ -539,8 +539,7 @@ __global__ void __launch_bounds__(kThreads, 1) kc_panel_kernel(const KPParams p0
             span_slot = atomicAdd(&g_kc_span_n, 1u) & 4095u;
             g_kc_span[span_slot][0] = globaltimer();
         }
-        double* const gcol = reinterpret_cast<double*>(p.colbuf);        // [8][64] multiplier columns
-        double* const gmov = gcol + kR * kB;                             // [8][64] moved columns
+        double* const gcol = reinterpret_cast<double*>(p.colbuf);  // [micro-panel parity][multiplier | top columns][8][64]
 
         KC_MARKH(half, 0);
         // ---- load my chunk of the 64 panel rows
@@ -559,6 +558,7 @@ __global__ void __launch_bounds__(kThreads, 1) kc_panel_kernel(const KPParams p0
         if (tid < kB) {
             sm.wit0[tid] = p.wit[p.row0 + tid];
             sm.rmaxhi[tid] = 0u;
+            sm.l[tid] = -2;  // "pivot not taken yet" (the publisher warp polls these)
         }
         __syncthreads();
         KC_MARKH(half, 1);
@@ -715,55 +715,102 @@ __global__ void __launch_bounds__(kThreads, 1) kc_panel_kernel(const KPParams p0
                 //      content moved (the composition of the 8 exchanges), identically in every CTA
                 if (tid < kR) {
                     const int k = tid;
-                    int pos = sm.l[r0 + k];
-                    for (int jj = k - 1; jj >= 0; --jj) pos = (pos == sm.l[r0 + jj]) ? (m - (r0 + jj) - 1) : pos;
-                    sm.P8[k] = pos;
-                    const int c = sm.l[r0 + k];
+                    int lv[kR];  // the 8 pivot positions in registers: the chains below are select-only
+#pragma unroll
+                    for (int tt = 0; tt < kR; ++tt) lv[tt] = sm.l[r0 + tt];
+                    int c = lv[0];
+#pragma unroll
+                    for (int tt = 1; tt < kR; ++tt) c = (tt == k) ? lv[tt] : c;
+                    int pos = c, q = c;
                     bool first = c < m - r0 - kR;
-                    for (int tt = 0; tt < k && first; ++tt) first = (sm.l[r0 + tt] != c);
-                    int q = c;
-                    if (first)
-                        for (int tt = kR - 1; tt >= 0; --tt) q = (q == sm.l[r0 + tt]) ? (m - (r0 + tt) - 1) : q;
+#pragma unroll
+                    for (int tt = kR - 1; tt >= 0; --tt) {
+                        q = (q == lv[tt]) ? (m - (r0 + tt) - 1) : q;
+                        if (tt < k) {
+                            pos = (pos == lv[tt]) ? (m - (r0 + tt) - 1) : pos;
+                            first = first && (lv[tt] != c);
+                        }
+                    }
+                    sm.P8[k] = pos;
                     sm.mc[k] = (first && q != c) ? c : -1;
                     sm.ms[k] = q;
                 }
-            } else if (j > 0) {
-                // the other warps meanwhile: the previous micro-panel's update of the rows the chain
-                // does not hold (12 blocks of four rows: all but the previous and the current
-                // micro-panel's), off the critical path
-                const int jp = j - 1;
-                const int wa = max(0, min(wc, m - jp * kR - kR - lo));
-                for (int q = warp - kChainWarps; q < 12; q += kWarps - kChainWarps) {
-                    const int grp = q < 2 * jp ? q : q + 2;          // skips the current micro-panel's blocks ...
-                    const int rb = 4 * (grp < 2 * jp ? grp : grp + 2);  // ... and the previous one's
-                    kc_update4(S, sm, cw, jp * kR, rb, lane, 32, wa);
+            } else {
+                // the other warps meanwhile, off the critical path: (1) the previous micro-panel's
+                // update of the rows the chain does not hold (12 blocks of four rows: all but the
+                // previous and the current micro-panel's)
+                if (j > 0) {
+                    const int jp = j - 1;
+                    const int wa = max(0, min(wc, m - jp * kR - kR - lo));
+                    for (int q = warp - kChainWarps; q < 12; q += kWarps - kChainWarps) {
+                        const int grp = q < 2 * jp ? q : q + 2;          // skips the current micro-panel's blocks ...
+                        const int rb = 4 * (grp < 2 * jp ? grp : grp + 2);  // ... and the previous one's
+                        kc_update4(S, sm, cw, jp * kR, rb, lane, 32, wa);
+                    }
+                }
+                asm volatile("bar.sync 3, %0;" ::"n"(kThreads - kChainThreads) : "memory");  // (1) done in this CTA
+                // (2) one warp publishes what the boundary exchanges, as soon as it exists: the 8
+                //     topmost active columns (the only possible sources of moved columns) now, the
+                //     multiplier column of pivot k as soon as the chain has taken it -- so the
+                //     boundary's cluster barrier finds the stores long complete
+                if (warp == kChainWarps) {
+                    double* const gc = gcol + (j & 1) * (2 * kR * kB);
+                    double* const gt = gc + kR * kB;
+                    const int ms0 = m - r0;
+#pragma unroll
+                    for (int tt = 0; tt < kR; ++tt) {
+                        const int P = ms0 - kR + tt;
+                        if (P >= lo && P < lo + wc) {
+#pragma unroll
+                            for (int h = 0; h < 2; ++h) {
+                                const int r = lane + 32 * h;
+                                if (r < r0 || r >= r0 + kR) gt[tt * kB + r] = S[r * cw + (P - lo)];
+                            }
+                        }
+                    }
+                    int lv[kR];
+#pragma unroll
+                    for (int k = 0; k < kR; ++k) {
+                        int v;
+                        for (;;) {
+                            v = *(volatile int*)&sm.l[r0 + k];
+                            if (v != -2 || *(volatile int*)&sm.bail) break;
+                            __nanosleep(64);
+                        }
+                        lv[k] = v;
+                        int pos = v;
+#pragma unroll
+                        for (int tt = kR - 1; tt >= 0; --tt)
+                            if (tt < k) pos = (pos == lv[tt]) ? (m - (r0 + tt) - 1) : pos;
+                        if (v >= 0 && pos >= lo && pos < lo + wc) {
+#pragma unroll
+                            for (int h = 0; h < 2; ++h) {
+                                const int r = lane + 32 * h;
+                                if (r < r0 || r >= r0 + kR) gc[k * kB + r] = S[r * cw + (pos - lo)];
+                            }
+                        }
+                    }
                 }
             }
             __syncthreads();
             if (sm.bail) goto finish;
             // ---- boundary: the 8 multiplier columns and the moved columns of the other 56 rows
-            //      cross the cluster through L2 around one cluster barrier
-            jitter(5u);
-            for (int e = tid; e < kR * kB; e += kThreads) {
-                const int k = e >> 6, r = e & 63;
-                if (r < r0 || r >= r0 + kR) {
-                    const int P = sm.P8[k];
-                    if (P >= lo && P < lo + wc) gcol[k * kB + r] = S[r * cw + (P - lo)];
-                    if (sm.mc[k] >= 0) {
-                        const int src = sm.ms[k];
-                        if (src >= lo && src < lo + wc) gmov[k * kB + r] = S[r * cw + (src - lo)];
-                    }
-                }
-            }
+            //      cross the cluster through L2 (published during the chain, above) around one
+            //      cluster barrier
             cluster_sync_all();
             KC_MARKB(j, 2);
             jitter(6u);
-            for (int e = tid; e < kR * kB; e += kThreads) {
-                const int k = e >> 6, r = e & 63;
-                if (r < r0 || r >= r0 + kR) {
-                    sm.L[r][k] = __ldcg(gcol + k * kB + r);
-                    const int c = sm.mc[k];
-                    if (c >= lo && c < lo + wc) S[r * cw + (c - lo)] = __ldcg(gmov + k * kB + r);
+            {
+                const double* const gc = gcol + (j & 1) * (2 * kR * kB);
+                const double* const gt = gc + kR * kB;
+                const int ms0 = m - r0;
+                for (int e = tid; e < kR * kB; e += kThreads) {
+                    const int k = e >> 6, r = e & 63;
+                    if (r < r0 || r >= r0 + kR) {
+                        sm.L[r][k] = __ldcg(gc + k * kB + r);
+                        const int c = sm.mc[k];
+                        if (c >= lo && c < lo + wc) S[r * cw + (c - lo)] = __ldcg(gt + (sm.ms[k] - (ms0 - kR)) * kB + r);
+                    }
                 }
             }
             __syncthreads();
