@@ -1010,8 +1010,9 @@ size_t kc_smem_bytes(int cw) { return (size_t)kB * cw * sizeof(double); }
 
 // Cluster size and chunk width for active width m (0: the cluster kernel does not take it)
 int kc_plan(int64_t m, int* cw_out) {
-    if (m < 2 * kB || m > (int64_t)kKCMaxC * kKCMaxCw) return 0;
-    int C = kKCMaxC;
+    const int cmax = kc_max_cluster();
+    if (cmax < 2 || m < 2 * kB || m > (int64_t)cmax * kKCMaxCw) return 0;
+    int C = cmax;
     while (C > 2 && m <= (int64_t)(C / 2) * 128) C /= 2;  // at least ~128 columns per CTA
     int cw = (int)((m + C - 1) / C);
     cw = (cw + 31) / 32 * 32;
@@ -1019,6 +1020,44 @@ int kc_plan(int64_t m, int* cw_out) {
     if (cw > kKCMaxCw) return 0;
     *cw_out = cw;
     return C;
+}
+
+// Largest cluster (16, 8, 4, 2; 0: none) the current device can co-schedule with the kernel's
+// largest footprint (352 columns per CTA), probed once per device: a device or partition without
+// 16 free SMs in one GPC takes smaller clusters, or the column-distributed kernel.
+int kc_max_cluster() {
+    constexpr int kMaxDev = 64;
+    static int cache[kMaxDev] = {};  // 0: not probed, -1: none
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDev) return 0;
+    if (cache[dev]) return cache[dev] < 0 ? 0 : cache[dev];
+    auto fn = kc_panel_kernel<3>;
+    const size_t smem = kc_smem_bytes(kKCMaxCw);
+    int best = -1;
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess &&
+        cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess) {
+        for (int C = kKCMaxC; C >= 2; C /= 2) {
+            cudaLaunchConfig_t cfg{};
+            cfg.gridDim = dim3(C);
+            cfg.blockDim = dim3(kThreads);
+            cfg.dynamicSmemBytes = smem;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = (unsigned)C;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            int n = 0;
+            if (cudaOccupancyMaxActiveClusters(&n, fn, &cfg) == cudaSuccess && n >= 1) {
+                best = C;
+                break;
+            }
+        }
+    }
+    (void)cudaGetLastError();
+    cache[dev] = best;
+    return best < 0 ? 0 : best;
 }
 
 cudaError_t kc_launch(const KPParams& p, cudaStream_t s, const KPParams* second) {

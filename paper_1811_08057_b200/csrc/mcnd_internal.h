@@ -181,7 +181,9 @@ size_t kp_smem_bytes(int cw);
 constexpr int kKCMaxC = 16;
 constexpr int kKCMaxCw = 352;  // 64 x 352 doubles = 176 KB dynamic + 48 KB static shared memory
 // cluster size for active width m and its chunk width; 0: m is outside the cluster kernel's range
+// on the current device (kc_max_cluster: the largest cluster it can co-schedule, probed once)
 int kc_plan(int64_t m, int* cw_out);
+int kc_max_cluster();
 cudaError_t kc_launch(const KPParams& p, cudaStream_t s, const KPParams* second = nullptr);
 size_t kc_smem_bytes(int cw);
 int kc_debug_spans(unsigned long long* out, int max_spans);
