@@ -166,6 +166,7 @@ struct KCSmem {
     unsigned long long rcv[2][16][kRecWords];    // per step parity: one record per CTA
     unsigned long long rxl[2][kR];               // per step parity: the last active column's 8 entries
     unsigned long long bar[2];                   // mbarriers (step parity)
+    unsigned long long bar_ld;                   // mbarrier of the bulk row load (one phase per panel)
     double L[kB][kR];                            // boundary: the multiplier columns of the other rows
     double T8[kR][kR];                           // micro-panel T (strict upper part)
     ulonglong2 wrec[4];                          // per chain warp: {|candidate| bits, column}
@@ -521,6 +522,7 @@ __global__ void __launch_bounds__(kThreads, 1) kc_panel_kernel(const KPParams p0
     if (tid == 0) {
         mbar_init(smem_u32(&sm.bar[0]), 1);
         mbar_init(smem_u32(&sm.bar[1]), 1);
+        mbar_init(smem_u32(&sm.bar_ld), 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         sm.bail = 0;
     }
@@ -542,19 +544,35 @@ __global__ void __launch_bounds__(kThreads, 1) kc_panel_kernel(const KPParams p0
         double* const gcol = reinterpret_cast<double*>(p.colbuf);  // [micro-panel parity][multiplier | top columns][8][64]
 
         KC_MARKH(half, 0);
-        // ---- load my chunk of the 64 panel rows
-        for (int r = warp; r < kB; r += kWarps) {
-            const double* src = p.ws + (int64_t)(p.row0 + r) * p.ld + lo;
-            for (int c = 2 * lane; c < wc; c += 64) {
-                if (c + 1 < wc) {
-                    const unsigned d = (unsigned)__cvta_generic_to_shared(S + r * cw + c);
-                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src + c) : "memory");
-                } else {
-                    S[r * cw + c] = __ldcg(src + c);
+        // ---- load my chunk of the 64 panel rows: one bulk copy (TMA engine, cp.async.bulk) per
+        //      row, issued by 64 threads, completing a transaction count on an mbarrier (rows are
+        //      16-byte aligned: ld and the chunk offset are even; an odd last column goes by hand)
+        const bool al_in = ((reinterpret_cast<uintptr_t>(p.ws) & 15u) == 0) && ((p.ld & 1) == 0);
+        const bool al_out = ((reinterpret_cast<uintptr_t>(p.W) & 15u) == 0) && ((p.ldw & 1) == 0);
+        {
+            // (rows not 16-byte aligned -- never from this library's workspaces -- go element-wise)
+            const unsigned rb = al_in ? (unsigned)(wc & ~1) * 8u : 0u;  // bytes per row through the bulk copy
+            if (tid == 0) mbar_arrive_expect_tx(smem_u32(&sm.bar_ld), rb * kB);
+            if (!al_in)
+                for (int e = tid; e < kB * wc; e += kThreads) {
+                    const int r = e / wc, c = e - r * wc;
+                    S[r * cw + c] = __ldcg(p.ws + (int64_t)(p.row0 + r) * p.ld + lo + c);
+                }
+            if (tid < kB) {
+                const double* src = p.ws + (int64_t)(p.row0 + tid) * p.ld + lo;
+                if (rb)
+                    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                                 ::"r"(smem_u32(S + tid * cw)), "l"(src), "r"(rb), "r"(smem_u32(&sm.bar_ld)) : "memory");
+                if (al_in && (wc & 1)) S[tid * cw + wc - 1] = __ldcg(src + wc - 1);
+            }
+            while (!mbar_try_wait(smem_u32(&sm.bar_ld), (unsigned)half & 1u)) {
+                if (globaltimer() - t_start > p.timeout_ns) {
+                    atomicExch(&p.err->error, 1u);
+                    atomicExch(&p.err->err_step, (unsigned)p.row0);
+                    break;
                 }
             }
         }
-        asm volatile("cp.async.wait_all;" ::: "memory");
         if (tid < kB) {
             sm.wit0[tid] = p.wit[p.row0 + tid];
             sm.rmaxhi[tid] = 0u;
@@ -835,16 +853,26 @@ __global__ void __launch_bounds__(kThreads, 1) kc_panel_kernel(const KPParams p0
         }
 
         KC_MARKH(half, 5);
-        // ---- the chunk holds W in the final layout: out (columns < m - 64)
+        // ---- the chunk holds W in the final layout: out (columns < m - 64), one bulk store per row
+        //      (shared -> global through the TMA engine; the generic-proxy writes of the chunk are
+        //      fenced into the async proxy first)
         {
             const int wf = max(0, min(wc, m - kB - lo));
-            for (int r = warp; r < kB; r += kWarps) {
-                double* const dstw = p.W + (int64_t)r * p.ldw + lo;
-                const double* const srow = S + r * cw;
-                for (int c = 2 * lane; c < wf; c += 64) {
-                    if (c + 1 < wf) *reinterpret_cast<double2*>(dstw + c) = *reinterpret_cast<const double2*>(srow + c);
-                    else dstw[c] = srow[c];
+            const unsigned rb = al_out ? (unsigned)(wf & ~1) * 8u : 0u;
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncthreads();
+            if (!al_out)
+                for (int e = tid; e < kB * wf; e += kThreads) {
+                    const int r = e / wf, c = e - r * wf;
+                    p.W[(int64_t)r * p.ldw + lo + c] = S[r * cw + c];
                 }
+            if (tid < kB) {
+                double* const dstw = p.W + (int64_t)tid * p.ldw + lo;
+                if (rb)
+                    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                                 ::"l"(dstw), "r"(smem_u32(S + tid * cw)), "r"(rb) : "memory");
+                if (al_out && (wf & 1)) dstw[wf - 1] = S[tid * cw + wf - 1];
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
             }
         }
         KC_MARKH(half, 6);
@@ -884,6 +912,9 @@ __global__ void __launch_bounds__(kThreads, 1) kc_panel_kernel(const KPParams p0
                 d1.moved_src[k] = q;
             }
             if (tid == 0) d1.n_moved = sm.cnt[0] + sm.cnt[1];
+            // the W rows are out (complete in global memory: the barriers below publish them; the
+            // chunk may be reused)
+            if (tid < kB) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
             __syncthreads();
             if (g == 0) kc_copy_desc(p.pan, &d1, tid);
         }
@@ -980,6 +1011,7 @@ __global__ void __launch_bounds__(kThreads, 1) kc_panel_kernel(const KPParams p0
         KC_MARKH(half, 10);
         if (g == 0 && tid == 0) g_kc_span[span_slot][1] = globaltimer();
         __threadfence();
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // (the next half's bulk load overwrites the chunk)
         __syncthreads();  // S / sm.l reads done before the next half reloads them
     }
 finish:
