@@ -2,10 +2,11 @@
 //
 // The column-distributed panel kernel of k2_panel.cu pays two L2 round trips per pivot
 // between ~45 CTAs (3.2 us per pivot at C3).  Here the 64 panel rows x m active columns
-// live in the shared memory of ONE thread-block cluster (C <= 16 CTAs, m <= C * 368) and the
+// live in the shared memory of ONE thread-block cluster (C <= 16 CTAs, m <= C * 352) and the
 // 64 pivots are taken in 8 micro-panels of 8 rows:
 //
-//   * inside a micro-panel the 8 rows live in REGISTERS (one column per thread).  Per pivot
+//   * inside a micro-panel the 8 rows live in REGISTERS of 4 "chain" warps (1-3 consecutive
+//     columns per thread: lane order = column order).  Per pivot
 //     (the reference's rule, condense.py:82-131, on micro-panel row i): warp argmax (redux),
 //     CTA argmax, then ONE hop: every CTA sends its {candidate, column, the candidate column's
 //     8 entries} (and the owner of the last active column that column's 8 entries) to every
@@ -17,9 +18,14 @@
 //     of the trailing update: row <- row o pi - row[P8] * W8 with W8 = T8^{-1} U8.  Finished
 //     rows are kept as rows of W (not U), for which the same formula is exactly the block
 //     recurrence of W = T^{-1} U -- so finished and future rows take one uniform rank-8 update
-//     and the chunk holds the panel's W at the end (no T^{-1}, no epilogue product).  The 8
-//     multiplier columns and the <= 8 moved columns cross CTAs through L2 around one cluster
-//     barrier.
+//     and the chunk holds the panel's W at the end (no T^{-1}, no epilogue product).  Only the
+//     next micro-panel's 8 rows are updated on the critical path; the other 48 follow on the
+//     8 non-chain warps while the next micro-panel's chain runs.  The 8 multiplier columns and
+//     the 8 topmost columns (the sources of moved columns) cross CTAs through L2 around one
+//     cluster barrier, published by a helper warp while the chain runs.
+//   * the chunk's rows come in and the W rows go out as bulk copies (cp.async.bulk, the TMA
+//     engine); descriptors stay in shared memory, the pair's composite descriptor is built from
+//     direct-address column maps in the dead chunk.
 //
 // Same KPParams, outputs (W, pivot records, gather descriptor, pair prep) and pair launch
 // (both panels of a pair in one launch, the second applying the first's update to its rows
@@ -336,10 +342,7 @@ __device__ __forceinline__ void kc_chain(KCSmem& sm, double* __restrict__ S, con
         KC_MARK(s, 2);
         // ---- every record of pivot s has arrived
         jitter(3u);
-#ifndef KC_WAIT_W0
-#define KC_WAIT_W0 0
-#endif
-        if (!stopped && (!KC_WAIT_W0 || warp == 0)) {
+        if (!stopped) {
             unsigned spins = 0;
             while (!mbar_try_wait(cc.l_bar + par * 8, ph)) {
                 if ((++spins & 63u) == 0u) {
@@ -352,9 +355,6 @@ __device__ __forceinline__ void kc_chain(KCSmem& sm, double* __restrict__ S, con
                 }
             }
         }
-#if KC_WAIT_W0
-        asm volatile("bar.sync 2, %0;" ::"n"(kChainThreads) : "memory");
-#endif
         KC_MARK(s, 3);
         // ---- the cluster's argmax (ties -> lowest column = lowest CTA); every lane < C also forms
         //      the reciprocal of its record's value while the reduction runs
