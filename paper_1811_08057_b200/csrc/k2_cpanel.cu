@@ -36,6 +36,7 @@
 #include <cstdint>
 #include <climits>
 #include <cstddef>
+#include <type_traits>
 #include "mcnd_internal.h"
 
 namespace mcnd {
@@ -639,25 +640,28 @@ __global__ void __launch_bounds__(kThreads, 1) kc_panel_kernel(const KPParams p0
             const double* W0 = p.r1_W + lo;
             const int gq = lane >> 2, qq = lane & 3;
             const int ntiles = (wc + 7) >> 3;
-            for (int tp = warp; tp < ntiles; tp += 2 * kWarps) {
+            // (two copies of the loop body, with and without the second tile: a predicate around
+            //  mma.sync makes the compiler bracket every DMMA with WARPSYNC)
+            auto tiles = [&](const int tp, auto two_c) {
+                constexpr bool two = decltype(two_c)::value;
+                constexpr int NT = two ? 2 : 1;
                 const int tl[2] = {tp, tp + kWarps};
-                const bool two = tl[1] < ntiles;  // warp-uniform
-                double acc[8][2][2];
+                double acc[8][NT][2];
 #pragma unroll
                 for (int i = 0; i < 8; ++i)
 #pragma unroll
-                    for (int t = 0; t < 2; ++t) {
+                    for (int t = 0; t < NT; ++t) {
                         const int c = tl[t] * 8 + 2 * qq;
                         const double* sp = S + (8 * i + gq) * cw + c;
                         acc[i][t][0] = (c < wc) ? sp[0] : 0.0;
                         acc[i][t][1] = (c + 1 < wc) ? sp[1] : 0.0;
                     }
                 constexpr int kPF = 4;
-                double bq[kPF][2];
+                double bq[kPF][NT];
 #pragma unroll
                 for (int s4 = 0; s4 < kPF; ++s4)
 #pragma unroll
-                    for (int t = 0; t < 2; ++t) {
+                    for (int t = 0; t < NT; ++t) {
                         const int c = tl[t] * 8 + gq;
                         bq[s4][t] = (c < wc) ? __ldcg(W0 + (int64_t)(4 * s4 + qq) * p.r1_ldw + c) : 0.0;
                     }
@@ -665,18 +669,18 @@ __global__ void __launch_bounds__(kThreads, 1) kc_panel_kernel(const KPParams p0
 #pragma unroll
                     for (int s4 = 0; s4 < kPF; ++s4) {
                         const int k = k0 + 4 * s4;
+                        double av[8];
 #pragma unroll
-                        for (int i = 0; i < 8; ++i) {
-                            const double av = sm.NL[8 * i + gq][k + qq];
-                            asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-                                : "+d"(acc[i][0][0]), "+d"(acc[i][0][1]) : "d"(av), "d"(bq[s4][0]));
-                            if (two)
+                        for (int i = 0; i < 8; ++i) av[i] = sm.NL[8 * i + gq][k + qq];
+#pragma unroll
+                        for (int i = 0; i < 8; ++i)
+#pragma unroll
+                            for (int t = 0; t < NT; ++t)
                                 asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-                                    : "+d"(acc[i][1][0]), "+d"(acc[i][1][1]) : "d"(av), "d"(bq[s4][1]));
-                        }
+                                    : "+d"(acc[i][t][0]), "+d"(acc[i][t][1]) : "d"(av[i]), "d"(bq[s4][t]));
                         if (k + 4 * kPF < kB) {
 #pragma unroll
-                            for (int t = 0; t < 2; ++t) {
+                            for (int t = 0; t < NT; ++t) {
                                 const int c = tl[t] * 8 + gq;
                                 bq[s4][t] = (c < wc) ? __ldcg(W0 + (int64_t)(k + 4 * kPF + qq) * p.r1_ldw + c) : 0.0;
                             }
@@ -686,12 +690,16 @@ __global__ void __launch_bounds__(kThreads, 1) kc_panel_kernel(const KPParams p0
 #pragma unroll
                 for (int i = 0; i < 8; ++i)
 #pragma unroll
-                    for (int t = 0; t < 2; ++t) {
+                    for (int t = 0; t < NT; ++t) {
                         const int c = tl[t] * 8 + 2 * qq;
                         double* const sp = S + (8 * i + gq) * cw + c;
                         if (c < wc) sp[0] = acc[i][t][0];
                         if (c + 1 < wc) sp[1] = acc[i][t][1];
                     }
+            };
+            for (int tp = warp; tp < ntiles; tp += 2 * kWarps) {
+                if (tp + kWarps < ntiles) tiles(tp, std::true_type{});
+                else tiles(tp, std::false_type{});
             }
             __syncthreads();
         }
