@@ -208,7 +208,121 @@ __global__ void k3_batched_warp(const double* __restrict__ a, int n, int64_t str
     }
 }
 
+// The blocked path's tail: the last mt <= 128 rows x mt columns of the workspace (rows row0 ..,
+// row stride ldw) condensed to the end by ONE pair of warps with the same step as above -- the
+// arithmetic of K1's in-place tail (bitwise: same pivots, same records), at ~0.3 us per step
+// instead of the 148-CTA kernel's ~3.9 us (its per-step cost is the inter-CTA publication, which
+// a 64 x 64 block does not need).  Witnesses start from the carried-in running maxima; every
+// pivot goes out as a PivRec {v, l (-1: failed the witness test), epoch}, the final 1 x 1 last.
+template <bool kFast, int TPM>
+__global__ void __launch_bounds__(TPM) k3_tail_kernel(const double* __restrict__ ws, int64_t ldw, int row0, int n,
+                                                       const double* __restrict__ wit_in, PivRec* __restrict__ rec,
+                                                       uint32_t epoch, const unsigned* __restrict__ abort) {
+    extern __shared__ __align__(16) double sh[];
+    if (abort && *(volatile const unsigned*)abort) return;
+    const int lane = threadIdx.x & 31, li = threadIdx.x;
+    const bool lead = li < 32;
+    const int ld = n + 1 + (n & 1);  // odd: threads walking different rows hit different banks
+    double* A = sh;
+    double* prow = A + n * ld;
+    double* wit = prow + n;
+    double* ctl = wit + n;  // [l]
+    for (int r = 0; r < n; ++r)
+        for (int c = li; c < n; c += TPM) A[r * ld + c] = __ldcg(ws + (int64_t)(row0 + r) * ldw + c);
+    for (int r = li; r < n; r += TPM) wit[r] = wit_in[row0 + r];
+    for (int s = 0; s < n - 1; ++s) {
+        const int m = n - s, w = m - 1;
+        __syncthreads();  // row s final, witnesses current
+        if (lead) {
+            const double* rk = A + s * ld;
+            unsigned long long best = 0ull;
+            int bi = INT_MAX;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int c = lane + 32 * k;
+                if (c < m) {
+                    const unsigned long long ab = abs_bits(rk[c]);
+                    if (bi == INT_MAX || ab > best) { best = ab; bi = c; }
+                }
+            }
+            const int l = warp_argmax(best, bi);  // ties -> lowest column (condense.py:88)
+            const double v = rk[l];
+            const bool singular = !(fabs(v) > kSingularRtol * wit[s]);  // condense.py:90
+            if (!singular) {
+                const double ylast = rk[w];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int c = lane + 32 * k;
+                    if (c < w) prow[c] = __ddiv_rn(c == l ? ylast : rk[c], v);
+                }
+            }
+            if (lane == 0) {
+                rec[s].v = v;
+                rec[s].l = singular ? -1 : l;
+                rec[s].flag = epoch;
+                ctl[0] = singular ? -1.0 : (double)l;
+            }
+        }
+        __syncthreads();  // pivot row + l published
+        const int l = (int)ctl[0];
+        if (l < 0) return;  // singular: uniform
+        constexpr int NR = 1;  // one row per thread (n <= TPM)
+        double mult[NR], mx[NR];
+        double* rr[NR];
+        bool live[NR];
+#pragma unroll
+        for (int k = 0; k < NR; ++k) {
+            const int r = li + TPM * k;
+            live[k] = r > s && r < n;
+            rr[k] = A + (live[k] ? r : s) * ld;
+            mult[k] = live[k] ? rr[k][l] : 0.0;
+            if (live[k]) rr[k][l] = rr[k][w];  // column exchange (mult already read)
+            mx[k] = 0.0;
+        }
+#pragma unroll 4
+        for (int c = 0; c < w; ++c) {
+            const double pc = prow[c];
+#pragma unroll
+            for (int k = 0; k < NR; ++k) {
+                if (live[k]) {
+                    const double y = upd<kFast>(rr[k][c], mult[k], pc);
+                    rr[k][c] = y;
+                    mx[k] = fmax(mx[k], fabs(y));
+                }
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < NR; ++k)
+            if (live[k]) wit[li + TPM * k] = fmax(wit[li + TPM * k], mx[k]);
+    }
+    __syncthreads();
+    if (li == 0) {  // the final 1 x 1 (condense.py:153-158)
+        const double v = A[(n - 1) * ld];
+        rec[n - 1].v = v;
+        rec[n - 1].l = (fabs(v) > kSingularRtol * wit[n - 1]) ? 0 : -1;
+        rec[n - 1].flag = epoch;
+    }
+}
+
 }  // namespace
+
+cudaError_t k3_tail_launch(const double* ws, int64_t ldw, int32_t row0, int32_t n, bool fast, const double* wit_in,
+                           PivRec* rec, uint32_t epoch, const unsigned* abort, cudaStream_t s) {
+    if (n < 1 || n > 128) return cudaErrorInvalidValue;
+    const size_t smem = (size_t)(n * (n + 1 + (n & 1)) + 2 * n + 2) * sizeof(double);
+    cudaError_t e;
+#define MCND_K3T(F, T)                                                                                  \
+    e = cudaFuncSetAttribute(k3_tail_kernel<F, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    if (e != cudaSuccess) return e;                                                                     \
+    k3_tail_kernel<F, T><<<1, T, smem, s>>>(ws, ldw, row0, n, wit_in, rec, epoch, abort);
+    if (n <= 64) {
+        if (fast) { MCND_K3T(true, 64) } else { MCND_K3T(false, 64) }
+    } else {
+        if (fast) { MCND_K3T(true, 128) } else { MCND_K3T(false, 128) }
+    }
+#undef MCND_K3T
+    return cudaGetLastError();
+}
 
 cudaError_t k3_launch(const double* a, int64_t batch, int64_t n, int64_t stride, bool fast,
                       int32_t* sign, double* log_abs, double* pivots, unsigned* nonfinite, cudaStream_t s) {

@@ -1339,7 +1339,13 @@ int blocked_dev(const double* d_a, int64_t n, int64_t lda, uint32_t flags, cudaS
     p.in_place = 1; p.wit_in = wit; p.row_pstep = d_iota;
     p.ncol0 = (int32_t)mt; p.n_steps = (int32_t)(mt - 1); p.seq = d_iota + kb_end; p.pstep_offset = (int32_t)kb_end;
     p.cta_row_ptr = d_tptr; p.cta_rows = d_trows; p.ctas_per_group = (int32_t)Gt; p.rec[0] = recs + kb_end;
-    e = k1_launch(p, fast, st);
+    // (after panels, a tail of at most 128 rows goes to one pair of warps -- the same arithmetic,
+    //  bitwise, without K1's per-step publication between 148 CTAs: 20 us instead of 240 us at
+    //  64 rows; MCND_K2_SMALL_TAIL=0: K1)
+    if (n_panels > 0 && mt >= 2 && mt <= 128 && env_long("MCND_K2_SMALL_TAIL", 1) != 0)
+        e = k3_tail_launch(ws, ld, (int32_t)kb_end, (int32_t)mt, fast, wit, recs + kb_end, epoch, abort, st);
+    else
+        e = k1_launch(p, fast, st);
     if (e != cudaSuccess) return fail(MCND_ECUDA, "K2 tail launch: %s", cudaGetErrorString(e));
     CUDA_TRY(cudaEventRecord(B->ev1, st));
     out->launches = n_launch + 1;

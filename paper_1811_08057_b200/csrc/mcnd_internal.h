@@ -211,6 +211,10 @@ cudaError_t k2_gemm(double* ws, int64_t ld, int32_t rbase, int32_t M, int32_t N2
                     int64_t ldl, const double* W, int64_t ldw, double* row_wit, const unsigned* abort, cudaStream_t s,
                     int sm_budget = 0, const double* W1 = nullptr);
 
+// The blocked path's tail (k3_batched.cu): rows row0 .. row0+n-1 x n columns of the workspace (n <= 128)
+// condensed to the end by one pair of warps, K1's in-place arithmetic; records rec[0 .. n-1].
+cudaError_t k3_tail_launch(const double* ws, int64_t ldw, int32_t row0, int32_t n, bool fast, const double* wit_in,
+                           PivRec* rec, uint32_t epoch, const unsigned* abort, cudaStream_t s);
 // nonfinite (nullable, device): set to nonzero if any input entry is NaN/Inf.
 cudaError_t k3_launch(const double* a, int64_t batch, int64_t n, int64_t stride, bool fast,
                       int32_t* sign, double* log_abs, double* pivots, unsigned* nonfinite, cudaStream_t s);

@@ -476,6 +476,25 @@ def test_blocked_panel_kernels_agree(mc, env_knob, n):
         assert np.mean(res["cluster"][2] == o.cols) > 0.99
 
 
+@pytest.mark.parametrize("n,tail", [(333, None), (700, None), (1187, None), (2000, 100), (3000, 2)])
+def test_blocked_small_tail_bitwise(mc, env_knob, n, tail):
+    """The blocked path's last <= 128 rows go to a one-CTA kernel (a row per thread) instead of
+    the 148-CTA K1 (MCND_K2_SMALL_TAIL=0): the same arithmetic, so every pivot, column and the
+    result are bitwise identical, for tails of 56 ... 123 rows; a row made singular inside the
+    tail is detected there."""
+    a = np.random.default_rng(n).uniform(-1, 1, (n, n))
+    if tail is not None:
+        env_knob("MCND_K2_TAIL", tail)
+    env_knob("MCND_K2_SMALL_TAIL", 0)
+    ref = mc.logdet_blocked(a, return_pivots=True)
+    env_knob("MCND_K2_SMALL_TAIL", 1)
+    got = mc.logdet_blocked(a, return_pivots=True)
+    assert got[0] == ref[0]
+    assert np.array_equal(got[1], ref[1]) and np.array_equal(got[2], ref[2])
+    a[n - 10] = a[n // 2]
+    assert mc.logdet_blocked(a) == mc.SINGULAR
+
+
 @pytest.mark.parametrize("pk", [None, "column"])
 def test_blocked_singular_and_edges(mc, env_knob, pk):
     env_knob("MCND_K2_TAIL", 2)
