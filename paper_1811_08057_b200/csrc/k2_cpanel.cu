@@ -2,7 +2,7 @@
 //
 // The column-distributed panel kernel of k2_panel.cu pays two L2 round trips per pivot
 // between ~45 CTAs (3.2 us per pivot at C3).  Here the 64 panel rows x m active columns
-// live in the shared memory of ONE thread-block cluster (C <= 16 CTAs, m <= C * 352) and the
+// live in the shared memory of ONE thread-block cluster (C <= 16 CTAs, m <= C * 400) and the
 // 64 pivots are taken in 8 micro-panels of 8 rows:
 //
 //   * inside a micro-panel the 8 rows live in REGISTERS of 4 "chain" warps (1-3 consecutive
@@ -169,15 +169,15 @@ __device__ __forceinline__ unsigned long long d2u(double x) { return (unsigned l
 __device__ __forceinline__ double u2d(unsigned long long x) { return __longlong_as_double((long long)x); }
 
 struct KCSmem {
-    double NL[kB][kB + 4];                       // r1 prologue staging (-A[rows, P0]); +4: conflict-free A fragments
+    double NL[kB][16 + 4];                       // r1 prologue staging: one k-block of 16 of -A[rows, P0]; +4: conflict-free A fragments
     unsigned long long rcv[2][16][kRecWords];    // per step parity: one record per CTA
     unsigned long long rxl[2][kR];               // per step parity: the last active column's 8 entries
     unsigned long long bar[2];                   // mbarriers (step parity)
     unsigned long long bar_ld;                   // mbarrier of the bulk row load (one phase per panel)
     double L[kB][kR];                            // boundary: the multiplier columns of the other rows
     double T8[kR][kR];                           // micro-panel T (strict upper part)
-    ulonglong2 wrec[4];                          // per chain warp: {|candidate| bits, column}
-    double wx[4][kR];                            // per chain warp: the candidate column's 8 entries
+    ulonglong2 wrec[8];                          // per chain warp: {|candidate| bits, column}
+    double wx[8][kR];                            // per chain warp: the candidate column's 8 entries
     double xl[kR];
     unsigned rmaxhi[kB];                         // per row: high word of the chunk's running max |.|
     double wit0[kB];
@@ -189,7 +189,7 @@ struct KCSmem {
     int cnt[4];
 };
 
-constexpr int kChainWarps = 4;
+constexpr int kChainWarps = 5;  // 160 chain threads x <= 3 columns: chunks up to 480 columns
 constexpr int kChainThreads = 32 * kChainWarps;
 
 struct KCChain {
@@ -596,18 +596,18 @@ __global__ void __launch_bounds__(kThreads, 1) kc_panel_kernel(const KPParams p0
             }
             const K2Gather& g0 = sm.d0;
             const double* const rows = p.ws + (int64_t)p.row0 * p.ld;
-            for (int e0 = tid; e0 < kB * kB; e0 += 6 * kThreads) {
-                double v[6];
+            // NL = -A[rows, P0] in registers: thread t gathers column k = t mod 64 of rows t/64,
+            // t/64 + 6, ... (all loads in flight); the staging buffer holds one k-block of 16 at a
+            // time (the shared memory a full 64 x 64 staging would take goes to the chunk: 400
+            // instead of 352 columns per CTA), so the thread stores its values in the pass of its
+            // k-block
+            constexpr int kNLper = (kB * kB + kThreads - 1) / kThreads;  // 11
+            static_assert(kThreads % kB == 0, "a thread's gathered elements share their column");
+            double nlv[kNLper];
 #pragma unroll
-                for (int u = 0; u < 6; ++u) {
-                    const int e = e0 + u * kThreads;
-                    v[u] = (e < kB * kB) ? __ldcg(rows + (int64_t)(e >> 6) * p.ld + g0.P[e & 63]) : 0.0;
-                }
-#pragma unroll
-                for (int u = 0; u < 6; ++u) {
-                    const int e = e0 + u * kThreads;
-                    if (e < kB * kB) sm.NL[e >> 6][e & 63] = -v[u];
-                }
+            for (int u = 0; u < kNLper; ++u) {
+                const int e = tid + u * kThreads;
+                nlv[u] = (e < kB * kB) ? __ldcg(rows + (int64_t)(e >> 6) * p.ld + g0.P[e & 63]) : 0.0;
             }
             const int nm = g0.n_moved;
             for (int e0 = tid; e0 < kB * nm; e0 += 4 * kThreads) {
@@ -631,75 +631,98 @@ __global__ void __launch_bounds__(kThreads, 1) kc_panel_kernel(const KPParams p0
                 for (int u = 0; u < 4; ++u)
                     if (at[u] >= 0) S[at[u]] = v[u];
             }
-            __syncthreads();
             KC_MARKH(half, 3);
             // S += NL * W0 on the FP64 tensor cores (mma.sync.m8n8k4.f64), k ascending (the trailing
-            // GEMM's arithmetic): warp w owns the 8-column tiles w, w + 12, ... two at a time for all
-            // 64 rows (one A fragment feeds both), W0 k-steps in a register ring; a missing second
-            // tile is skipped
+            // GEMM's arithmetic), in 4 passes of 16 k: warp w owns the 8-column tiles w, w + 12, ...
+            // two at a time for all 64 rows (one A fragment feeds both)
             const double* W0 = p.r1_W + lo;
             const int gq = lane >> 2, qq = lane & 3;
             const int ntiles = (wc + 7) >> 3;
             // (two copies of the loop body, with and without the second tile: a predicate around
             //  mma.sync makes the compiler bracket every DMMA with WARPSYNC)
-            auto tiles = [&](const int tp, auto two_c) {
-                constexpr bool two = decltype(two_c)::value;
-                constexpr int NT = two ? 2 : 1;
-                const int tl[2] = {tp, tp + kWarps};
-                double acc[8][NT][2];
+            // Rounds of 24 tiles (two per warp); inside a round the 4 k-block passes run with the
+            // accumulators in registers (the chunk's tiles are read and written once).  Three copies
+            // of the round body -- two tiles, one tile, no tile (barriers and staging only) -- since
+            // a predicate around mma.sync makes the compiler bracket every DMMA with WARPSYNC.
+            auto stage = [&](const int k0) {
+                __syncthreads();  // (the previous pass is done with the staging)
+                if (((tid & 63) >> 4) == (k0 >> 4)) {
 #pragma unroll
-                for (int i = 0; i < 8; ++i)
-#pragma unroll
-                    for (int t = 0; t < NT; ++t) {
-                        const int c = tl[t] * 8 + 2 * qq;
-                        const double* sp = S + (8 * i + gq) * cw + c;
-                        acc[i][t][0] = (c < wc) ? sp[0] : 0.0;
-                        acc[i][t][1] = (c + 1 < wc) ? sp[1] : 0.0;
+                    for (int u = 0; u < kNLper; ++u) {
+                        const int e = tid + u * kThreads;
+                        if (e < kB * kB) sm.NL[e >> 6][e & 15] = -nlv[u];
                     }
-                constexpr int kPF = 4;
-                double bq[kPF][NT];
+                }
+                __syncthreads();
+            };
+            auto round = [&](const int tp, auto nt_c) {
+                constexpr int NT = decltype(nt_c)::value;
+                if constexpr (NT == 0) {
+                    for (int k0 = 0; k0 < kB; k0 += 16) stage(k0);
+                } else {
+                    const int tl[2] = {tp, tp + kWarps};
+                    auto load_bq = [&](const int k0, double (&bv)[4][NT]) {
 #pragma unroll
-                for (int s4 = 0; s4 < kPF; ++s4)
-#pragma unroll
-                    for (int t = 0; t < NT; ++t) {
-                        const int c = tl[t] * 8 + gq;
-                        bq[s4][t] = (c < wc) ? __ldcg(W0 + (int64_t)(4 * s4 + qq) * p.r1_ldw + c) : 0.0;
-                    }
-                for (int k0 = 0; k0 < kB; k0 += 4 * kPF) {
-#pragma unroll
-                    for (int s4 = 0; s4 < kPF; ++s4) {
-                        const int k = k0 + 4 * s4;
-                        double av[8];
-#pragma unroll
-                        for (int i = 0; i < 8; ++i) av[i] = sm.NL[8 * i + gq][k + qq];
-#pragma unroll
-                        for (int i = 0; i < 8; ++i)
-#pragma unroll
-                            for (int t = 0; t < NT; ++t)
-                                asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-                                    : "+d"(acc[i][t][0]), "+d"(acc[i][t][1]) : "d"(av[i]), "d"(bq[s4][t]));
-                        if (k + 4 * kPF < kB) {
+                        for (int s4 = 0; s4 < 4; ++s4)
 #pragma unroll
                             for (int t = 0; t < NT; ++t) {
                                 const int c = tl[t] * 8 + gq;
-                                bq[s4][t] = (c < wc) ? __ldcg(W0 + (int64_t)(k + 4 * kPF + qq) * p.r1_ldw + c) : 0.0;
+                                bv[s4][t] = (c < wc) ? __ldcg(W0 + (int64_t)(k0 + 4 * s4 + qq) * p.r1_ldw + c) : 0.0;
                             }
+                    };
+                    double bq[4][NT];
+                    load_bq(0, bq);
+                    double acc[8][NT][2];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i)
+#pragma unroll
+                        for (int t = 0; t < NT; ++t) {
+                            const int c = tl[t] * 8 + 2 * qq;
+                            const double* sp = S + (8 * i + gq) * cw + c;
+                            acc[i][t][0] = (c < wc) ? sp[0] : 0.0;
+                            acc[i][t][1] = (c + 1 < wc) ? sp[1] : 0.0;
+                        }
+                    for (int k0 = 0; k0 < kB; k0 += 16) {
+                        stage(k0);
+                        double bn[4][NT];
+                        if (k0 + 16 < kB) load_bq(k0 + 16, bn);  // the next pass's W0 rows meanwhile
+#pragma unroll
+                        for (int s4 = 0; s4 < 4; ++s4) {
+                            double av[8];
+#pragma unroll
+                            for (int i = 0; i < 8; ++i) av[i] = sm.NL[8 * i + gq][4 * s4 + qq];
+#pragma unroll
+                            for (int i = 0; i < 8; ++i)
+#pragma unroll
+                                for (int t = 0; t < NT; ++t)
+                                    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                                        : "+d"(acc[i][t][0]), "+d"(acc[i][t][1]) : "d"(av[i]), "d"(bq[s4][t]));
+                        }
+                        if (k0 + 16 < kB) {
+#pragma unroll
+                            for (int s4 = 0; s4 < 4; ++s4)
+#pragma unroll
+                                for (int t = 0; t < NT; ++t) bq[s4][t] = bn[s4][t];
                         }
                     }
+#pragma unroll
+                    for (int i = 0; i < 8; ++i)
+#pragma unroll
+                        for (int t = 0; t < NT; ++t) {
+                            const int c = tl[t] * 8 + 2 * qq;
+                            double* const sp = S + (8 * i + gq) * cw + c;
+                            if (c < wc) sp[0] = acc[i][t][0];
+                            if (c + 1 < wc) sp[1] = acc[i][t][1];
+                        }
                 }
-#pragma unroll
-                for (int i = 0; i < 8; ++i)
-#pragma unroll
-                    for (int t = 0; t < NT; ++t) {
-                        const int c = tl[t] * 8 + 2 * qq;
-                        double* const sp = S + (8 * i + gq) * cw + c;
-                        if (c < wc) sp[0] = acc[i][t][0];
-                        if (c + 1 < wc) sp[1] = acc[i][t][1];
-                    }
             };
-            for (int tp = warp; tp < ntiles; tp += 2 * kWarps) {
-                if (tp + kWarps < ntiles) tiles(tp, std::true_type{});
-                else tiles(tp, std::false_type{});
+            __syncthreads();  // the moved columns are in the chunk
+            const int rounds = (ntiles + 2 * kWarps - 1) / (2 * kWarps);  // CTA-uniform
+            for (int rd = 0; rd < rounds; ++rd) {
+                const int tp = warp + rd * 2 * kWarps;
+                if (tp + kWarps < ntiles) round(tp, std::integral_constant<int, 2>{});
+                else if (tp < ntiles) round(tp, std::integral_constant<int, 1>{});
+                else round(tp, std::integral_constant<int, 0>{});
             }
             __syncthreads();
         }
@@ -1063,7 +1086,7 @@ int kc_plan(int64_t m, int* cw_out) {
 }
 
 // Largest cluster (16, 8, 4, 2; 0: none) the current device can co-schedule with the kernel's
-// largest footprint (352 columns per CTA), probed once per device: a device or partition without
+// largest footprint (400 columns per CTA), probed once per device: a device or partition without
 // 16 free SMs in one GPC takes smaller clusters, or the column-distributed kernel.
 int kc_max_cluster() {
     constexpr int kMaxDev = 64;

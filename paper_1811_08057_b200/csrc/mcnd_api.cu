@@ -60,7 +60,7 @@ long env_long(const char* name, long dflt) {
 }
 
 // One panel (second == nullptr) or both panels of a pair in one launch: the cluster-resident
-// kernel (k2_cpanel.cu) while the panel fits one thread-block cluster (active width <= 16 x 352
+// kernel (k2_cpanel.cu) while the panel fits one thread-block cluster (active width <= 16 x 400
 // columns), the column-distributed kernel (k2_panel.cu) above.  Test hooks: MCND_KC=0 keeps the
 // column-distributed kernel everywhere, MCND_KC_MAXM lowers the cluster kernel's range, MCND_KC_C
 // caps the cluster size.

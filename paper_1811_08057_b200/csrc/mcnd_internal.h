@@ -179,7 +179,7 @@ size_t kp_smem_bytes(int cw);
 // distributed shared memory in micro-panels of 8 rows.  Same parameters and outputs as kp_launch
 // (cand / wrec / lastbuf unused, colbuf is a small scratch).
 constexpr int kKCMaxC = 16;
-constexpr int kKCMaxCw = 352;  // 64 x 352 doubles = 176 KB dynamic + 48 KB static shared memory
+constexpr int kKCMaxCw = 400;  // 64 x 400 doubles = 200 KB dynamic + 24 KB static shared memory
 // cluster size for active width m and its chunk width; 0: m is outside the cluster kernel's range
 // on the current device (kc_max_cluster: the largest cluster it can co-schedule, probed once)
 int kc_plan(int64_t m, int* cw_out);

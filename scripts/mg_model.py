@@ -11,9 +11,9 @@ NVL = 770e9           # B/s, NVLink 5 peer bandwidth per direction (bulk, NCCL b
 NVL_LAT = 10e-6       # s, per NCCL broadcast (launch + protocol latency)
 PUSH_SM = 120e9       # B/s, remote stores from ONE SM (the unblocked pivot-row push)
 DGEMM = 25.6e12       # flop/s, the trailing GEMM as it runs beside the panels (C5 0.918 s)
-PIVOT = 3.3e-6        # s per pivot, column-distributed panel kernel (active widths above 5632)
+PIVOT = 3.3e-6        # s per pivot, column-distributed panel kernel (active widths above 6400)
 PIVOT_KC = 1.95e-6    # s per pivot, cluster panel kernel at m = 4000 (pair 250 us), 1.5 at m <= 1000
-KC_MAXM = 5632        # active widths the cluster panel kernel takes
+KC_MAXM = 6400        # active widths the cluster panel kernel takes
 PAIR_EXTRA = 40e-6    # s, per pair on the critical stream besides the panels (prologue, W, pair prep)
 CRIT_GAP = 75e-6      # s, per pair: join, gather + L correction, the next 128 rows' update, launch gaps (r2_k2_timeline_c3.txt)
 K1_STEP = 4.5e-6      # s, unblocked per-step chain (publish -> flag -> stage), C1 3.8 us + NVLink flag

@@ -359,7 +359,7 @@ GROUPS = [None, 0]
 
 
 # The panel factorisation has two kernels: the cluster-resident one (k2_cpanel.cu, active widths
-# <= 5632: every small-N test runs it by default) and the column-distributed one (k2_panel.cu,
+# <= 6400: every small-N test runs it by default) and the column-distributed one (k2_panel.cu,
 # above).  MCND_KC=0 keeps the column-distributed kernel at every size; MCND_KC_C caps the cluster
 # size (wider chunks: 2 or 3 columns per chain thread at small N).
 PANEL_KERNELS = [None, "column", "cluster2", "cluster4"]
