@@ -12,10 +12,10 @@ NVL_LAT = 10e-6       # s, per NCCL broadcast (launch + protocol latency)
 PUSH_SM = 120e9       # B/s, remote stores from ONE SM (the unblocked pivot-row push)
 DGEMM = 25.6e12       # flop/s, the trailing GEMM as it runs beside the panels (C5 0.918 s)
 PIVOT = 3.3e-6        # s per pivot, column-distributed panel kernel (active widths above 6400)
-PIVOT_KC = 1.95e-6    # s per pivot, cluster panel kernel at m = 4000 (pair 250 us), 1.5 at m <= 1000
+PIVOT_KC = 1.97e-6    # s per pivot, cluster panel kernel at m = 4000 (pair 252 us; 2.3 at m = 6400), 1.6 at m <= 1000
 KC_MAXM = 6400        # active widths the cluster panel kernel takes
 PAIR_EXTRA = 40e-6    # s, per pair on the critical stream besides the panels (prologue, W, pair prep)
-CRIT_GAP = 75e-6      # s, per pair: join, gather + L correction, the next 128 rows' update, launch gaps (r2_k2_timeline_c3.txt)
+CRIT_GAP = 80e-6      # s, per pair: join, gather + L correction, the next 128 rows' update, launch gaps (r2_k2_timeline_c3.txt)
 K1_STEP = 4.5e-6      # s, unblocked per-step chain (publish -> flag -> stage), C1 3.8 us + NVLink flag
 
 
@@ -26,7 +26,7 @@ def blocked(n, p, t1_meas=None):
     b = 64
     for k in range(0, n - 128, 2 * b):
         m = n - k
-        piv = PIVOT if m > KC_MAXM else (1.5e-6 + (PIVOT_KC - 1.5e-6) * max(0.0, (m - 1000) / 3000.0))
+        piv = PIVOT if m > KC_MAXM else (1.6e-6 + (PIVOT_KC - 1.6e-6) * max(0.0, (m - 1000) / 3000.0))
         t_chain += 2 * b * piv + (PAIR_EXTRA if m > KC_MAXM else 0.0) + CRIT_GAP
         if p > 1:
             t_bcast += NVL_LAT + 128 * m * 8 / NVL
