@@ -73,9 +73,15 @@ cudaError_t panel_launch(KPParams q0, cudaStream_t st, KPParams* q1) {
             C = (int)fc;
             cw = (int)(((q0.m + fc - 1) / fc + 31) / 32 * 32);
         }
-        q0.G = C; q0.cw = cw;
-        if (q1) { q1->G = C; q1->cw = cw; }
-        return kc_launch(q0, st, q1);
+        KPParams c0 = q0, c1 = q1 ? *q1 : q0;
+        c0.G = C; c0.cw = cw;
+        c1.G = C; c1.cw = cw;
+        const cudaError_t e = kc_launch(c0, st, q1 ? &c1 : nullptr);
+        // a cluster the device cannot place after all (the probe of kc_max_cluster is an estimate):
+        // nothing was launched, the column-distributed kernel takes the panel
+        if (e != cudaErrorLaunchOutOfResources && e != cudaErrorInvalidConfiguration && e != cudaErrorInvalidClusterSize)
+            return e;
+        (void)cudaGetLastError();
     }
     if (q0.cw > kKPMaxCw) return cudaErrorInvalidValue;
     return kp_launch(q0, st, q1);
